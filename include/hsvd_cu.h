@@ -1,0 +1,139 @@
+/*
+ * hsvd_cu.h -- C ABI of the B200-native hierarchical merge-and-truncate SVD.
+ *
+ * Drop-in boundary for the hot path of the reference library hsvd::core
+ * (/root/reference/proj/core).  The reference has no FFI; its boundary is the
+ * C++ API below, and each entry point here replaces one of those functions
+ * (same argument meaning, same error behaviour mapped to status codes):
+ *
+ *   hsvd_cu_hierarchical_svd     hsvd::hierarchical_svd      hierarchy.hpp:45, hierarchy.cpp:65-94
+ *   hsvd_cu_recover_left_vectors hsvd::recover_left_vectors  hierarchy.hpp:50, hierarchy.cpp:96-112
+ *   hsvd_cu_rank_k_svd           hierarchical_svd followed by recover_left_vectors
+ *                                (the pipeline of hsvd_main.cpp:132-143 / bench.cpp:109-113)
+ *   hsvd_cu_svd_of_col_slices    hsvd::svd_of_col_slices     hierarchy.hpp:39-40, hierarchy.cpp:50-63
+ *   hsvd_cu_tree_merge           hsvd::tree_merge            hierarchy.hpp:32-34, hierarchy.cpp:31-48
+ *   hsvd_cu_merge_pair           hsvd::merge_pair_qr /       merge.hpp:19-30, merge.cpp:42-117
+ *                                hsvd::merge_pair_naive
+ *   hsvd_cu_full_svd             hsvd::full_svd              kernels.hpp:26, kernels.cpp:21-48
+ *
+ * Matrices crossing the boundary use the reference's DenseMatrix layout:
+ * row-major, real64 (fp32 is accepted for the input matrix X), leading
+ * dimension in elements.  Results live in device memory owned by the context
+ * and are valid until the next call on the same context; the accessors copy
+ * them out (row-major) or expose the column-major device pointers.
+ *
+ * Every function returns HSVD_CU_OK or an error code; hsvd_cu_last_error()
+ * returns the thread-local message (HSVD_CU_EINVAL <-> std::invalid_argument,
+ * HSVD_CU_EDECOMP <-> hsvd::DecompositionError with rows/cols from
+ * hsvd_cu_last_error_dims()).  There is no CPU fallback: without a CUDA
+ * device every compute entry point fails with HSVD_CU_ECUDA.
+ */
+#ifndef HSVD_CU_H_
+#define HSVD_CU_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hsvd_cu_ctx hsvd_cu_ctx;
+typedef struct hsvd_cu_result hsvd_cu_result;
+
+enum {
+  HSVD_CU_OK = 0,
+  HSVD_CU_EINVAL = 1,
+  HSVD_CU_EDECOMP = 2,
+  HSVD_CU_ECUDA = 3,
+  HSVD_CU_ENCCL = 4,
+  HSVD_CU_ENOMEM = 5
+};
+enum { HSVD_CU_F32 = 0, HSVD_CU_F64 = 1 };
+enum { HSVD_CU_COLUMN_CONCAT = 0, HSVD_CU_ROW_CONCAT = 1 };
+enum { HSVD_CU_HOST = 0, HSVD_CU_DEVICE = 1 };
+
+/* hsvd::MatConfig (svd_factor.hpp:28-35); max_rank <= 0 means "no cap". */
+typedef struct {
+  double gamma;
+  int64_t row_block_rows;
+  int64_t col_block_cols;
+  double epsilon;
+  int32_t max_iters;
+  int64_t max_rank;
+} hsvd_cu_config;
+
+/* One side of an hsvd::SvdFactor (svd_factor.hpp:14-25): the carried basis
+ * (dim x rank, row-major, leading dimension ld, host memory) and sigma. */
+typedef struct {
+  const double* basis;
+  int64_t dim;
+  int64_t rank;
+  int64_t ld;
+  const double* sigma;
+  int32_t degenerate;
+} hsvd_cu_factor_in;
+
+int hsvd_cu_version(void);
+const char* hsvd_cu_last_error(void);
+void hsvd_cu_last_error_dims(int64_t* rows, int64_t* cols);
+
+int hsvd_cu_ctx_create(int device, hsvd_cu_ctx** out);
+int hsvd_cu_ctx_destroy(hsvd_cu_ctx* ctx);
+/* cudaStream_t the context launches on (for event timing by callers). */
+int hsvd_cu_ctx_stream(hsvd_cu_ctx* ctx, void** stream);
+/* Number of kernels this library has launched on the context. */
+int64_t hsvd_cu_launch_count(const hsvd_cu_ctx* ctx);
+/* Device bytes currently reserved by the context arena. */
+int64_t hsvd_cu_arena_bytes(const hsvd_cu_ctx* ctx);
+int hsvd_cu_synchronize(hsvd_cu_ctx* ctx);
+
+/* hsvd::validate (svd_factor.cpp:10-21). */
+int hsvd_cu_validate(const hsvd_cu_config* cfg);
+
+/* x: m x n row-major with leading dimension ldx, dtype HSVD_CU_F32/F64, in
+ * host (where = HSVD_CU_HOST) or device memory.  Result: (sigma, V), u absent. */
+int hsvd_cu_hierarchical_svd(hsvd_cu_ctx* ctx, const void* x, int dtype, int64_t m, int64_t n,
+                             int64_t ldx, int where, const hsvd_cu_config* cfg,
+                             hsvd_cu_result** out);
+
+/* v_r: n x r row-major (ldv), host or device.  Result: (U, sigma, V). */
+int hsvd_cu_recover_left_vectors(hsvd_cu_ctx* ctx, const void* x, int dtype, int64_t m, int64_t n,
+                                 int64_t ldx, int where, const double* v_r, int64_t r,
+                                 int64_t ldv, int v_where, hsvd_cu_result** out);
+
+/* hierarchical_svd + recover_left_vectors with V_r kept on the device. */
+int hsvd_cu_rank_k_svd(hsvd_cu_ctx* ctx, const void* x, int dtype, int64_t m, int64_t n,
+                       int64_t ldx, int where, const hsvd_cu_config* cfg, hsvd_cu_result** out);
+
+int hsvd_cu_svd_of_col_slices(hsvd_cu_ctx* ctx, const void* x, int dtype, int64_t m, int64_t n,
+                              int64_t ldx, int where, int64_t c, double gamma, int64_t max_rank,
+                              hsvd_cu_result** out);
+
+/* Result: (U, sigma, V) with p = min(rows, cols) (host row-major input). */
+int hsvd_cu_full_svd(hsvd_cu_ctx* ctx, const double* a, int64_t rows, int64_t cols, int64_t lda,
+                     hsvd_cu_result** out);
+
+/* orient: HSVD_CU_COLUMN_CONCAT (bases are U) or HSVD_CU_ROW_CONCAT (V). */
+int hsvd_cu_merge_pair(hsvd_cu_ctx* ctx, int orient, const hsvd_cu_factor_in* f1,
+                       const hsvd_cu_factor_in* f2, double gamma, int64_t max_rank,
+                       hsvd_cu_result** out);
+
+int hsvd_cu_tree_merge(hsvd_cu_ctx* ctx, int orient, const hsvd_cu_factor_in* factors,
+                       int64_t count, double gamma, int64_t max_rank, int64_t* pair_merges,
+                       hsvd_cu_result** out);
+
+/* Result accessors. */
+int hsvd_cu_result_info(const hsvd_cu_result* res, int64_t* rank, int32_t* has_u, int32_t* has_v,
+                        int64_t* u_rows, int64_t* v_rows, int32_t* degenerate);
+int hsvd_cu_result_sigma(const hsvd_cu_result* res, double* out);
+int hsvd_cu_result_u(const hsvd_cu_result* res, double* out); /* u_rows x rank, row-major */
+int hsvd_cu_result_v(const hsvd_cu_result* res, double* out); /* v_rows x rank, row-major */
+int hsvd_cu_result_device(const hsvd_cu_result* res, const double** sigma, const double** u,
+                          int64_t* ldu, const double** v, int64_t* ldv); /* column-major */
+void hsvd_cu_result_free(hsvd_cu_result* res);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HSVD_CU_H_ */

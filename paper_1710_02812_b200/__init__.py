@@ -1,0 +1,14 @@
+"""B200-native hierarchical merge-and-truncate SVD (arXiv 1710.02812).
+
+Drop-in for the hot path of the reference ``hsvd::core`` library:
+``hierarchical_svd`` followed by ``recover_left_vectors``, computed by
+hand-written sm_100a CUDA kernels in ``libhsvd_b200.so`` behind the C ABI in
+``include/hsvd_cu.h``.
+"""
+from .hsvd import (  # noqa: F401
+    COLUMN_CONCAT, ROW_CONCAT, BlockPlan, Context, DecompositionError, HsvdCudaError,
+    MatConfig, MergeStats, SvdFactor, default_context, full_svd, hierarchical_svd,
+    load_library, merge_pair_naive, merge_pair_qr, normalize_signs, partition,
+    rank_k_svd, reconstruct, recover_left_vectors, retained_count, svd_of_col_slices,
+    tree_merge, truncate_factor, validate, LIB_PATH, EXPORTED,
+)

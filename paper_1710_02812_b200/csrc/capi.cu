@@ -1,0 +1,436 @@
+// C ABI (include/hsvd_cu.h) over the device engine.
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "../../include/hsvd_cu.h"
+#include "engine.h"
+#include "factor_ops.h"
+
+using namespace hsvdcu;
+
+struct hsvd_cu_ctx {
+  Ctx c;
+  long long generation = 0;
+};
+
+struct hsvd_cu_result {
+  hsvd_cu_ctx* ctx = nullptr;
+  long long gen = 0;
+  int rank = 0;
+  bool degenerate = false;
+  const double* sigma = nullptr;
+  const double* u = nullptr;
+  long long ldu = 0, u_rows = 0;
+  const double* v = nullptr;
+  long long ldv = 0, v_rows = 0;
+};
+
+namespace {
+
+thread_local std::string g_err;
+thread_local long long g_err_rows = 0, g_err_cols = 0;
+
+int fail(int code, const std::string& msg, long long rows = 0, long long cols = 0) {
+  g_err = msg;
+  g_err_rows = rows;
+  g_err_cols = cols;
+  return code;
+}
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    g_err.clear();
+    return f();
+  } catch (const Error& e) {
+    return fail(e.code, e.what(), e.rows, e.cols);
+  } catch (const std::bad_alloc&) {
+    return fail(HSVD_CU_ENOMEM, "host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(HSVD_CU_EINVAL, e.what());
+  }
+}
+
+void begin(hsvd_cu_ctx* ctx) {
+  if (!ctx) throw Error(kInvalid, "null context");
+  HSVD_CUDA(cudaSetDevice(ctx->c.device));
+  ctx->c.arena.reset();
+  ++ctx->generation;
+}
+
+DType dtype_of(int dt) {
+  if (dt == HSVD_CU_F32) return DType::F32;
+  if (dt == HSVD_CU_F64) return DType::F64;
+  throw Error(kInvalid, "dtype must be HSVD_CU_F32 or HSVD_CU_F64");
+}
+
+// Brings x to the device (contiguous, ld = n) unless it already is there.
+XView stage_x(Ctx& c, const void* x, int dtype, int64_t m, int64_t n, int64_t ldx, int where) {
+  if (!x) throw Error(kInvalid, "x is null");
+  if (m <= 0 || n <= 0) throw Error(kInvalid, "matrix is empty");
+  if (ldx < n) throw Error(kInvalid, "ldx < n");
+  if (m > 0x7fffffffLL || n > 0x7fffffffLL) throw Error(kInvalid, "dimension exceeds 2^31-1");
+  XView v{x, dtype_of(dtype), ldx, m, n};
+  if (where == HSVD_CU_DEVICE) return v;
+  const size_t es = v.dt == DType::F32 ? 4 : 8;
+  void* d = c.arena.alloc((size_t)m * n * es);
+  HSVD_CUDA(cudaMemcpy2DAsync(d, n * es, x, ldx * es, n * es, m, cudaMemcpyHostToDevice, c.stream));
+  v.X = d;
+  v.ld = n;
+  return v;
+}
+
+// Row-major host/device fp64 (rows x cols, ld) -> column-major device.
+double* stage_rowmajor(Ctx& c, const double* a, int64_t rows, int64_t cols, int64_t ld, int where) {
+  double* raw;
+  if (where == HSVD_CU_DEVICE) {
+    raw = const_cast<double*>(a);
+  } else {
+    raw = c.arena.alloc_n<double>((size_t)rows * cols);
+    HSVD_CUDA(cudaMemcpy2DAsync(raw, cols * 8, a, ld * 8, cols * 8, rows, cudaMemcpyHostToDevice,
+                                c.stream));
+    ld = cols;
+  }
+  double* colm = c.arena.alloc_n<double>((size_t)rows * cols);
+  rowmajor_to_colmajor(c, raw, ld, (int)rows, (int)cols, colm, rows);
+  return colm;
+}
+
+hsvd_cu_result* make_result(hsvd_cu_ctx* ctx, const DFac& f, bool b_is_u, bool with_b2) {
+  auto* r = new hsvd_cu_result();
+  r->ctx = ctx;
+  r->gen = ctx->generation;
+  r->rank = f.rank;
+  r->degenerate = f.degenerate;
+  r->sigma = f.sigma;
+  if (b_is_u) {
+    r->u = f.B;
+    r->ldu = f.ld;
+    r->u_rows = f.dim;
+    if (with_b2) {
+      r->v = f.B2;
+      r->ldv = f.ld2;
+      r->v_rows = f.dim2;
+    }
+  } else {
+    r->v = f.B;
+    r->ldv = f.ld;
+    r->v_rows = f.dim;
+    if (with_b2) {
+      r->u = f.B2;
+      r->ldu = f.ld2;
+      r->u_rows = f.dim2;
+    }
+  }
+  return r;
+}
+
+void check_cfg(const hsvd_cu_config* cfg) {
+  if (!cfg) throw Error(kInvalid, "MatConfig is null");
+  if (cfg->gamma < 0.0 || !std::isfinite(cfg->gamma))
+    throw Error(kInvalid, "MatConfig: gamma must be finite and >= 0");
+  if (!(cfg->epsilon > 0.0)) throw Error(kInvalid, "MatConfig: epsilon must be > 0");
+  if (cfg->max_iters < 1) throw Error(kInvalid, "MatConfig: max_iters must be >= 1");
+  if (cfg->row_block_rows < 0 || cfg->col_block_cols < 0)
+    throw Error(kInvalid, "MatConfig: block sizes must be >= 0");
+  if (cfg->max_rank < 0) throw Error(kInvalid, "MatConfig: max_rank must be >= 1");
+}
+
+HsvdConfig to_cfg(const hsvd_cu_config* cfg) {
+  HsvdConfig h;
+  h.gamma = cfg->gamma;
+  h.d = cfg->row_block_rows;
+  h.c = cfg->col_block_cols;
+  h.cap = cfg->max_rank > 0 ? (int)std::min<int64_t>(cfg->max_rank, 0x7fffffff) : 0;
+  return h;
+}
+
+int cap_of(int64_t max_rank) { return max_rank > 0 ? (int)std::min<int64_t>(max_rank, 0x7fffffff) : 0; }
+
+DFac stage_factor(Ctx& c, const hsvd_cu_factor_in& f) {
+  if (!f.basis || !f.sigma) throw Error(kInvalid, "merge: factor requires a carried basis");
+  if (f.rank < 1 || f.dim < 1) throw Error(kInvalid, "merge: factor is empty");
+  DFac d;
+  d.dim = (int)f.dim;
+  d.rank = (int)f.rank;
+  d.ld = f.dim;
+  d.B = stage_rowmajor(c, f.basis, f.dim, f.rank, f.ld > 0 ? f.ld : f.rank, HSVD_CU_HOST);
+  d.sigma = c.arena.alloc_n<double>(f.rank);
+  HSVD_CUDA(cudaMemcpyAsync(d.sigma, f.sigma, f.rank * sizeof(double), cudaMemcpyHostToDevice,
+                            c.stream));
+  d.degenerate = f.degenerate != 0;
+  return d;
+}
+
+int check_result(const hsvd_cu_result* r) {
+  if (!r) return fail(HSVD_CU_EINVAL, "null result");
+  if (!r->ctx || r->ctx->generation != r->gen)
+    return fail(HSVD_CU_EINVAL, "stale result: the context has run another call since");
+  return HSVD_CU_OK;
+}
+
+int copy_side(const hsvd_cu_result* r, const double* src, long long ld, long long rows, double* out) {
+  if (int s = check_result(r)) return s;
+  if (!src) return fail(HSVD_CU_EINVAL, "result has no such factor");
+  return guarded([&] {
+    Ctx& c = r->ctx->c;
+    HSVD_CUDA(cudaSetDevice(c.device));
+    Arena::Mark mk = c.arena.mark();
+    double* tmp = c.arena.alloc_n<double>((size_t)rows * r->rank);
+    colmajor_to_rowmajor(c, src, ld, (int)rows, r->rank, tmp, r->rank);
+    HSVD_CUDA(cudaMemcpyAsync(out, tmp, (size_t)rows * r->rank * 8, cudaMemcpyDeviceToHost, c.stream));
+    HSVD_CUDA(cudaStreamSynchronize(c.stream));
+    c.arena.release(mk);
+    return HSVD_CU_OK;
+  });
+}
+
+}  // namespace
+
+extern "C" {
+
+int hsvd_cu_version(void) { return 100; }
+const char* hsvd_cu_last_error(void) { return g_err.c_str(); }
+void hsvd_cu_last_error_dims(int64_t* rows, int64_t* cols) {
+  if (rows) *rows = g_err_rows;
+  if (cols) *cols = g_err_cols;
+}
+
+int hsvd_cu_ctx_create(int device, hsvd_cu_ctx** out) {
+  if (!out) return fail(HSVD_CU_EINVAL, "out is null");
+  *out = nullptr;
+  return guarded([&] {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) {
+      (void)cudaGetLastError();
+      throw Error(kCuda, "no CUDA device available (this library has no CPU fallback)");
+    }
+    if (device < 0 || device >= n) throw Error(kInvalid, "device index out of range");
+    auto* c = new hsvd_cu_ctx();
+    try {
+      c->c.device = device;
+      HSVD_CUDA(cudaSetDevice(device));
+      cudaDeviceProp prop;
+      HSVD_CUDA(cudaGetDeviceProperties(&prop, device));
+      if (prop.major < 10)
+        throw Error(kCuda, std::string("device ") + prop.name + " is not sm_100 (Blackwell)");
+      c->c.num_sms = prop.multiProcessorCount;
+      HSVD_CUDA(cudaStreamCreateWithFlags(&c->c.stream, cudaStreamNonBlocking));
+      c->c.own_stream = true;
+      c->c.staging.init(size_t(8) << 20);
+    } catch (...) {
+      delete c;
+      throw;
+    }
+    *out = c;
+    return HSVD_CU_OK;
+  });
+}
+
+int hsvd_cu_ctx_destroy(hsvd_cu_ctx* ctx) {
+  if (!ctx) return HSVD_CU_OK;
+  cudaSetDevice(ctx->c.device);
+  cudaStreamSynchronize(ctx->c.stream);
+  if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.stream);
+  delete ctx;
+  return HSVD_CU_OK;
+}
+
+int hsvd_cu_ctx_stream(hsvd_cu_ctx* ctx, void** stream) {
+  if (!ctx || !stream) return fail(HSVD_CU_EINVAL, "null argument");
+  *stream = ctx->c.stream;
+  return HSVD_CU_OK;
+}
+
+int64_t hsvd_cu_launch_count(const hsvd_cu_ctx* ctx) { return ctx ? ctx->c.launches : 0; }
+int64_t hsvd_cu_arena_bytes(const hsvd_cu_ctx* ctx) {
+  return ctx ? (int64_t)ctx->c.arena.capacity() : 0;
+}
+
+int hsvd_cu_synchronize(hsvd_cu_ctx* ctx) {
+  return guarded([&] {
+    if (!ctx) throw Error(kInvalid, "null context");
+    HSVD_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    return HSVD_CU_OK;
+  });
+}
+
+int hsvd_cu_validate(const hsvd_cu_config* cfg) {
+  return guarded([&] {
+    check_cfg(cfg);
+    return HSVD_CU_OK;
+  });
+}
+
+int hsvd_cu_hierarchical_svd(hsvd_cu_ctx* ctx, const void* x, int dtype, int64_t m, int64_t n,
+                             int64_t ldx, int where, const hsvd_cu_config* cfg,
+                             hsvd_cu_result** out) {
+  return guarded([&] {
+    if (!out) throw Error(kInvalid, "out is null");
+    *out = nullptr;
+    if (!x || m <= 0 || n <= 0) throw Error(kInvalid, "hierarchical_svd: matrix is empty");
+    check_cfg(cfg);
+    begin(ctx);
+    XView xv = stage_x(ctx->c, x, dtype, m, n, ldx, where);
+    DFac f = hierarchical_svd(ctx->c, xv, to_cfg(cfg));
+    *out = make_result(ctx, f, false, false);
+    return HSVD_CU_OK;
+  });
+}
+
+int hsvd_cu_recover_left_vectors(hsvd_cu_ctx* ctx, const void* x, int dtype, int64_t m, int64_t n,
+                                 int64_t ldx, int where, const double* v_r, int64_t r,
+                                 int64_t ldv, int v_where, hsvd_cu_result** out) {
+  return guarded([&] {
+    if (!out) throw Error(kInvalid, "out is null");
+    *out = nullptr;
+    if (!v_r || r < 1) throw Error(kInvalid, "recover_left_vectors: v_r must have x.cols() rows");
+    begin(ctx);
+    XView xv = stage_x(ctx->c, x, dtype, m, n, ldx, where);
+    double* vd = stage_rowmajor(ctx->c, v_r, n, r, ldv > 0 ? ldv : r, v_where);
+    DFac f = recover_left_vectors(ctx->c, xv, vd, n, (int)r);
+    *out = make_result(ctx, f, true, true);
+    return HSVD_CU_OK;
+  });
+}
+
+int hsvd_cu_rank_k_svd(hsvd_cu_ctx* ctx, const void* x, int dtype, int64_t m, int64_t n,
+                       int64_t ldx, int where, const hsvd_cu_config* cfg, hsvd_cu_result** out) {
+  return guarded([&] {
+    if (!out) throw Error(kInvalid, "out is null");
+    *out = nullptr;
+    if (!x || m <= 0 || n <= 0) throw Error(kInvalid, "hierarchical_svd: matrix is empty");
+    check_cfg(cfg);
+    begin(ctx);
+    XView xv = stage_x(ctx->c, x, dtype, m, n, ldx, where);
+    DFac right = hierarchical_svd(ctx->c, xv, to_cfg(cfg));
+    DFac f = recover_left_vectors(ctx->c, xv, right.B, right.ld, right.rank);
+    *out = make_result(ctx, f, true, true);
+    return HSVD_CU_OK;
+  });
+}
+
+int hsvd_cu_svd_of_col_slices(hsvd_cu_ctx* ctx, const void* x, int dtype, int64_t m, int64_t n,
+                              int64_t ldx, int where, int64_t c, double gamma, int64_t max_rank,
+                              hsvd_cu_result** out) {
+  return guarded([&] {
+    if (!out) throw Error(kInvalid, "out is null");
+    *out = nullptr;
+    begin(ctx);
+    XView xv = stage_x(ctx->c, x, dtype, m, n, ldx, where);
+    DFac f = svd_of_col_slices(ctx->c, xv, c, gamma, cap_of(max_rank));
+    *out = make_result(ctx, f, true, false);
+    return HSVD_CU_OK;
+  });
+}
+
+int hsvd_cu_full_svd(hsvd_cu_ctx* ctx, const double* a, int64_t rows, int64_t cols, int64_t lda,
+                     hsvd_cu_result** out) {
+  return guarded([&] {
+    if (!out) throw Error(kInvalid, "out is null");
+    *out = nullptr;
+    if (!a || rows <= 0 || cols <= 0) throw Error(kInvalid, "full_svd: matrix is empty");
+    begin(ctx);
+    XView xv = stage_x(ctx->c, a, HSVD_CU_F64, rows, cols, lda > 0 ? lda : cols, HSVD_CU_HOST);
+    std::vector<DFac> f =
+        block_svd_batch(ctx->c, xv, {{0, (int)rows, 0, (int)cols}}, 0.0, 0, true, true);
+    // full_svd keeps every singular value (no truncation)
+    int p = (int)std::min(rows, cols);
+    f[0].rank = p;
+    *out = make_result(ctx, f[0], true, true);
+    return HSVD_CU_OK;
+  });
+}
+
+int hsvd_cu_merge_pair(hsvd_cu_ctx* ctx, int orient, const hsvd_cu_factor_in* f1,
+                       const hsvd_cu_factor_in* f2, double gamma, int64_t max_rank,
+                       hsvd_cu_result** out) {
+  return guarded([&] {
+    if (!out) throw Error(kInvalid, "out is null");
+    *out = nullptr;
+    if (!f1 || !f2) throw Error(kInvalid, "merge: null factor");
+    if (f1->dim != f2->dim)
+      throw Error(kInvalid, orient == HSVD_CU_COLUMN_CONCAT
+                                ? "merge: ColumnConcat factors must have equal row counts"
+                                : "merge: RowConcat factors must have equal column counts");
+    begin(ctx);
+    DFac a = stage_factor(ctx->c, *f1), b = stage_factor(ctx->c, *f2);
+    std::vector<DFac> r = merge_batch(ctx->c, {{a, b}}, gamma, cap_of(max_rank));
+    *out = make_result(ctx, r[0], orient == HSVD_CU_COLUMN_CONCAT, false);
+    return HSVD_CU_OK;
+  });
+}
+
+int hsvd_cu_tree_merge(hsvd_cu_ctx* ctx, int orient, const hsvd_cu_factor_in* factors,
+                       int64_t count, double gamma, int64_t max_rank, int64_t* pair_merges,
+                       hsvd_cu_result** out) {
+  return guarded([&] {
+    if (!out) throw Error(kInvalid, "out is null");
+    *out = nullptr;
+    if (!factors || count < 1) throw Error(kInvalid, "tree_merge: factor list is empty");
+    for (int64_t i = 1; i < count; ++i)
+      if (factors[i].dim != factors[0].dim)
+        throw Error(kInvalid, orient == HSVD_CU_COLUMN_CONCAT
+                                  ? "merge: ColumnConcat factors must have equal row counts"
+                                  : "merge: RowConcat factors must have equal column counts");
+    begin(ctx);
+    std::vector<DFac> fs;
+    for (int64_t i = 0; i < count; ++i) fs.push_back(stage_factor(ctx->c, factors[i]));
+    long long pm = 0;
+    DFac f = tree_merge_many(ctx->c, {fs}, gamma, cap_of(max_rank), &pm).front();
+    if (pair_merges) *pair_merges = pm;
+    *out = make_result(ctx, f, orient == HSVD_CU_COLUMN_CONCAT, false);
+    return HSVD_CU_OK;
+  });
+}
+
+int hsvd_cu_result_info(const hsvd_cu_result* r, int64_t* rank, int32_t* has_u, int32_t* has_v,
+                        int64_t* u_rows, int64_t* v_rows, int32_t* degenerate) {
+  if (int s = check_result(r)) return s;
+  if (rank) *rank = r->rank;
+  if (has_u) *has_u = r->u != nullptr;
+  if (has_v) *has_v = r->v != nullptr;
+  if (u_rows) *u_rows = r->u_rows;
+  if (v_rows) *v_rows = r->v_rows;
+  if (degenerate) *degenerate = r->degenerate;
+  return HSVD_CU_OK;
+}
+
+int hsvd_cu_result_sigma(const hsvd_cu_result* r, double* out) {
+  if (int s = check_result(r)) return s;
+  return guarded([&] {
+    Ctx& c = r->ctx->c;
+    HSVD_CUDA(cudaSetDevice(c.device));
+    HSVD_CUDA(cudaMemcpyAsync(out, r->sigma, r->rank * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    HSVD_CUDA(cudaStreamSynchronize(c.stream));
+    return HSVD_CU_OK;
+  });
+}
+
+int hsvd_cu_result_u(const hsvd_cu_result* r, double* out) {
+  if (!r) return fail(HSVD_CU_EINVAL, "null result");
+  return copy_side(r, r->u, r->ldu, r->u_rows, out);
+}
+
+int hsvd_cu_result_v(const hsvd_cu_result* r, double* out) {
+  if (!r) return fail(HSVD_CU_EINVAL, "null result");
+  return copy_side(r, r->v, r->ldv, r->v_rows, out);
+}
+
+int hsvd_cu_result_device(const hsvd_cu_result* r, const double** sigma, const double** u,
+                          int64_t* ldu, const double** v, int64_t* ldv) {
+  if (int s = check_result(r)) return s;
+  if (sigma) *sigma = r->sigma;
+  if (u) *u = r->u;
+  if (ldu) *ldu = r->ldu;
+  if (v) *v = r->v;
+  if (ldv) *ldv = r->ldv;
+  return HSVD_CU_OK;
+}
+
+void hsvd_cu_result_free(hsvd_cu_result* r) { delete r; }
+
+}  // extern "C"

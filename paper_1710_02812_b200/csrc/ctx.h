@@ -1,0 +1,179 @@
+// Per-device execution context: stream, device arena, pinned staging ring,
+// launch accounting.  Host-side only.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace hsvdcu {
+
+// Stream-ordered bump allocator over cudaMalloc'd chunks.  Everything on the
+// context's single stream, so memory released with release(mark) may be
+// reused by later launches without a sync.
+class Arena {
+ public:
+  struct Mark {
+    size_t chunk;
+    size_t off;
+  };
+  ~Arena() { free_all(); }
+  void* alloc(size_t bytes) {
+    bytes = (bytes + 255) & ~size_t(255);
+    if (bytes == 0) bytes = 256;
+    while (cur_ < chunks_.size()) {
+      Chunk& c = chunks_[cur_];
+      if (off_ + bytes <= c.size) {
+        void* p = static_cast<char*>(c.ptr) + off_;
+        off_ += bytes;
+        peak_ = peak_ > used() ? peak_ : used();
+        return p;
+      }
+      ++cur_;
+      off_ = 0;
+    }
+    size_t want = chunks_.empty() ? (size_t(256) << 20) : chunks_.back().size * 2;
+    if (want < bytes) want = bytes;
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e != cudaSuccess) {
+      (void)cudaGetLastError();
+      want = bytes;
+      e = cudaMalloc(&p, want);
+      if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        throw Error(kNoMemory, "device arena: cudaMalloc of " + std::to_string(want) +
+                                   " bytes failed: " + cudaGetErrorString(e));
+      }
+    }
+    chunks_.push_back({p, want});
+    cur_ = chunks_.size() - 1;
+    off_ = bytes;
+    peak_ = peak_ > used() ? peak_ : used();
+    return p;
+  }
+  template <typename T>
+  T* alloc_n(size_t n) { return static_cast<T*>(alloc(n * sizeof(T))); }
+  Mark mark() const { return {cur_, off_}; }
+  void release(Mark m) {
+    cur_ = m.chunk;
+    off_ = m.off;
+  }
+  void reset() {
+    cur_ = 0;
+    off_ = 0;
+  }
+  size_t used() const {
+    size_t u = off_;
+    for (size_t i = 0; i < cur_ && i < chunks_.size(); ++i) u += chunks_[i].size;
+    return u;
+  }
+  size_t capacity() const {
+    size_t u = 0;
+    for (auto& c : chunks_) u += c.size;
+    return u;
+  }
+  void free_all() {
+    for (auto& c : chunks_) cudaFree(c.ptr);
+    chunks_.clear();
+    cur_ = off_ = 0;
+  }
+
+ private:
+  struct Chunk {
+    void* ptr;
+    size_t size;
+  };
+  std::vector<Chunk> chunks_;
+  size_t cur_ = 0, off_ = 0, peak_ = 0;
+};
+
+// Pinned host ring mirrored on the device: small descriptor arrays are
+// written on the host and copied with one cudaMemcpyAsync per launch.
+class Staging {
+ public:
+  void init(size_t bytes) {
+    size_ = bytes;
+    HSVD_CUDA(cudaMallocHost(&host_, bytes));
+    HSVD_CUDA(cudaMalloc(&dev_, bytes));
+  }
+  ~Staging() {
+    if (host_) cudaFreeHost(host_);
+    if (dev_) cudaFree(dev_);
+  }
+  // Copies `bytes` from src into the ring and returns the device address.
+  void* put(const void* src, size_t bytes, cudaStream_t s) {
+    size_t b = (bytes + 255) & ~size_t(255);
+    if (b > size_) throw Error(kInvalid, "staging ring too small");
+    if (off_ + b > size_) {
+      HSVD_CUDA(cudaStreamSynchronize(s));  // all earlier copies consumed
+      off_ = 0;
+    }
+    char* h = static_cast<char*>(host_) + off_;
+    char* d = static_cast<char*>(dev_) + off_;
+    std::memcpy(h, src, bytes);
+    HSVD_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s));
+    off_ += b;
+    return d;
+  }
+
+ private:
+  void* host_ = nullptr;
+  void* dev_ = nullptr;
+  size_t size_ = 0, off_ = 0;
+};
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  Arena arena;
+  Staging staging;
+  long long launches = 0;  // kernels launched by this library on this context
+  int* d_flags = nullptr;  // device status word (bit0: non-finite seen)
+  int num_sms = 148;
+  // multi-GPU (optional)
+  void* nccl_comm = nullptr;
+  int rank = 0, world = 1;
+
+  int* h_ints = nullptr;  // pinned readback buffer
+  size_t h_ints_cap = 0;
+  double* h_dbl = nullptr;
+  size_t h_dbl_cap = 0;
+
+  int* pinned_ints(size_t n) {
+    if (n > h_ints_cap) {
+      if (h_ints) cudaFreeHost(h_ints);
+      h_ints_cap = n < 1024 ? 1024 : n;
+      HSVD_CUDA(cudaMallocHost(&h_ints, h_ints_cap * sizeof(int)));
+    }
+    return h_ints;
+  }
+  double* pinned_dbl(size_t n) {
+    if (n > h_dbl_cap) {
+      if (h_dbl) cudaFreeHost(h_dbl);
+      h_dbl_cap = n < 1024 ? 1024 : n;
+      HSVD_CUDA(cudaMallocHost(&h_dbl, h_dbl_cap * sizeof(double)));
+    }
+    return h_dbl;
+  }
+  ~Ctx() {
+    if (h_ints) cudaFreeHost(h_ints);
+    if (h_dbl) cudaFreeHost(h_dbl);
+  }
+
+  void count(int n = 1) { launches += n; }
+  void check_launch(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw Error(kCuda, std::string(what) + ": " + cudaGetErrorString(e));
+    count();
+  }
+};
+
+}  // namespace hsvdcu

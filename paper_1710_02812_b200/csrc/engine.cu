@@ -1,0 +1,419 @@
+// Host orchestration of Algorithm 1 (hierarchical merge-and-truncate SVD) on
+// device-resident data.  Mirrors /root/reference/proj/core/src/hierarchy.cpp
+// and merge.cpp; every dense step is one batched launch across all blocks /
+// pairs / row slices of a tree level.
+#include <algorithm>
+#include <cstring>
+#include <string>
+
+#include "engine.h"
+#include "factor_ops.h"
+#include "syev.h"
+
+namespace hsvdcu {
+
+namespace {
+
+size_t esize(DType t) { return t == DType::F32 ? 4 : 8; }
+
+const void* xptr(const XView& x, long long r0, long long c0) {
+  return static_cast<const char*>(x.X) + (r0 * x.ld + c0) * (long long)esize(x.dt);
+}
+
+void check_decomp(const std::vector<int>& deg, const std::vector<std::pair<long long, long long>>& dims,
+                  const std::string& prefix) {
+  for (size_t i = 0; i < deg.size(); ++i)
+    if (deg[i] == 2)
+      throw Error(kDecomposition,
+                  prefix + "SVD did not converge for a " + std::to_string(dims[i].first) + "x" +
+                      std::to_string(dims[i].second) + " matrix",
+                  dims[i].first, dims[i].second);
+}
+
+}  // namespace
+
+std::vector<Slice> partition(long long extent, long long block) {
+  if (block < 1 || block > extent) block = extent;
+  std::vector<Slice> out;
+  for (long long s = 0; s < extent; s += block) out.push_back({s, std::min(block, extent - s)});
+  return out;
+}
+
+void fetch_ranks(Ctx& ctx, const int* d_ranks, int count, std::vector<int>& out) {
+  out.assign(count, 0);
+  if (count == 0) return;
+  int* h = ctx.pinned_ints(count);
+  HSVD_CUDA(cudaMemcpyAsync(h, d_ranks, count * sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+  HSVD_CUDA(cudaStreamSynchronize(ctx.stream));
+  std::memcpy(out.data(), h, count * sizeof(int));
+}
+
+// ---------------------------------------------------------------------------
+// block SVD (leaves): Gram of the smaller side + top-k eigenpairs + projection
+// ---------------------------------------------------------------------------
+std::vector<DFac> block_svd_batch(Ctx& ctx, const XView& x, const std::vector<Block>& blocks,
+                                  double gamma, int cap, bool keep_both, bool write_all) {
+  const int nb = static_cast<int>(blocks.size());
+  std::vector<DFac> out(nb);
+  if (nb == 0) return out;
+  struct Tmp {
+    bool tall;
+    int q, kk, s;
+    double *G, *lam, *Z, *P, *Bp, *sig;
+    int* perm;
+  };
+  std::vector<Tmp> t(nb);
+  std::vector<GemmDesc> gram_t, gram_w, proj_t, proj_w;
+  std::vector<EigJob> ej;
+  int* d_rd = ctx.arena.alloc_n<int>(2 * (size_t)nb);
+  for (int b = 0; b < nb; ++b) {
+    const Block& bl = blocks[b];
+    Tmp& m = t[b];
+    m.tall = bl.d >= bl.c;
+    m.q = m.tall ? bl.c : bl.d;
+    const int p = std::min(bl.d, bl.c);
+    m.kk = cap > 0 ? std::min(cap, p) : p;
+    m.s = m.tall ? bl.d : bl.c;
+    m.G = ctx.arena.alloc_n<double>((size_t)m.q * m.q);
+    m.lam = ctx.arena.alloc_n<double>(m.kk);
+    m.Z = ctx.arena.alloc_n<double>((size_t)m.q * m.kk);
+    m.P = ctx.arena.alloc_n<double>((size_t)m.s * m.kk);
+    m.Bp = ctx.arena.alloc_n<double>((size_t)m.s * m.kk);
+    m.sig = ctx.arena.alloc_n<double>(m.kk);
+    m.perm = ctx.arena.alloc_n<int>(m.kk);
+    const void* base = xptr(x, bl.r0, bl.c0);
+    // column-major view of the row-major block: Xt (c x d, ld = x.ld)
+    if (m.tall)  // G = X_b^T X_b = Xt Xt^T
+      gram_t.push_back({base, base, m.G, x.ld, x.ld, m.q, m.q, m.q, bl.d, 1.0, 0.0});
+    else  // G = X_b X_b^T = Xt^T Xt
+      gram_w.push_back({base, base, m.G, x.ld, x.ld, m.q, m.q, m.q, bl.c, 1.0, 0.0});
+    ej.push_back({m.G, m.q, m.q, m.kk, m.lam, m.Z, m.q});
+    if (m.tall)  // P = X_b Z = Xt^T Z  (d x kk)
+      proj_t.push_back({base, m.Z, m.P, x.ld, m.q, m.s, bl.d, m.kk, bl.c, 1.0, 0.0});
+    else  // P = X_b^T Z = Xt Z  (c x kk)
+      proj_w.push_back({base, m.Z, m.P, x.ld, m.q, m.s, bl.c, m.kk, bl.d, 1.0, 0.0});
+  }
+  gemm_grouped(ctx, x.dt, x.dt, false, true, true, gram_t);
+  gemm_grouped(ctx, x.dt, x.dt, true, false, true, gram_w);
+  eig_topk(ctx, ej);
+  gemm_grouped(ctx, x.dt, DType::F64, true, false, false, proj_t);
+  gemm_grouped(ctx, x.dt, DType::F64, false, false, false, proj_w);
+  std::vector<FinJob> fj;
+  for (int b = 0; b < nb; ++b) {
+    Tmp& m = t[b];
+    fj.push_back({m.P, m.s, m.s, m.kk, gamma, cap, m.Bp, m.s, m.sig, m.perm, d_rd + b,
+                  d_rd + nb + b, (write_all || !m.tall || keep_both) ? 1 : 0});
+  }
+  finalize(ctx, fj);
+  // the eigenvector side, permuted to the sigma order
+  std::vector<GatherJob> gj;
+  std::vector<double*> zside(nb, nullptr);
+  for (int b = 0; b < nb; ++b) {
+    Tmp& m = t[b];
+    if (!m.tall || keep_both) {
+      zside[b] = ctx.arena.alloc_n<double>((size_t)m.q * m.kk);
+      gj.push_back({zside[b], m.q, m.Z, m.q, m.q, m.kk, m.perm});
+    }
+  }
+  gather_cols(ctx, gj);
+  std::vector<int> rd;
+  fetch_ranks(ctx, d_rd, 2 * nb, rd);
+  std::vector<int> deg(rd.begin() + nb, rd.end());
+  std::vector<std::pair<long long, long long>> dims;
+  for (auto& bl : blocks) dims.push_back({bl.d, bl.c});
+  check_decomp(deg, dims, "");
+  for (int b = 0; b < nb; ++b) {
+    Tmp& m = t[b];
+    DFac& f = out[b];
+    f.rank = rd[b];
+    f.degenerate = deg[b] == 1;
+    f.sigma = m.sig;
+    if (m.tall) {
+      f.B = m.Bp;
+      f.ld = m.s;
+      f.dim = blocks[b].d;
+      if (keep_both) {
+        f.B2 = zside[b];
+        f.ld2 = m.q;
+        f.dim2 = blocks[b].c;
+      }
+    } else {
+      f.B = zside[b];
+      f.ld = m.q;
+      f.dim = blocks[b].d;
+      if (keep_both) {
+        f.B2 = m.Bp;
+        f.ld2 = m.s;
+        f.dim2 = blocks[b].c;
+      }
+    }
+  }
+  return out;
+}
+
+// ---------------------------------------------------------------------------
+// merge (Gram form of merge_pair_qr / merge_pair_naive)
+// ---------------------------------------------------------------------------
+std::vector<DFac> merge_batch(Ctx& ctx, const std::vector<std::pair<DFac, DFac>>& pairs,
+                              double gamma, int cap) {
+  const int np = static_cast<int>(pairs.size());
+  std::vector<DFac> out(np);
+  if (np == 0) return out;
+  struct Tmp {
+    int s, k1, k2, q, kk;
+    double *G, *w, *lam, *Z, *Zh, *P, *Bn, *sig;
+  };
+  std::vector<Tmp> t(np);
+  std::vector<GemmDesc> gsy, gx, p1, p2;
+  std::vector<EigJob> ej;
+  std::vector<ScaleSymJob> ss;
+  std::vector<ScaleRowsJob> sr;
+  int* d_rd = ctx.arena.alloc_n<int>(2 * (size_t)np);
+  for (int i = 0; i < np; ++i) {
+    const DFac& a = pairs[i].first;
+    const DFac& b = pairs[i].second;
+    if (a.dim != b.dim) throw Error(kInvalid, "merge: factors must share the basis dimension");
+    Tmp& m = t[i];
+    m.s = a.dim;
+    m.k1 = a.rank;
+    m.k2 = b.rank;
+    m.q = m.k1 + m.k2;
+    m.kk = std::min(m.q, m.s);
+    if (cap > 0) m.kk = std::min(m.kk, cap);
+    m.G = ctx.arena.alloc_n<double>((size_t)m.q * m.q);
+    m.w = ctx.arena.alloc_n<double>(m.q);
+    m.lam = ctx.arena.alloc_n<double>(m.kk);
+    m.Z = ctx.arena.alloc_n<double>((size_t)m.q * m.kk);
+    m.Zh = ctx.arena.alloc_n<double>((size_t)m.q * m.kk);
+    m.P = ctx.arena.alloc_n<double>((size_t)m.s * m.kk);
+    m.Bn = ctx.arena.alloc_n<double>((size_t)m.s * m.kk);
+    m.sig = ctx.arena.alloc_n<double>(m.kk);
+    HSVD_CUDA(cudaMemcpyAsync(m.w, a.sigma, m.k1 * sizeof(double), cudaMemcpyDeviceToDevice,
+                              ctx.stream));
+    HSVD_CUDA(cudaMemcpyAsync(m.w + m.k1, b.sigma, m.k2 * sizeof(double),
+                              cudaMemcpyDeviceToDevice, ctx.stream));
+    // Gram of [B1 | B2]
+    gsy.push_back({a.B, a.B, m.G, a.ld, a.ld, m.q, m.k1, m.k1, m.s, 1.0, 0.0});
+    gsy.push_back({b.B, b.B, m.G + m.k1 + (long long)m.k1 * m.q, b.ld, b.ld, m.q, m.k2, m.k2,
+                   m.s, 1.0, 0.0});
+    gx.push_back({a.B, b.B, m.G + (long long)m.k1 * m.q, a.ld, b.ld, m.q, m.k1, m.k2, m.s, 1.0,
+                  0.0});
+    gx.push_back({b.B, a.B, m.G + m.k1, b.ld, a.ld, m.q, m.k2, m.k1, m.s, 1.0, 0.0});
+    ss.push_back({m.G, m.q, m.q, m.w});
+    ej.push_back({m.G, m.q, m.q, m.kk, m.lam, m.Z, m.q});
+    sr.push_back({m.Zh, m.q, m.Z, m.q, m.q, m.kk, m.w});
+    // P = B1 (S1 Z1) + B2 (S2 Z2)
+    p1.push_back({a.B, m.Zh, m.P, a.ld, m.q, m.s, m.s, m.kk, m.k1, 1.0, 0.0});
+    p2.push_back({b.B, m.Zh + m.k1, m.P, b.ld, m.q, m.s, m.s, m.kk, m.k2, 1.0, 1.0});
+  }
+  gemm_grouped(ctx, DType::F64, DType::F64, true, false, true, gsy);
+  gemm_grouped(ctx, DType::F64, DType::F64, true, false, false, gx);
+  scale_sym(ctx, ss);
+  eig_topk(ctx, ej);
+  scale_rows(ctx, sr);
+  gemm_grouped(ctx, DType::F64, DType::F64, false, false, false, p1);
+  gemm_grouped(ctx, DType::F64, DType::F64, false, false, false, p2);
+  std::vector<FinJob> fj;
+  for (int i = 0; i < np; ++i) {
+    Tmp& m = t[i];
+    fj.push_back({m.P, m.s, m.s, m.kk, gamma, cap, m.Bn, m.s, m.sig, nullptr, d_rd + i,
+                  d_rd + np + i, 0});
+  }
+  finalize(ctx, fj);
+  std::vector<int> rd;
+  fetch_ranks(ctx, d_rd, 2 * np, rd);
+  std::vector<int> deg(rd.begin() + np, rd.end());
+  std::vector<std::pair<long long, long long>> dims;
+  for (auto& m : t) dims.push_back({m.q, m.q});
+  check_decomp(deg, dims, "");
+  for (int i = 0; i < np; ++i) {
+    DFac& f = out[i];
+    f.B = t[i].Bn;
+    f.ld = t[i].s;
+    f.dim = t[i].s;
+    f.rank = rd[i];
+    f.sigma = t[i].sig;
+    f.degenerate = deg[i] == 1;
+  }
+  return out;
+}
+
+std::vector<DFac> tree_merge_many(Ctx& ctx, std::vector<std::vector<DFac>> trees, double gamma,
+                                  int cap, long long* pair_merges) {
+  for (auto& tr : trees)
+    if (tr.empty()) throw Error(kInvalid, "tree_merge: factor list is empty");
+  while (true) {
+    std::vector<std::pair<DFac, DFac>> pairs;
+    for (auto& tr : trees)
+      for (size_t i = 0; i + 1 < tr.size(); i += 2) pairs.push_back({tr[i], tr[i + 1]});
+    if (pairs.empty()) break;
+    std::vector<DFac> merged = merge_batch(ctx, pairs, gamma, cap);
+    if (pair_merges) *pair_merges += (long long)pairs.size();
+    size_t k = 0;
+    for (auto& tr : trees) {
+      std::vector<DFac> nxt;
+      for (size_t i = 0; i + 1 < tr.size(); i += 2) nxt.push_back(merged[k++]);
+      if (tr.size() % 2 == 1) nxt.push_back(tr.back());
+      tr.swap(nxt);
+    }
+  }
+  std::vector<DFac> out;
+  for (auto& tr : trees) out.push_back(tr.front());
+  return out;
+}
+
+// ---------------------------------------------------------------------------
+// V-recovery of each row slice: SVD of U_j^T X_j through its k x k Gram
+// ---------------------------------------------------------------------------
+static std::vector<DFac> vrecover_batch(Ctx& ctx, const XView& x, const std::vector<Slice>& rows,
+                                        const std::vector<DFac>& us, double gamma, int cap) {
+  const int ns = static_cast<int>(rows.size());
+  std::vector<DFac> out(ns);
+  struct Tmp {
+    int r, kk;
+    double *Bt, *H, *lam, *Z, *V, *Vn, *sig;
+  };
+  std::vector<Tmp> t(ns);
+  const int n = static_cast<int>(x.n);
+  std::vector<GemmDesc> g1, g2, g3;
+  std::vector<EigJob> ej;
+  int* d_rd = ctx.arena.alloc_n<int>(2 * (size_t)ns);
+  for (int j = 0; j < ns; ++j) {
+    Tmp& m = t[j];
+    const DFac& u = us[j];
+    m.r = u.rank;
+    m.kk = std::min(m.r, n);
+    if (cap > 0) m.kk = std::min(m.kk, cap);
+    m.Bt = ctx.arena.alloc_n<double>((size_t)n * m.r);
+    m.H = ctx.arena.alloc_n<double>((size_t)m.r * m.r);
+    m.lam = ctx.arena.alloc_n<double>(m.kk);
+    m.Z = ctx.arena.alloc_n<double>((size_t)m.r * m.kk);
+    m.V = ctx.arena.alloc_n<double>((size_t)n * m.kk);
+    m.Vn = ctx.arena.alloc_n<double>((size_t)n * m.kk);
+    m.sig = ctx.arena.alloc_n<double>(m.kk);
+    const void* base = xptr(x, rows[j].start, 0);
+    // B^T = X_j^T U_j (n x r): Xt (n x d_j) * U_j
+    g1.push_back({base, u.B, m.Bt, x.ld, u.ld, n, n, m.r, (int)rows[j].count, 1.0, 0.0});
+    g2.push_back({m.Bt, m.Bt, m.H, n, n, m.r, m.r, m.r, n, 1.0, 0.0});
+    ej.push_back({m.H, m.r, m.r, m.kk, m.lam, m.Z, m.r});
+    g3.push_back({m.Bt, m.Z, m.V, n, m.r, n, n, m.kk, m.r, 1.0, 0.0});
+  }
+  gemm_grouped(ctx, x.dt, DType::F64, false, false, false, g1);
+  gemm_grouped(ctx, DType::F64, DType::F64, true, false, true, g2);
+  eig_topk(ctx, ej);
+  gemm_grouped(ctx, DType::F64, DType::F64, false, false, false, g3);
+  std::vector<FinJob> fj;
+  for (int j = 0; j < ns; ++j) {
+    Tmp& m = t[j];
+    fj.push_back({m.V, n, n, m.kk, gamma, cap, m.Vn, n, m.sig, nullptr, d_rd + j, d_rd + ns + j, 0});
+  }
+  finalize(ctx, fj);
+  std::vector<int> rd;
+  fetch_ranks(ctx, d_rd, 2 * ns, rd);
+  for (int j = 0; j < ns; ++j)
+    if (rd[ns + j] == 2)
+      throw Error(kDecomposition,
+                  "row slice " + std::to_string(j) + ": SVD did not converge for a " +
+                      std::to_string(t[j].r) + "x" + std::to_string(n) + " matrix",
+                  t[j].r, n);
+  for (int j = 0; j < ns; ++j) {
+    DFac& f = out[j];
+    f.B = t[j].Vn;
+    f.ld = n;
+    f.dim = n;
+    f.rank = rd[j];
+    f.sigma = t[j].sig;
+    f.degenerate = rd[ns + j] == 1;
+  }
+  return out;
+}
+
+DFac svd_of_col_slices(Ctx& ctx, const XView& x, long long c, double gamma, int cap) {
+  auto cols = partition(x.n, c);
+  std::vector<Block> blocks;
+  for (auto& cs : cols) blocks.push_back({0, (int)x.m, cs.start, (int)cs.count});
+  std::vector<DFac> leaves = block_svd_batch(ctx, x, blocks, gamma, cap, false, false);
+  return tree_merge_many(ctx, {leaves}, gamma, cap, nullptr).front();
+}
+
+DFac hierarchical_svd(Ctx& ctx, const XView& x, const HsvdConfig& cfg) {
+  auto rows = partition(x.m, cfg.d);
+  auto cols = partition(x.n, cfg.c);
+  const int P = static_cast<int>(rows.size()), Q = static_cast<int>(cols.size());
+  std::vector<Block> blocks;
+  for (int j = 0; j < P; ++j)
+    for (int i = 0; i < Q; ++i)
+      blocks.push_back({rows[j].start, (int)rows[j].count, cols[i].start, (int)cols[i].count});
+  std::vector<DFac> leaves;
+  try {
+    leaves = block_svd_batch(ctx, x, blocks, cfg.gamma, cfg.cap, false, false);
+  } catch (const Error& e) {
+    if (e.code != kDecomposition) throw;
+    for (int j = 0; j < P; ++j)  // attribute to the first failing slice
+      if (e.rows <= rows[j].count)
+        throw Error(kDecomposition, "row slice " + std::to_string(j) + ": " + e.what(), e.rows,
+                    e.cols);
+    throw;
+  }
+  std::vector<std::vector<DFac>> trees(P);
+  for (int j = 0; j < P; ++j) trees[j].assign(leaves.begin() + j * Q, leaves.begin() + (j + 1) * Q);
+  std::vector<DFac> us = tree_merge_many(ctx, trees, cfg.gamma, cfg.cap, nullptr);
+  std::vector<DFac> vs = vrecover_batch(ctx, x, rows, us, cfg.gamma, cfg.cap);
+  return tree_merge_many(ctx, {vs}, cfg.gamma, cfg.cap, nullptr).front();
+}
+
+DFac recover_left_vectors(Ctx& ctx, const XView& x, const double* v_r, long long ldv, int r) {
+  const int m = static_cast<int>(x.m), n = static_cast<int>(x.n);
+  if (r < 1) throw Error(kInvalid, "recover_left_vectors: v_r has no columns");
+  double* H = ctx.arena.alloc_n<double>((size_t)r * r);
+  double* dd = ctx.arena.alloc_n<double>(1);
+  gemm_grouped(ctx, DType::F64, DType::F64, true, false, true,
+               {{v_r, v_r, H, ldv, ldv, r, r, r, n, 1.0, 0.0}});
+  ortho_defect(ctx, H, r, r, dd);
+  double* hd = ctx.pinned_dbl(1);
+  HSVD_CUDA(cudaMemcpyAsync(hd, dd, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+  HSVD_CUDA(cudaStreamSynchronize(ctx.stream));
+  if (!(hd[0] <= 1e-6))
+    throw Error(kInvalid, "recover_left_vectors: v_r columns are not orthonormal");
+  const int kk = std::min(r, m);
+  double* Y = ctx.arena.alloc_n<double>((size_t)m * r);
+  double* lam = ctx.arena.alloc_n<double>(kk);
+  double* Z = ctx.arena.alloc_n<double>((size_t)r * kk);
+  double* Yh = ctx.arena.alloc_n<double>((size_t)m * kk);
+  double* U = ctx.arena.alloc_n<double>((size_t)m * kk);
+  double* sig = ctx.arena.alloc_n<double>(kk);
+  int* perm = ctx.arena.alloc_n<int>(kk);
+  double* Zp = ctx.arena.alloc_n<double>((size_t)r * kk);
+  double* V = ctx.arena.alloc_n<double>((size_t)n * kk);
+  int* d_rd = ctx.arena.alloc_n<int>(2);
+  // Y = X V_r : Xt (n x m) transposed
+  gemm_grouped(ctx, x.dt, DType::F64, true, false, false,
+               {{x.X, v_r, Y, x.ld, ldv, m, m, r, n, 1.0, 0.0}});
+  gemm_grouped(ctx, DType::F64, DType::F64, true, false, true, {{Y, Y, H, m, m, r, r, r, m, 1.0, 0.0}});
+  eig_topk(ctx, {{H, r, r, kk, lam, Z, r}});
+  gemm_grouped(ctx, DType::F64, DType::F64, false, false, false,
+               {{Y, Z, Yh, m, r, m, m, kk, r, 1.0, 0.0}});
+  finalize(ctx, {{Yh, m, m, kk, 0.0, 0, U, m, sig, perm, d_rd, d_rd + 1, 1}});
+  gather_cols(ctx, {{Zp, r, Z, r, r, kk, perm}});
+  gemm_grouped(ctx, DType::F64, DType::F64, false, false, false,
+               {{v_r, Zp, V, ldv, r, n, n, kk, r, 1.0, 0.0}});
+  std::vector<int> rd;
+  fetch_ranks(ctx, d_rd, 2, rd);
+  if (rd[1] == 2)
+    throw Error(kDecomposition,
+                "SVD did not converge for a " + std::to_string(m) + "x" + std::to_string(r) + " matrix",
+                m, r);
+  DFac f;
+  f.B = U;
+  f.ld = m;
+  f.dim = m;
+  f.rank = kk;
+  f.sigma = sig;
+  f.degenerate = rd[1] == 1;
+  f.B2 = V;
+  f.ld2 = n;
+  f.dim2 = n;
+  return f;
+}
+
+}  // namespace hsvdcu

@@ -1,0 +1,79 @@
+// Host orchestrator of the hierarchical merge-and-truncate SVD on one B200
+// (and, with a communicator, on the row shards of several).
+#pragma once
+
+#include <vector>
+
+#include "ctx.h"
+#include "gemm.h"
+
+namespace hsvdcu {
+
+// Device factor: one (or two) column-major bases + sigma, all in ctx.arena.
+struct DFac {
+  double* B = nullptr;  // carried basis, dim x rank (col-major, ld)
+  long long ld = 0;
+  int dim = 0;
+  int rank = 0;
+  double* sigma = nullptr;
+  bool degenerate = false;
+  double* B2 = nullptr;  // optional other side (dim2 x rank)
+  long long ld2 = 0;
+  int dim2 = 0;
+};
+
+// Row-major m x n matrix on the device (reference DenseMatrix layout).
+struct XView {
+  const void* X;
+  DType dt;
+  long long ld;
+  long long m, n;
+};
+
+struct Block {
+  long long r0;
+  int d;
+  long long c0;
+  int c;
+};
+
+struct Slice {
+  long long start;
+  long long count;
+};
+std::vector<Slice> partition(long long extent, long long block);  // hierarchy.cpp:11-18
+
+struct HsvdConfig {
+  double gamma = 1e-2;
+  long long d = 0, c = 0;
+  int cap = 0;  // max_rank, 0 = none
+};
+
+// Exact thin SVD of each block, truncated (hierarchy.cpp:57: truncate_factor
+// (full_svd(block))).  keep_both: also return the other side in B2.
+std::vector<DFac> block_svd_batch(Ctx& ctx, const XView& x, const std::vector<Block>& blocks,
+                                  double gamma, int cap, bool keep_both, bool write_all);
+
+// merge_pair_qr semantics (merge.cpp:71-117) for a batch of pairs sharing
+// the basis dimension per pair.
+std::vector<DFac> merge_batch(Ctx& ctx, const std::vector<std::pair<DFac, DFac>>& pairs,
+                              double gamma, int cap);
+
+// Several independent trees advanced level by level (hierarchy.cpp:31-48).
+std::vector<DFac> tree_merge_many(Ctx& ctx, std::vector<std::vector<DFac>> trees, double gamma,
+                                  int cap, long long* pair_merges);
+
+// hierarchy.cpp:65-94 -> (sigma, V); rows of x may be a shard of the full
+// matrix in multi-GPU mode (engine handles the cross-rank levels).
+DFac hierarchical_svd(Ctx& ctx, const XView& x, const HsvdConfig& cfg);
+
+// hierarchy.cpp:50-63
+DFac svd_of_col_slices(Ctx& ctx, const XView& x, long long c, double gamma, int cap);
+
+// hierarchy.cpp:96-112 -> U (m x r) in B, V (n x r) in B2.
+DFac recover_left_vectors(Ctx& ctx, const XView& x, const double* v_r, long long ldv, int r);
+
+// Reads back ranks / degenerate flags written by finalize (synchronises).
+void fetch_ranks(Ctx& ctx, const int* d_ranks, int count, std::vector<int>& out);
+
+}  // namespace hsvdcu

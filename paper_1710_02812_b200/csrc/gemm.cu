@@ -1,0 +1,265 @@
+// Grouped fp64 GEMM for the HSVD path on sm_100a.
+//
+// Every contraction of the hot path (block Grams X_b^T X_b, projections
+// X_b Z, V-recovery X_j^T U_j, U-recovery X V_r, merge Grams/projections,
+// the blocked Householder back-transform) runs through this kernel.  The
+// reference computes all of them in IEEE binary64 (Eigen, dense_matrix.hpp:9);
+// tcgen05.mma has no f64 kind, so the fp64-exact tensor path on B200 is DMMA
+// (mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4).  fp32 inputs (the BASELINE
+// matrices) are promoted to fp64 on the way into shared memory, which is
+// exactly what the reference's fp64 DenseMatrix computes on the same bytes.
+//
+// Tile: 64x64 per CTA (4 warps, 32x32 each = 4x4 DMMA tiles), BK = 16,
+// register-prefetch double buffering; optional split-K with a deterministic
+// fixed-order reduction (run-to-run bitwise stable).
+#include <algorithm>
+
+#include "gemm.h"
+
+namespace hsvdcu {
+
+namespace {
+
+constexpr int BM = 64, BN = 64, BK = 16, PAD = 4, NT = 128;
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+template <typename T>
+__device__ __forceinline__ double ldg(const T* p) { return static_cast<double>(__ldg(p)); }
+
+template <typename TA, typename TB, bool TRA, bool TRB>
+__global__ void __launch_bounds__(NT) k_gemm(const GemmDesc* __restrict__ descs, int syrk,
+                                             int splits, double* __restrict__ ws,
+                                             long long ws_slot) {
+  const int g = blockIdx.z / splits;
+  const int split = blockIdx.z - g * splits;
+  const GemmDesc d = descs[g];
+  const int tm = blockIdx.x, tn = blockIdx.y;
+  if (tm * BM >= d.M || tn * BN >= d.N) return;
+  if (syrk && tn > tm) return;
+
+  int kchunk = (d.K + splits - 1) / splits;
+  kchunk = (kchunk + BK - 1) / BK * BK;
+  const int kb = split * kchunk;
+  const int ke = min(d.K, kb + kchunk);
+
+  __shared__ __align__(16) double As[2][BK][BM + PAD];
+  __shared__ __align__(16) double Bs[2][BK][BN + PAD];
+
+  const TA* A = static_cast<const TA*>(d.A);
+  const TB* B = static_cast<const TB*>(d.B);
+  const int tid = threadIdx.x;
+  const int m0 = tm * BM, n0 = tn * BN;
+
+  double ra[8], rb[8];
+  auto load = [&](int k0) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int idx = tid + i * NT;
+      int m, k;
+      if (!TRA) { m = idx & (BM - 1); k = idx >> 6; }
+      else      { k = idx & (BK - 1); m = idx >> 4; }
+      const int gm = m0 + m, gk = k0 + k;
+      double v = 0.0;
+      if (gm < d.M && gk < ke)
+        v = TRA ? ldg(A + (long long)gk + (long long)gm * d.lda)
+                : ldg(A + (long long)gm + (long long)gk * d.lda);
+      ra[i] = v;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int idx = tid + i * NT;
+      int n, k;
+      if (!TRB) { k = idx & (BK - 1); n = idx >> 4; }
+      else      { n = idx & (BN - 1); k = idx >> 6; }
+      const int gn = n0 + n, gk = k0 + k;
+      double v = 0.0;
+      if (gn < d.N && gk < ke)
+        v = TRB ? ldg(B + (long long)gn + (long long)gk * d.ldb)
+                : ldg(B + (long long)gk + (long long)gn * d.ldb);
+      rb[i] = v;
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int idx = tid + i * NT;
+      int m, k;
+      if (!TRA) { m = idx & (BM - 1); k = idx >> 6; }
+      else      { k = idx & (BK - 1); m = idx >> 4; }
+      As[buf][k][m] = ra[i];
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int idx = tid + i * NT;
+      int n, k;
+      if (!TRB) { k = idx & (BK - 1); n = idx >> 4; }
+      else      { n = idx & (BN - 1); k = idx >> 6; }
+      Bs[buf][k][n] = rb[i];
+    }
+  };
+
+  const int lane = tid & 31, warp = tid >> 5;
+  const int grp = lane >> 2, tig = lane & 3;
+  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
+
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  int buf = 0;
+  if (kb < ke) {
+    load(kb);
+    store(0);
+  }
+  __syncthreads();
+  for (int k0 = kb; k0 < ke; k0 += BK) {
+    const bool more = k0 + BK < ke;
+    if (more) load(k0 + BK);
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[buf][kk + tig][wm + i * 8 + grp];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[buf][kk + tig][wn + j * 8 + grp];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma(acc[i][j], a[i], b[j]);
+    }
+    if (more) {
+      store(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
+    }
+  }
+
+  // epilogue
+  const bool to_ws = ws != nullptr;
+  double* out = to_ws ? ws + (long long)blockIdx.z * ws_slot : d.C;
+  const long long ldo = to_ws ? (long long)d.M : d.ldc;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int m = m0 + wm + i * 8 + grp;
+    if (m >= d.M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int n = n0 + wn + j * 8 + 2 * tig + r;
+        if (n >= d.N) continue;
+        double v = acc[i][j][r];
+        if (to_ws) {
+          out[m + n * ldo] = v;
+        } else {
+          v *= d.alpha;
+          if (d.beta != 0.0) v += d.beta * out[m + n * ldo];
+          out[m + n * ldo] = v;
+          if (syrk && tm != tn) out[n + m * ldo] = v;
+        }
+      }
+    }
+  }
+}
+
+__global__ void k_splitk_reduce(const GemmDesc* __restrict__ descs, int splits, int syrk,
+                                const double* __restrict__ ws, long long ws_slot) {
+  const int g = blockIdx.y;
+  const GemmDesc d = descs[g];
+  const long long total = (long long)d.M * d.N;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int m = (int)(e % d.M), n = (int)(e / d.M);
+    if (syrk && m < n) continue;
+    double s = 0.0;
+    const double* base = ws + (long long)g * splits * ws_slot + m + (long long)n * d.M;
+    for (int t = 0; t < splits; ++t) s += base[t * ws_slot];
+    s *= d.alpha;
+    double* c = d.C + m + (long long)n * d.ldc;
+    if (d.beta != 0.0) s += d.beta * *c;
+    *c = s;
+    if (syrk && m != n) d.C[n + (long long)m * d.ldc] = s;
+  }
+}
+
+template <typename TA, typename TB>
+void launch_typed(Ctx& ctx, bool ta, bool tb, dim3 grid, const GemmDesc* dd, int syrk,
+                  int splits, double* ws, long long slot) {
+  cudaStream_t s = ctx.stream;
+  if (!ta && !tb) k_gemm<TA, TB, false, false><<<grid, NT, 0, s>>>(dd, syrk, splits, ws, slot);
+  else if (!ta && tb) k_gemm<TA, TB, false, true><<<grid, NT, 0, s>>>(dd, syrk, splits, ws, slot);
+  else if (ta && !tb) k_gemm<TA, TB, true, false><<<grid, NT, 0, s>>>(dd, syrk, splits, ws, slot);
+  else k_gemm<TA, TB, true, true><<<grid, NT, 0, s>>>(dd, syrk, splits, ws, slot);
+  ctx.check_launch("k_gemm");
+}
+
+}  // namespace
+
+void gemm_grouped(Ctx& ctx, DType ta, DType tb, bool trans_a, bool trans_b, bool syrk,
+                  const std::vector<GemmDesc>& descs) {
+  std::vector<GemmDesc> live;
+  live.reserve(descs.size());
+  int maxM = 0, maxN = 0, maxK = 0;
+  long long tiles = 0;
+  for (const auto& d : descs) {
+    if (d.M <= 0 || d.N <= 0) continue;
+    if (d.K <= 0) {
+      // C = beta*C: express as a 1-deep product with zero operands is wasteful;
+      // handled by a dedicated scale below.
+    }
+    live.push_back(d);
+    maxM = std::max(maxM, d.M);
+    maxN = std::max(maxN, d.N);
+    maxK = std::max(maxK, d.K);
+    long long t = (long long)ceil_div(d.M, BM) * ceil_div(d.N, BN);
+    if (syrk) t = (t + ceil_div(d.M, BM)) / 2;
+    tiles += t;
+  }
+  if (live.empty()) return;
+  const int count = static_cast<int>(live.size());
+  if (count > 65535) throw Error(kInvalid, "gemm_grouped: too many groups");
+
+  int splits = 1;
+  const long long target = 4LL * ctx.num_sms;
+  if (tiles < target && maxK >= 2 * 256) {
+    splits = static_cast<int>(std::min<long long>((target + tiles - 1) / tiles, maxK / 256));
+    splits = std::max(1, std::min(splits, 128));
+    while (splits > 1 && (long long)count * splits > 65535) --splits;
+  }
+  const GemmDesc* dd =
+      static_cast<const GemmDesc*>(ctx.staging.put(live.data(), live.size() * sizeof(GemmDesc),
+                                                   ctx.stream));
+  dim3 grid(ceil_div(maxM, BM), ceil_div(maxN, BN), count * splits);
+  double* ws = nullptr;
+  long long slot = 0;
+  Arena::Mark mk = ctx.arena.mark();
+  if (splits > 1) {
+    slot = (long long)maxM * maxN;
+    ws = ctx.arena.alloc_n<double>((size_t)slot * count * splits);
+  }
+  const int sy = syrk ? 1 : 0;
+  if (ta == DType::F64 && tb == DType::F64)
+    launch_typed<double, double>(ctx, trans_a, trans_b, grid, dd, sy, splits, ws, slot);
+  else if (ta == DType::F32 && tb == DType::F64)
+    launch_typed<float, double>(ctx, trans_a, trans_b, grid, dd, sy, splits, ws, slot);
+  else if (ta == DType::F64 && tb == DType::F32)
+    launch_typed<double, float>(ctx, trans_a, trans_b, grid, dd, sy, splits, ws, slot);
+  else
+    launch_typed<float, float>(ctx, trans_a, trans_b, grid, dd, sy, splits, ws, slot);
+  if (splits > 1) {
+    const long long elems = (long long)maxM * maxN;
+    int bx = static_cast<int>(std::min<long long>((elems + 255) / 256, 4096));
+    k_splitk_reduce<<<dim3(bx, count), 256, 0, ctx.stream>>>(dd, splits, sy, ws, slot);
+    ctx.check_launch("k_splitk_reduce");
+  }
+  ctx.arena.release(mk);
+}
+
+}  // namespace hsvdcu

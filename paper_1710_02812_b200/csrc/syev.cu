@@ -1,0 +1,587 @@
+// Batched fp64 symmetric eigensolver, top-kk eigenpairs (one matrix per CTA
+// for the latency-bound phases, grouped DMMA GEMMs for the back-transform).
+//
+// Replaces the dense SVD kernel of the reference (Eigen BDCSVD/JacobiSVD,
+// kernels.cpp:21-48) on the Gram form of every decomposition in the path:
+// a block X_b (d x c) is decomposed through G = X_b^T X_b (c x c), whose top
+// eigenpairs give (sigma^2, V_b); U_b = X_b V_b / sigma follows by GEMM.
+//
+//   1. k_sytrd   Householder tridiagonalisation Q^T G Q = T (LAPACK dsytd2 'L'
+//                algorithm), with the rank-2 update of step j fused with the
+//                symmetric mat-vec of step j+1: one read+write pass of the
+//                trailing matrix per column.
+//   2. k_steig   top-kk eigenvalues of T by Sturm-count bisection, vectors by
+//                LDL^T inverse iteration with Gram-Schmidt inside clusters
+//                (LAPACK dstebz + dstein algorithm).
+//   3. back-transform Z <- Q Z with the compact-WY form of 32 reflectors at a
+//                time (LAPACK dlarft + dlarfb): three grouped DMMA GEMMs per
+//                reflector block, the reflectors read in place from A.
+#include <algorithm>
+#include <cfloat>
+#include <cmath>
+
+#include "gemm.h"
+#include "syev.h"
+
+namespace hsvdcu {
+
+namespace {
+
+constexpr int TRD_THREADS = 1024;
+constexpr int TRD_QMAX = 8;  // rows per thread when n > 1024 (n <= 8192)
+constexpr int EIG_THREADS = 256;
+constexpr int NB = 32;       // reflectors per compact-WY block
+
+struct EigDev {
+  double* A;
+  long long lda;
+  int n;
+  int kk;
+  double* d;
+  double* e;
+  double* tau;
+  double* lam;
+  double* Z;
+  long long ldz;
+  double* piv;   // n * kk scratch (LDL^T pivots)
+  double* T;     // (nblocks * NB * NB) compact-WY T factors
+};
+
+// ---------------------------------------------------------------------------
+// 1. tridiagonalisation
+// ---------------------------------------------------------------------------
+
+// Householder reflector (LAPACK dlarfg) annihilating A[r0+1:, c]; v has
+// v[r0] = 1, stored to vout[r0..n) and to A[r0+1:, c].  Returns tau.
+__device__ double make_reflector(double* A, long long lda, int n, int c, int r0, double* vout,
+                                 double* red, double* e_out, double* tau_out) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  double part = 0.0;
+  for (int i = r0 + 1 + tid; i < n; i += nt) {
+    const double x = A[i + c * lda];
+    part += x * x;
+  }
+  const double xn2 = block_sum(part, red);
+  const double alpha = A[r0 + c * lda];
+  double tau = 0.0, beta = alpha, scal = 0.0;
+  if (xn2 > 0.0) {
+    const double nrm = sqrt(alpha * alpha + xn2);
+    beta = alpha >= 0.0 ? -nrm : nrm;
+    tau = (beta - alpha) / beta;
+    scal = 1.0 / (alpha - beta);
+  }
+  for (int i = r0 + 1 + tid; i < n; i += nt) {
+    const double v = A[i + c * lda] * scal;
+    A[i + c * lda] = v;
+    vout[i] = v;
+  }
+  if (tid == 0) {
+    vout[r0] = 1.0;
+    *e_out = beta;
+    *tau_out = tau;
+  }
+  return tau;
+}
+
+// One pass over the trailing block A[lo:, lo:]: optional rank-2 update
+// A -= v w^T + w v^T, and p = A_new * mv.  p written to ps[lo..n).
+template <bool UPDATE>
+__device__ void trailing_pass(double* A, long long lda, int n, int lo, const double* vs,
+                              const double* wv, const double* mv, double* ps, double* pp,
+                              int RT, int CT, int tr, int tc) {
+  double pacc[TRD_QMAX];
+  double vi[TRD_QMAX], wi[TRD_QMAX];
+  int Q = (n - lo + RT - 1) / RT;
+  if (Q > TRD_QMAX) Q = TRD_QMAX;
+#pragma unroll
+  for (int q = 0; q < TRD_QMAX; ++q) {
+    pacc[q] = 0.0;
+    const int i = lo + tr + q * RT;
+    vi[q] = (q < Q && i < n && UPDATE) ? vs[i] : 0.0;
+    wi[q] = (q < Q && i < n && UPDATE) ? wv[i] : 0.0;
+  }
+  int k = lo + tc;
+  // unrolled by 2 columns for memory-level parallelism
+  for (; k + CT < n; k += 2 * CT) {
+    const int k1 = k + CT;
+    const double mk0 = mv[k], mk1 = mv[k1];
+    double vk0 = 0, wk0 = 0, vk1 = 0, wk1 = 0;
+    if (UPDATE) {
+      vk0 = vs[k]; wk0 = wv[k]; vk1 = vs[k1]; wk1 = wv[k1];
+    }
+    double* c0 = A + (long long)k * lda;
+    double* c1 = A + (long long)k1 * lda;
+#pragma unroll
+    for (int q = 0; q < TRD_QMAX; ++q) {
+      const int i = lo + tr + q * RT;
+      if (q < Q && i < n) {
+        double a0 = c0[i], a1 = c1[i];
+        if (UPDATE) {
+          a0 -= vi[q] * wk0 + wi[q] * vk0;
+          a1 -= vi[q] * wk1 + wi[q] * vk1;
+          c0[i] = a0;
+          c1[i] = a1;
+        }
+        pacc[q] += a0 * mk0 + a1 * mk1;
+      }
+    }
+  }
+  for (; k < n; k += CT) {
+    const double mk = mv[k];
+    double vk = 0, wk = 0;
+    if (UPDATE) { vk = vs[k]; wk = wv[k]; }
+    double* c0 = A + (long long)k * lda;
+#pragma unroll
+    for (int q = 0; q < TRD_QMAX; ++q) {
+      const int i = lo + tr + q * RT;
+      if (q < Q && i < n) {
+        double a = c0[i];
+        if (UPDATE) {
+          a -= vi[q] * wk + wi[q] * vk;
+          c0[i] = a;
+        }
+        pacc[q] += a * mk;
+      }
+    }
+  }
+  if (CT == 1) {
+#pragma unroll
+    for (int q = 0; q < TRD_QMAX; ++q) {
+      const int i = lo + tr + q * RT;
+      if (q < Q && i < n) ps[i] = pacc[q];
+    }
+  } else {
+    pp[tc * RT + tr] = pacc[0];  // Q == 1 whenever CT > 1
+    __syncthreads();
+    if (threadIdx.x < RT) {
+      const int i = lo + threadIdx.x;
+      double s = 0.0;
+      for (int c = 0; c < CT; ++c) s += pp[c * RT + threadIdx.x];
+      if (i < n) ps[i] = s;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(TRD_THREADS) k_sytrd(const EigDev* __restrict__ jobs) {
+  const EigDev J = jobs[blockIdx.x];
+  const int n = J.n;
+  double* A = J.A;
+  const long long lda = J.lda;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  extern __shared__ double sm[];
+  double* vs = sm;
+  double* wv = vs + n;
+  double* vn = wv + n;
+  double* ps = vn + n;
+  double* pp = ps + n;
+  double* red = pp + TRD_THREADS;
+  __shared__ double s_tau, s_tau_next, s_e;
+
+  if (n == 1) {
+    if (tid == 0) J.d[0] = A[0];
+    return;
+  }
+  int RT = 32;
+  while (RT < n && RT < TRD_THREADS) RT <<= 1;
+  const int CT = nt / RT;
+  const int tr = tid % RT, tc = tid / RT;
+
+  // reflector 0 from column 0
+  make_reflector(A, lda, n, 0, 1, vn, red, &s_e, &s_tau);
+  __syncthreads();
+  if (tid == 0) {
+    J.d[0] = A[0];
+    J.e[0] = s_e;
+    J.tau[0] = s_tau;
+  }
+  for (int i = 1 + tid; i < n; i += nt) vs[i] = vn[i];
+  __syncthreads();
+  trailing_pass<false>(A, lda, n, 1, vs, wv, vs, ps, pp, RT, CT, tr, tc);
+  __syncthreads();
+
+  for (int j = 0; j <= n - 2; ++j) {
+    const double tau = s_tau;
+    if (tau != 0.0) {
+      double part = 0.0;
+      for (int i = j + 1 + tid; i < n; i += nt) part += ps[i] * vs[i];
+      const double dot = tau * block_sum(part, red);
+      const double alpha = -0.5 * tau * dot;
+      for (int i = j + 1 + tid; i < n; i += nt) wv[i] = tau * ps[i] + alpha * vs[i];
+    } else {
+      for (int i = j + 1 + tid; i < n; i += nt) wv[i] = 0.0;
+    }
+    __syncthreads();
+    if (j == n - 2) {
+      if (tid == 0) {
+        const long long ii = (long long)(n - 1) * (lda + 1);
+        J.d[n - 1] = A[ii] - 2.0 * vs[n - 1] * wv[n - 1];
+      }
+      break;
+    }
+    // update column j+1 (rows j+1..n-1)
+    {
+      const long long cj = (long long)(j + 1) * lda;
+      const double vj = vs[j + 1], wj = wv[j + 1];
+      for (int i = j + 1 + tid; i < n; i += nt) A[i + cj] -= vs[i] * wj + wv[i] * vj;
+    }
+    __syncthreads();
+    make_reflector(A, lda, n, j + 1, j + 2, vn, red, &s_e, &s_tau_next);
+    __syncthreads();
+    if (tid == 0) {
+      J.d[j + 1] = A[(long long)(j + 1) * (lda + 1)];
+      J.e[j + 1] = s_e;
+      J.tau[j + 1] = s_tau_next;
+    }
+    trailing_pass<true>(A, lda, n, j + 2, vs, wv, vn, ps, pp, RT, CT, tr, tc);
+    __syncthreads();
+    for (int i = j + 2 + tid; i < n; i += nt) vs[i] = vn[i];
+    if (tid == 0) s_tau = s_tau_next;
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// 2. tridiagonal eigenpairs: bisection + inverse iteration
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ int sturm_count_less(const double* dd, const double* e2, int n,
+                                                double x, double pivmin) {
+  double q = dd[0] - x;
+  if (fabs(q) < pivmin) q = -pivmin;
+  int cnt = q < 0.0;
+  for (int i = 1; i < n; ++i) {
+    q = dd[i] - x - e2[i - 1] / q;
+    if (fabs(q) < pivmin) q = -pivmin;
+    cnt += q < 0.0;
+  }
+  return cnt;
+}
+
+__device__ __forceinline__ double guard_pivot(double D, double tiny) {
+  if (fabs(D) < tiny) return D < 0.0 ? -tiny : tiny;
+  return D;
+}
+
+__device__ __forceinline__ unsigned hash32(unsigned x) {
+  x ^= x >> 16;
+  x *= 0x7feb352dU;
+  x ^= x >> 15;
+  x *= 0x846ca68bU;
+  x ^= x >> 16;
+  return x;
+}
+
+__global__ void __launch_bounds__(EIG_THREADS) k_steig(const EigDev* __restrict__ jobs) {
+  const EigDev J = jobs[blockIdx.x];
+  const int n = J.n, kk = J.kk;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
+  extern __shared__ double sm[];
+  double* dd = sm;
+  double* ee = dd + n;
+  double* e2 = ee + n;
+  double* lam = e2 + n;
+  double* shift = lam + kk;
+  double* dots = shift + kk;
+  double* red = dots + kk;
+  int* cstart = reinterpret_cast<int*>(red + 32);
+
+  double lo_g = 1e308, hi_g = -1e308, ee2max = 0.0;
+  for (int i = tid; i < n; i += nt) {
+    const double di = J.d[i];
+    const double ei = i < n - 1 ? J.e[i] : 0.0;
+    const double eim = i > 0 ? J.e[i - 1] : 0.0;
+    dd[i] = di;
+    ee[i] = ei;
+    e2[i] = ei * ei;
+    const double r = fabs(ei) + fabs(eim);
+    lo_g = fmin(lo_g, di - r);
+    hi_g = fmax(hi_g, di + r);
+    ee2max = fmax(ee2max, ei * ei);
+  }
+  const double gl = -block_max(-lo_g, red);
+  const double gu = block_max(hi_g, red);
+  const double e2m = block_max(ee2max, red);
+  const double tnorm = fmax(fabs(gl), fabs(gu));
+  const double eps = DBL_EPSILON;
+
+  if (!(tnorm > 0.0) || !isfinite(tnorm)) {
+    // zero (or non-finite) matrix: eigenvalues 0, vectors = identity columns
+    for (int t = tid; t < kk; t += nt) {
+      J.lam[t] = isfinite(tnorm) ? 0.0 : tnorm;
+      double* z = J.Z + (long long)t * J.ldz;
+      for (int r = 0; r < n; ++r) z[r] = (r == t) ? 1.0 : 0.0;
+    }
+    return;
+  }
+  const double pivmin = DBL_MIN * fmax(1.0, e2m);
+
+  // bisection (dstebz): eigenvalue with ascending index n-1-t
+  for (int t = tid; t < kk; t += nt) {
+    const int idx = n - 1 - t;
+    double lo = gl - 4.0 * eps * tnorm - 2.0 * pivmin;
+    double hi = gu + 4.0 * eps * tnorm + 2.0 * pivmin;
+    for (int it = 0; it < 256; ++it) {
+      const double tol = 2.0 * eps * fmax(fabs(lo), fabs(hi)) + 4.0 * pivmin;
+      if (hi - lo <= tol) break;
+      const double mid = 0.5 * (lo + hi);
+      if (mid <= lo || mid >= hi) break;
+      if (sturm_count_less(dd, e2, n, mid, pivmin) > idx) hi = mid;
+      else lo = mid;
+    }
+    lam[t] = 0.5 * (lo + hi);
+  }
+  __syncthreads();
+
+  // clusters (dstein: ORTOL = 1e-3 * ||T||_1) and perturbed shifts
+  if (tid == 0) {
+    double onenrm = 0.0;
+    for (int i = 0; i < n; ++i)
+      onenrm = fmax(onenrm, fabs(dd[i]) + fabs(ee[i]) + (i > 0 ? fabs(ee[i - 1]) : 0.0));
+    const double ortol = 1e-3 * onenrm;
+    const double pertol = 10.0 * eps * onenrm;
+    int cs = 0;
+    for (int t = 0; t < kk; ++t) {
+      double s = lam[t];
+      if (t > 0) {
+        if (lam[t - 1] - lam[t] > ortol) cs = t;
+        if (shift[t - 1] - s < pertol) s = shift[t - 1] - pertol;
+      }
+      shift[t] = s;
+      cstart[t] = cs;
+    }
+  }
+  __syncthreads();
+
+  const double tiny = eps * tnorm;
+  // start vectors (deterministic pseudo-random, dstein uses dlarnv uniform(-1,1))
+  for (int t = tid; t < kk; t += nt) {
+    double* z = J.Z + (long long)t * J.ldz;
+    for (int r = 0; r < n; ++r) {
+      const unsigned h = hash32((unsigned)r * 2654435761u ^ hash32((unsigned)t + 0x9e3779b9u));
+      z[r] = ((double)h / 4294967296.0) * 2.0 - 1.0;
+    }
+  }
+  __syncthreads();
+
+  for (int it = 0; it < 3; ++it) {
+    for (int t = tid; t < kk; t += nt) {
+      const double s = shift[t];
+      double* z = J.Z + (long long)t * J.ldz;
+      double* Dw = J.piv + (long long)t * n;
+      double D = guard_pivot(dd[0] - s, tiny);
+      Dw[0] = D;
+      double y = z[0];
+      for (int r = 1; r < n; ++r) {
+        const double l = ee[r - 1] / D;
+        D = guard_pivot(dd[r] - s - l * ee[r - 1], tiny);
+        Dw[r] = D;
+        y = z[r] - l * y;
+        z[r] = y;
+      }
+      double zr = z[n - 1] / Dw[n - 1];
+      z[n - 1] = zr;
+      double nrm2 = zr * zr;
+      for (int r = n - 2; r >= 0; --r) {
+        zr = (z[r] - ee[r] * zr) / Dw[r];
+        z[r] = zr;
+        nrm2 += zr * zr;
+      }
+      double sc = 1.0 / sqrt(nrm2);
+      if (!isfinite(sc) || nrm2 == 0.0) sc = 0.0;
+      for (int r = 0; r < n; ++r) z[r] *= sc;
+      if (sc == 0.0) z[t % n] = 1.0;
+    }
+    __syncthreads();
+    if (it == 0) continue;
+    // Gram-Schmidt (twice) inside clusters, in eigenvalue order
+    for (int t = 0; t < kk; ++t) {
+      const int cs = cstart[t];
+      if (cs == t) continue;
+      double* zt = J.Z + (long long)t * J.ldz;
+      for (int rep = 0; rep < 2; ++rep) {
+        for (int c = cs + warp; c < t; c += nwarps) {
+          const double* zc = J.Z + (long long)c * J.ldz;
+          double s = 0.0;
+          for (int r = lane; r < n; r += 32) s += zc[r] * zt[r];
+          s = warp_sum(s);
+          if (lane == 0) dots[c - cs] = s;
+        }
+        __syncthreads();
+        for (int r = tid; r < n; r += nt) {
+          double a = zt[r];
+          for (int c = cs; c < t; ++c) a -= dots[c - cs] * J.Z[r + (long long)c * J.ldz];
+          zt[r] = a;
+        }
+        __syncthreads();
+      }
+      double part = 0.0;
+      for (int r = tid; r < n; r += nt) part += zt[r] * zt[r];
+      const double nrm2 = block_sum(part, red);
+      const double sc = nrm2 > 0.0 ? 1.0 / sqrt(nrm2) : 0.0;
+      for (int r = tid; r < n; r += nt) zt[r] *= sc;
+      __syncthreads();
+    }
+  }
+  for (int t = tid; t < kk; t += nt) J.lam[t] = lam[t];
+}
+
+// ---------------------------------------------------------------------------
+// 3. compact-WY preparation: V in place in A, T per block of NB reflectors
+// ---------------------------------------------------------------------------
+
+// Zero the upper triangle and diagonal of A, unit subdiagonal: column j of
+// A (rows j+1..) becomes reflector v_j.
+__global__ void k_prep_v(const EigDev* __restrict__ jobs) {
+  const EigDev J = jobs[blockIdx.y];
+  const int n = J.n;
+  const long long total = (long long)n * n;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e % n), j = (int)(e / n);
+    if (i <= j) J.A[i + j * J.lda] = 0.0;
+    else if (i == j + 1) J.A[i + j * J.lda] = 1.0;
+  }
+}
+
+// T factor (dlarft, forward, columnwise) of every reflector block.
+__global__ void __launch_bounds__(256) k_build_t(const EigDev* __restrict__ jobs) {
+  const EigDev J = jobs[blockIdx.y];
+  const int b = blockIdx.x;
+  const int nref = J.n - 1;
+  const int j0 = b * NB;
+  if (j0 >= nref) return;
+  const int nb = min(NB, nref - j0);
+  __shared__ double S[NB][NB + 1];
+  __shared__ double T[NB][NB + 1];
+  __shared__ double tau[NB];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  if (tid < NB) tau[tid] = tid < nb ? J.tau[j0 + tid] : 0.0;
+  // S = V^T V over rows j0+1..n-1 (V stored in A columns j0..j0+nb-1)
+  for (int pq = warp; pq < nb * nb; pq += nwarps) {
+    const int p = pq / nb, q = pq % nb;
+    if (p > q) continue;
+    const double* vp = J.A + (long long)(j0 + p) * J.lda;
+    const double* vq = J.A + (long long)(j0 + q) * J.lda;
+    double s = 0.0;
+    for (int r = j0 + 1 + q + lane; r < J.n; r += 32) s += vp[r] * vq[r];
+    s = warp_sum(s);
+    if (lane == 0) S[p][q] = s;
+  }
+  for (int e = tid; e < NB * NB; e += blockDim.x) T[e / NB][e % NB] = 0.0;
+  __syncthreads();
+  for (int t = 0; t < nb; ++t) {
+    // T[i,t] = -tau_t * sum_{l=i}^{t-1} T[i,l] S[l,t]
+    if (tid < t) {
+      double s = 0.0;
+      for (int l = tid; l < t; ++l) s += T[tid][l] * S[l][t];
+      T[tid][t] = -tau[t] * s;
+    }
+    if (tid == 0) T[t][t] = tau[t];
+    __syncthreads();
+  }
+  double* out = J.T + (long long)b * NB * NB;
+  for (int e = tid; e < NB * NB; e += blockDim.x) {
+    const int i = e % NB, j = e / NB;  // column-major
+    out[e] = T[i][j];
+  }
+}
+
+}  // namespace
+
+void eig_topk(Ctx& ctx, const std::vector<EigJob>& jobs_in) {
+  std::vector<EigJob> jobs;
+  for (const auto& j : jobs_in)
+    if (j.n > 0 && j.kk > 0) jobs.push_back(j);
+  if (jobs.empty()) return;
+  const int count = static_cast<int>(jobs.size());
+  Arena::Mark mk = ctx.arena.mark();
+  std::vector<EigDev> dev(count);
+  int nmax = 0, kkmax = 0;
+  for (int g = 0; g < count; ++g) {
+    const EigJob& j = jobs[g];
+    if (j.kk > j.n) throw Error(kInvalid, "eig_topk: kk > n");
+    if (j.n > 6144) throw Error(kInvalid, "eig_topk: n > 6144 not supported");
+    EigDev& d = dev[g];
+    d.A = j.A;
+    d.lda = j.lda;
+    d.n = j.n;
+    d.kk = j.kk;
+    d.d = ctx.arena.alloc_n<double>(j.n);
+    d.e = ctx.arena.alloc_n<double>(j.n);
+    d.tau = ctx.arena.alloc_n<double>(j.n);
+    d.lam = j.lam;
+    d.Z = j.Z;
+    d.ldz = j.ldz;
+    d.piv = ctx.arena.alloc_n<double>((size_t)j.n * j.kk);
+    const int nblk = std::max(1, ceil_div(j.n - 1, NB));
+    d.T = ctx.arena.alloc_n<double>((size_t)nblk * NB * NB);
+    nmax = std::max(nmax, j.n);
+    kkmax = std::max(kkmax, j.kk);
+  }
+  const EigDev* dd =
+      static_cast<const EigDev*>(ctx.staging.put(dev.data(), dev.size() * sizeof(EigDev), ctx.stream));
+
+  // 1. tridiagonalise
+  {
+    const size_t smem = (4 * (size_t)nmax + TRD_THREADS + 64) * sizeof(double);
+    HSVD_CUDA(cudaFuncSetAttribute(k_sytrd, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem));
+    k_sytrd<<<count, TRD_THREADS, smem, ctx.stream>>>(dd);
+    ctx.check_launch("k_sytrd");
+  }
+  // 2. tridiagonal eigenpairs
+  {
+    const size_t smem = (3 * (size_t)nmax + 3 * (size_t)kkmax + 32) * sizeof(double) +
+                        (size_t)kkmax * sizeof(int) + 64;
+    HSVD_CUDA(cudaFuncSetAttribute(k_steig, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem));
+    k_steig<<<count, EIG_THREADS, smem, ctx.stream>>>(dd);
+    ctx.check_launch("k_steig");
+  }
+  // 3. back-transform Z <- Q Z (blocks applied last to first)
+  if (nmax > 2) {
+    const long long nn = (long long)nmax * nmax;
+    int gx = static_cast<int>(std::min<long long>((nn + 255) / 256, 2048));
+    k_prep_v<<<dim3(gx, count), 256, 0, ctx.stream>>>(dd);
+    ctx.check_launch("k_prep_v");
+    const int nblk_max = ceil_div(nmax - 1, NB);
+    k_build_t<<<dim3(nblk_max, count), 256, 0, ctx.stream>>>(dd);
+    ctx.check_launch("k_build_t");
+    std::vector<double*> W(count), W2(count);
+    for (int g = 0; g < count; ++g) {
+      W[g] = ctx.arena.alloc_n<double>((size_t)NB * jobs[g].kk);
+      W2[g] = ctx.arena.alloc_n<double>((size_t)NB * jobs[g].kk);
+    }
+    std::vector<GemmDesc> d1, d2, d3;
+    for (int b = nblk_max - 1; b >= 0; --b) {
+      const int j0 = b * NB;
+      d1.clear();
+      d2.clear();
+      d3.clear();
+      for (int g = 0; g < count; ++g) {
+        const EigDev& e = dev[g];
+        const int nref = e.n - 1;
+        if (j0 >= nref || e.n <= 2) continue;
+        const int m = e.n - j0 - 1;
+        const int nb = std::min(NB, nref - j0);
+        const double* V = e.A + j0 + 1 + (long long)j0 * e.lda;
+        double* Zs = e.Z + j0 + 1;
+        // W = V^T Zs   (nb x kk)
+        d1.push_back({V, Zs, W[g], e.lda, e.ldz, NB, nb, e.kk, m, 1.0, 0.0});
+        // W2 = T W
+        d2.push_back({e.T + (long long)b * NB * NB, W[g], W2[g], NB, NB, NB, nb, e.kk, nb, 1.0,
+                      0.0});
+        // Zs -= V W2
+        d3.push_back({V, W2[g], Zs, e.lda, NB, e.ldz, m, e.kk, nb, -1.0, 1.0});
+      }
+      if (d1.empty()) continue;
+      gemm_grouped(ctx, DType::F64, DType::F64, true, false, false, d1);
+      gemm_grouped(ctx, DType::F64, DType::F64, false, false, false, d2);
+      gemm_grouped(ctx, DType::F64, DType::F64, false, false, false, d3);
+    }
+  }
+  ctx.arena.release(mk);
+}
+
+}  // namespace hsvdcu

@@ -1,0 +1,503 @@
+"""Python mirror of the reference ``hsvd::core`` API over the B200 C ABI.
+
+Same names, argument meaning and error behaviour as the reference library
+(``/root/reference/proj/core/include/hsvd``): ``std::invalid_argument`` maps
+to ``ValueError`` and ``hsvd::DecompositionError`` to :class:`DecompositionError`.
+Every decomposition runs on the GPU through ``libhsvd_b200.so``
+(``include/hsvd_cu.h``); there is no CPU fallback -- without the library or a
+CUDA device the compute functions raise.
+
+Host-side helpers that the reference implements as plain control logic
+(``validate``, ``retained_count``, ``truncate_factor``, ``BlockPlan``,
+``reconstruct``, ``normalize_signs``) are restated here directly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+import threading
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhsvd_b200.so")
+
+OK, EINVAL, EDECOMP, ECUDA, ENCCL, ENOMEM = range(6)
+F32, F64 = 0, 1
+HOST, DEVICE = 0, 1
+COLUMN_CONCAT = "ColumnConcat"
+ROW_CONCAT = "RowConcat"
+_ORIENT = {COLUMN_CONCAT: 0, ROW_CONCAT: 1}
+
+
+class DecompositionError(RuntimeError):
+    """hsvd::DecompositionError (kernels.hpp:12-17)."""
+
+    def __init__(self, what: str, rows: int = 0, cols: int = 0):
+        super().__init__(what)
+        self.rows = rows
+        self.cols = cols
+
+
+class HsvdCudaError(RuntimeError):
+    """CUDA / NCCL / allocation failure inside the library."""
+
+
+class _Config(C.Structure):
+    _fields_ = [("gamma", C.c_double), ("row_block_rows", C.c_int64),
+                ("col_block_cols", C.c_int64), ("epsilon", C.c_double),
+                ("max_iters", C.c_int32), ("max_rank", C.c_int64)]
+
+
+class _FactorIn(C.Structure):
+    _fields_ = [("basis", C.POINTER(C.c_double)), ("dim", C.c_int64), ("rank", C.c_int64),
+                ("ld", C.c_int64), ("sigma", C.POINTER(C.c_double)),
+                ("degenerate", C.c_int32)]
+
+
+_lib = None
+_lib_lock = threading.Lock()
+
+# Every symbol include/hsvd_cu.h declares (checked by tests/test_abi.py).
+EXPORTED = [
+    "hsvd_cu_version", "hsvd_cu_last_error", "hsvd_cu_last_error_dims",
+    "hsvd_cu_ctx_create", "hsvd_cu_ctx_destroy", "hsvd_cu_ctx_stream",
+    "hsvd_cu_launch_count", "hsvd_cu_arena_bytes", "hsvd_cu_synchronize",
+    "hsvd_cu_validate", "hsvd_cu_hierarchical_svd", "hsvd_cu_recover_left_vectors",
+    "hsvd_cu_rank_k_svd", "hsvd_cu_svd_of_col_slices", "hsvd_cu_full_svd",
+    "hsvd_cu_merge_pair", "hsvd_cu_tree_merge", "hsvd_cu_result_info",
+    "hsvd_cu_result_sigma", "hsvd_cu_result_u", "hsvd_cu_result_v",
+    "hsvd_cu_result_device", "hsvd_cu_result_free",
+]
+
+
+def load_library(path: str = LIB_PATH):
+    """Loads libhsvd_b200.so (raises if it has not been built)."""
+    global _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise ImportError(
+                f"{path} is missing: build it with `make -C paper_1710_02812_b200` "
+                "(or __graft_entry__.build()); there is no CPU fallback")
+        lib = C.CDLL(path)
+        P, I64, I32, D = C.c_void_p, C.c_int64, C.c_int, C.c_double
+        pp = C.POINTER(C.c_void_p)
+        lib.hsvd_cu_version.restype = I32
+        lib.hsvd_cu_last_error.restype = C.c_char_p
+        lib.hsvd_cu_last_error_dims.argtypes = [C.POINTER(I64), C.POINTER(I64)]
+        lib.hsvd_cu_ctx_create.argtypes = [I32, pp]
+        lib.hsvd_cu_ctx_destroy.argtypes = [P]
+        lib.hsvd_cu_ctx_stream.argtypes = [P, pp]
+        lib.hsvd_cu_launch_count.argtypes = [P]
+        lib.hsvd_cu_launch_count.restype = I64
+        lib.hsvd_cu_arena_bytes.argtypes = [P]
+        lib.hsvd_cu_arena_bytes.restype = I64
+        lib.hsvd_cu_synchronize.argtypes = [P]
+        lib.hsvd_cu_validate.argtypes = [C.POINTER(_Config)]
+        xargs = [P, P, I32, I64, I64, I64, I32]
+        lib.hsvd_cu_hierarchical_svd.argtypes = xargs + [C.POINTER(_Config), pp]
+        lib.hsvd_cu_rank_k_svd.argtypes = xargs + [C.POINTER(_Config), pp]
+        lib.hsvd_cu_recover_left_vectors.argtypes = xargs + [P, I64, I64, I32, pp]
+        lib.hsvd_cu_svd_of_col_slices.argtypes = xargs + [I64, D, I64, pp]
+        lib.hsvd_cu_full_svd.argtypes = [P, P, I64, I64, I64, pp]
+        lib.hsvd_cu_merge_pair.argtypes = [P, I32, C.POINTER(_FactorIn), C.POINTER(_FactorIn),
+                                           D, I64, pp]
+        lib.hsvd_cu_tree_merge.argtypes = [P, I32, C.POINTER(_FactorIn), I64, D, I64,
+                                           C.POINTER(I64), pp]
+        lib.hsvd_cu_result_info.argtypes = [P, C.POINTER(I64), C.POINTER(C.c_int32),
+                                            C.POINTER(C.c_int32), C.POINTER(I64),
+                                            C.POINTER(I64), C.POINTER(C.c_int32)]
+        lib.hsvd_cu_result_sigma.argtypes = [P, P]
+        lib.hsvd_cu_result_u.argtypes = [P, P]
+        lib.hsvd_cu_result_v.argtypes = [P, P]
+        lib.hsvd_cu_result_device.argtypes = [P, pp, pp, C.POINTER(I64), pp, C.POINTER(I64)]
+        lib.hsvd_cu_result_free.argtypes = [P]
+        lib.hsvd_cu_result_free.restype = None
+        _lib = lib
+        return lib
+
+
+def _raise(code: int):
+    lib = load_library()
+    msg = lib.hsvd_cu_last_error().decode(errors="replace")
+    if code == EINVAL:
+        raise ValueError(msg)
+    if code == EDECOMP:
+        r, c = C.c_int64(), C.c_int64()
+        lib.hsvd_cu_last_error_dims(C.byref(r), C.byref(c))
+        raise DecompositionError(msg, r.value, c.value)
+    raise HsvdCudaError(f"[{code}] {msg}")
+
+
+def _check(code: int):
+    if code != OK:
+        _raise(code)
+
+
+# --------------------------------------------------------------------------
+# value types (svd_factor.hpp)
+# --------------------------------------------------------------------------
+
+@dataclass
+class SvdFactor:
+    """hsvd::SvdFactor (svd_factor.hpp:14-25)."""
+
+    u: Optional[np.ndarray] = None
+    sigma: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    v: Optional[np.ndarray] = None
+    degenerate: bool = False
+
+    def rank(self) -> int:
+        return int(np.asarray(self.sigma).shape[0])
+
+    def has_u(self) -> bool:
+        return self.u is not None
+
+    def has_v(self) -> bool:
+        return self.v is not None
+
+
+@dataclass
+class MatConfig:
+    """hsvd::MatConfig (svd_factor.hpp:28-35)."""
+
+    gamma: float = 1e-2
+    row_block_rows: int = 0
+    col_block_cols: int = 0
+    epsilon: float = 1e-3
+    max_iters: int = 10
+    max_rank: Optional[int] = None
+
+    def _c(self) -> _Config:
+        return _Config(float(self.gamma), int(self.row_block_rows), int(self.col_block_cols),
+                       float(self.epsilon), int(self.max_iters),
+                       int(self.max_rank) if self.max_rank is not None else 0)
+
+
+def validate(cfg: MatConfig) -> None:
+    """svd_factor.cpp:10-21."""
+    if cfg.gamma < 0.0 or not math.isfinite(cfg.gamma):
+        raise ValueError("MatConfig: gamma must be finite and >= 0")
+    if not (cfg.epsilon > 0.0):
+        raise ValueError("MatConfig: epsilon must be > 0")
+    if cfg.max_iters < 1:
+        raise ValueError("MatConfig: max_iters must be >= 1")
+    if cfg.row_block_rows < 0 or cfg.col_block_cols < 0:
+        raise ValueError("MatConfig: block sizes must be >= 0")
+    if cfg.max_rank is not None and cfg.max_rank < 1:
+        raise ValueError("MatConfig: max_rank must be >= 1")
+
+
+def retained_count(sigma, gamma: float) -> int:
+    """svd_factor.cpp:23-30."""
+    sigma = np.asarray(sigma)
+    if sigma.shape[0] == 0:
+        return 0
+    if sigma[0] == 0.0:
+        return 1
+    cutoff = gamma * sigma[0]
+    kept = int(np.argmin(sigma >= cutoff)) if not np.all(sigma >= cutoff) else sigma.shape[0]
+    return max(kept, 1)
+
+
+def truncate_factor(f: SvdFactor, gamma: float, max_rank: Optional[int] = None) -> SvdFactor:
+    """svd_factor.cpp:32-46."""
+    if np.asarray(f.sigma).shape[0] == 0:
+        raise ValueError("truncate_factor: factor has an empty spectrum")
+    keep = retained_count(f.sigma, gamma)
+    if max_rank is not None:
+        keep = min(keep, max(int(max_rank), 1))
+    return SvdFactor(u=None if f.u is None else f.u[:, :keep].copy(),
+                     sigma=np.asarray(f.sigma)[:keep].copy(),
+                     v=None if f.v is None else f.v[:, :keep].copy(),
+                     degenerate=bool(f.degenerate or f.sigma[0] == 0.0))
+
+
+def reconstruct(f: SvdFactor) -> np.ndarray:
+    """svd_factor.cpp:48-52 (host utility)."""
+    if f.u is None or f.v is None:
+        raise ValueError("reconstruct: factor must carry both u and v")
+    return (f.u * f.sigma) @ f.v.T
+
+
+def normalize_signs(f: SvdFactor) -> None:
+    """svd_factor.cpp:87-104 (host utility)."""
+    for j in range(f.rank()):
+        side = f.u if f.u is not None else f.v
+        if side is None:
+            return
+        imax = int(np.argmax(np.abs(side[:, j])))
+        if side[imax, j] < 0.0:
+            if f.u is not None:
+                f.u[:, j] = -f.u[:, j]
+            if f.v is not None:
+                f.v[:, j] = -f.v[:, j]
+
+
+def partition(extent: int, block: int):
+    """hierarchy.cpp:11-18."""
+    if block < 1 or block > extent:
+        block = extent
+    return [(s, min(block, extent - s)) for s in range(0, extent, block)]
+
+
+@dataclass
+class BlockPlan:
+    """hsvd::BlockPlan (hierarchy.hpp:18-23)."""
+
+    row_slices: list = field(default_factory=list)
+    col_slices: list = field(default_factory=list)
+
+    @staticmethod
+    def make(rows: int, cols: int, d: int, c: int) -> "BlockPlan":
+        if rows < 1 or cols < 1:
+            raise ValueError("BlockPlan: matrix must be nonempty")
+        return BlockPlan(partition(rows, d), partition(cols, c))
+
+
+@dataclass
+class MergeStats:
+    """hsvd::MergeStats (hierarchy.hpp:25-27)."""
+
+    pair_merges: int = 0
+
+
+# --------------------------------------------------------------------------
+# device context
+# --------------------------------------------------------------------------
+
+class Context:
+    """One CUDA device + stream + device arena (hsvd_cu_ctx)."""
+
+    def __init__(self, device: int = 0):
+        self.lib = load_library()
+        h = C.c_void_p()
+        _check(self.lib.hsvd_cu_ctx_create(int(device), C.byref(h)))
+        self.handle = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.lib.hsvd_cu_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def stream(self) -> int:
+        s = C.c_void_p()
+        _check(self.lib.hsvd_cu_ctx_stream(self.handle, C.byref(s)))
+        return s.value or 0
+
+    def launch_count(self) -> int:
+        return int(self.lib.hsvd_cu_launch_count(self.handle))
+
+    def arena_bytes(self) -> int:
+        return int(self.lib.hsvd_cu_arena_bytes(self.handle))
+
+    def synchronize(self):
+        _check(self.lib.hsvd_cu_synchronize(self.handle))
+
+
+_default_ctx: Optional[Context] = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(0)
+    return _default_ctx
+
+
+# --------------------------------------------------------------------------
+# marshalling
+# --------------------------------------------------------------------------
+
+def _matrix_arg(x):
+    """(pointer, dtype code, m, n, ld, where, keepalive) for numpy / torch."""
+    mod = type(x).__module__
+    if mod.startswith("torch"):
+        if x.dim() != 2:
+            raise ValueError("matrix must be 2-D")
+        if x.stride(1) != 1:
+            x = x.contiguous()
+        import torch
+        dt = {torch.float32: F32, torch.float64: F64}.get(x.dtype)
+        if dt is None:
+            raise ValueError("matrix dtype must be float32 or float64")
+        where = DEVICE if x.is_cuda else HOST
+        return (x.data_ptr(), dt, x.shape[0], x.shape[1], x.stride(0), where, x)
+    a = np.asarray(x)
+    if a.ndim != 2:
+        raise ValueError("matrix must be 2-D")
+    if a.dtype not in (np.float32, np.float64):
+        a = a.astype(np.float64)
+    if not a.flags.c_contiguous or a.strides[1] != a.itemsize:
+        a = np.ascontiguousarray(a)
+    dt = F32 if a.dtype == np.float32 else F64
+    return (a.ctypes.data, dt, a.shape[0], a.shape[1], a.strides[0] // a.itemsize, HOST, a)
+
+
+def _factor_in(f: SvdFactor, orient: str, keep: list) -> _FactorIn:
+    b = f.u if orient == COLUMN_CONCAT else f.v
+    if b is None:
+        raise ValueError(
+            "merge: ColumnConcat requires both factors to carry u" if orient == COLUMN_CONCAT
+            else "merge: RowConcat requires both factors to carry v")
+    b = np.ascontiguousarray(np.asarray(b, dtype=np.float64))
+    s = np.ascontiguousarray(np.asarray(f.sigma, dtype=np.float64))
+    if b.ndim != 2 or b.shape[1] != s.shape[0] or s.shape[0] < 1:
+        raise ValueError("merge: basis / sigma shape mismatch")
+    keep += [b, s]
+    return _FactorIn(b.ctypes.data_as(C.POINTER(C.c_double)), b.shape[0], b.shape[1],
+                     b.shape[1], s.ctypes.data_as(C.POINTER(C.c_double)),
+                     1 if f.degenerate else 0)
+
+
+def _result(ctx: Context, h: C.c_void_p, want_u=True, want_v=True) -> SvdFactor:
+    lib = ctx.lib
+    try:
+        rank, hu, hv = C.c_int64(), C.c_int32(), C.c_int32()
+        ur, vr, deg = C.c_int64(), C.c_int64(), C.c_int32()
+        _check(lib.hsvd_cu_result_info(h, C.byref(rank), C.byref(hu), C.byref(hv),
+                                       C.byref(ur), C.byref(vr), C.byref(deg)))
+        k = rank.value
+        sigma = np.empty(k)
+        _check(lib.hsvd_cu_result_sigma(h, sigma.ctypes.data))
+        u = v = None
+        if hu.value and want_u:
+            u = np.empty((ur.value, k))
+            _check(lib.hsvd_cu_result_u(h, u.ctypes.data))
+        if hv.value and want_v:
+            v = np.empty((vr.value, k))
+            _check(lib.hsvd_cu_result_v(h, v.ctypes.data))
+        return SvdFactor(u=u, sigma=sigma, v=v, degenerate=bool(deg.value))
+    finally:
+        lib.hsvd_cu_result_free(h)
+
+
+def _ctx(ctx):
+    return ctx if ctx is not None else default_context()
+
+
+# --------------------------------------------------------------------------
+# the drop-in API (hierarchy.hpp, merge.hpp, kernels.hpp)
+# --------------------------------------------------------------------------
+
+def hierarchical_svd(x, cfg: MatConfig, ctx: Optional[Context] = None) -> SvdFactor:
+    """hsvd::hierarchical_svd (hierarchy.cpp:65-94) -> (Sigma, V), u absent."""
+    validate(cfg)
+    c = _ctx(ctx)
+    p, dt, m, n, ld, where, _keep = _matrix_arg(x)
+    if m == 0 or n == 0:
+        raise ValueError("hierarchical_svd: matrix is empty")
+    h = C.c_void_p()
+    cc = cfg._c()
+    _check(c.lib.hsvd_cu_hierarchical_svd(c.handle, p, dt, m, n, ld, where, C.byref(cc),
+                                          C.byref(h)))
+    return _result(c, h)
+
+
+def recover_left_vectors(x, v_r, ctx: Optional[Context] = None) -> SvdFactor:
+    """hsvd::recover_left_vectors (hierarchy.cpp:96-112) -> (U, Sigma, V)."""
+    c = _ctx(ctx)
+    p, dt, m, n, ld, where, _keep = _matrix_arg(x)
+    vr = np.ascontiguousarray(np.asarray(v_r, dtype=np.float64))
+    if vr.ndim != 2 or vr.shape[0] != n:
+        raise ValueError("recover_left_vectors: v_r must have x.cols() rows")
+    h = C.c_void_p()
+    _check(c.lib.hsvd_cu_recover_left_vectors(c.handle, p, dt, m, n, ld, where, vr.ctypes.data,
+                                              vr.shape[1], vr.shape[1], HOST, C.byref(h)))
+    return _result(c, h)
+
+
+def rank_k_svd(x, cfg: MatConfig, ctx: Optional[Context] = None, want_u: bool = True) -> SvdFactor:
+    """hierarchical_svd + recover_left_vectors in one device-resident call."""
+    validate(cfg)
+    c = _ctx(ctx)
+    p, dt, m, n, ld, where, _keep = _matrix_arg(x)
+    h = C.c_void_p()
+    cc = cfg._c()
+    _check(c.lib.hsvd_cu_rank_k_svd(c.handle, p, dt, m, n, ld, where, C.byref(cc), C.byref(h)))
+    return _result(c, h, want_u=want_u)
+
+
+def svd_of_col_slices(x_slice, c: int, gamma: float, max_rank: Optional[int] = None,
+                      ctx: Optional[Context] = None) -> SvdFactor:
+    """hsvd::svd_of_col_slices (hierarchy.cpp:50-63) -> (U, Sigma), v absent."""
+    cx = _ctx(ctx)
+    p, dt, m, n, ld, where, _keep = _matrix_arg(x_slice)
+    h = C.c_void_p()
+    _check(cx.lib.hsvd_cu_svd_of_col_slices(cx.handle, p, dt, m, n, ld, where, int(c),
+                                            float(gamma), int(max_rank or 0), C.byref(h)))
+    return _result(cx, h)
+
+
+def full_svd(a, ctx: Optional[Context] = None) -> SvdFactor:
+    """hsvd::full_svd (kernels.cpp:21-48): thin SVD, p = min(rows, cols)."""
+    cx = _ctx(ctx)
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+    if a.ndim != 2 or a.shape[0] == 0 or a.shape[1] == 0:
+        raise ValueError("full_svd: matrix is empty")
+    h = C.c_void_p()
+    _check(cx.lib.hsvd_cu_full_svd(cx.handle, a.ctypes.data, a.shape[0], a.shape[1], a.shape[1],
+                                   C.byref(h)))
+    return _result(cx, h)
+
+
+def _merge(f1: SvdFactor, f2: SvdFactor, orient: str, gamma: float, max_rank, ctx) -> SvdFactor:
+    cx = _ctx(ctx)
+    keep: list = []
+    a = _factor_in(f1, orient, keep)
+    b = _factor_in(f2, orient, keep)
+    if a.dim != b.dim:
+        raise ValueError("merge: ColumnConcat factors must have equal row counts"
+                         if orient == COLUMN_CONCAT else
+                         "merge: RowConcat factors must have equal column counts")
+    h = C.c_void_p()
+    _check(cx.lib.hsvd_cu_merge_pair(cx.handle, _ORIENT[orient], C.byref(a), C.byref(b),
+                                     float(gamma), int(max_rank or 0), C.byref(h)))
+    return _result(cx, h)
+
+
+def merge_pair_qr(f1: SvdFactor, f2: SvdFactor, orient: str, gamma: float,
+                  max_rank: Optional[int] = None, ctx: Optional[Context] = None) -> SvdFactor:
+    """hsvd::merge_pair_qr (merge.cpp:71-117); on the GPU both merges compute
+    the SVD of [B1 S1 | B2 S2] through its (k+l)^2 Gram."""
+    return _merge(f1, f2, orient, gamma, max_rank, ctx)
+
+
+def merge_pair_naive(f1: SvdFactor, f2: SvdFactor, orient: str, gamma: float,
+                     max_rank: Optional[int] = None, ctx: Optional[Context] = None) -> SvdFactor:
+    """hsvd::merge_pair_naive (merge.cpp:42-69)."""
+    return _merge(f1, f2, orient, gamma, max_rank, ctx)
+
+
+def tree_merge(factors: Sequence[SvdFactor], orient: str, gamma: float,
+               max_rank: Optional[int] = None, stats: Optional[MergeStats] = None,
+               ctx: Optional[Context] = None) -> SvdFactor:
+    """hsvd::tree_merge (hierarchy.cpp:31-48)."""
+    factors = list(factors)
+    if not factors:
+        raise ValueError("tree_merge: factor list is empty")
+    if len(factors) == 1:
+        return factors[0]
+    cx = _ctx(ctx)
+    keep: list = []
+    arr = (_FactorIn * len(factors))(*[_factor_in(f, orient, keep) for f in factors])
+    pm = C.c_int64()
+    h = C.c_void_p()
+    _check(cx.lib.hsvd_cu_tree_merge(cx.handle, _ORIENT[orient], arr, len(factors), float(gamma),
+                                     int(max_rank or 0), C.byref(pm), C.byref(h)))
+    if stats is not None:
+        stats.pair_merges += int(pm.value)
+    return _result(cx, h)
