@@ -86,6 +86,11 @@ int64_t hsvd_cu_launch_count(const hsvd_cu_ctx* ctx);
 /* Device bytes currently reserved by the context arena. */
 int64_t hsvd_cu_arena_bytes(const hsvd_cu_ctx* ctx);
 int hsvd_cu_synchronize(hsvd_cu_ctx* ctx);
+/* Per-launch CUDA-event timing of this library's kernels (for benchmarks).
+ * report: "phase:kernel\tlaunches\ttotal_ms\n" lines since the last report;
+ * returns the bytes needed (including the NUL), or -1 on error. */
+int hsvd_cu_profile(hsvd_cu_ctx* ctx, int enable);
+int64_t hsvd_cu_profile_report(hsvd_cu_ctx* ctx, char* buf, int64_t len);
 
 /* hsvd::validate (svd_factor.cpp:10-21). */
 int hsvd_cu_validate(const hsvd_cu_config* cfg);

@@ -250,6 +250,49 @@ int64_t hsvd_cu_arena_bytes(const hsvd_cu_ctx* ctx) {
   return ctx ? (int64_t)ctx->c.arena.capacity() : 0;
 }
 
+int hsvd_cu_profile(hsvd_cu_ctx* ctx, int enable) {
+  if (!ctx) return fail(HSVD_CU_EINVAL, "null context");
+  ctx->c.profiling = enable != 0;
+  return HSVD_CU_OK;
+}
+
+int64_t hsvd_cu_profile_report(hsvd_cu_ctx* ctx, char* buf, int64_t len) {
+  if (!ctx) return -1;
+  std::string out;
+  int64_t rc = guarded([&] {
+    Ctx& c = ctx->c;
+    HSVD_CUDA(cudaSetDevice(c.device));
+    HSVD_CUDA(cudaStreamSynchronize(c.stream));
+    std::vector<std::string> order;
+    std::vector<std::pair<long long, double>> agg;
+    for (auto& r : c.prof) {
+      float ms = 0.f;
+      HSVD_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+      size_t i = 0;
+      while (i < order.size() && order[i] != r.name) ++i;
+      if (i == order.size()) {
+        order.push_back(r.name);
+        agg.push_back({0, 0.0});
+      }
+      agg[i].first += 1;
+      agg[i].second += ms;
+      c.ev_free.push_back(r.a);
+      c.ev_free.push_back(r.b);
+    }
+    c.prof.clear();
+    for (size_t i = 0; i < order.size(); ++i)
+      out += order[i] + "\t" + std::to_string(agg[i].first) + "\t" + std::to_string(agg[i].second) + "\n";
+    return HSVD_CU_OK;
+  });
+  if (rc != HSVD_CU_OK) return -1;
+  if (buf && len > 0) {
+    const size_t n = std::min<size_t>(out.size(), (size_t)len - 1);
+    std::memcpy(buf, out.data(), n);
+    buf[n] = 0;
+  }
+  return (int64_t)out.size() + 1;
+}
+
 int hsvd_cu_synchronize(hsvd_cu_ctx* ctx) {
   return guarded([&] {
     if (!ctx) throw Error(kInvalid, "null context");

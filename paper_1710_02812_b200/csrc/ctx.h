@@ -166,6 +166,38 @@ struct Ctx {
   ~Ctx() {
     if (h_ints) cudaFreeHost(h_ints);
     if (h_dbl) cudaFreeHost(h_dbl);
+    for (auto& r : prof) {
+      cudaEventDestroy(r.a);
+      cudaEventDestroy(r.b);
+    }
+    for (auto e : ev_free) cudaEventDestroy(e);
+  }
+
+  // --- per-launch CUDA-event profiler (off unless enabled) ---
+  struct ProfRec {
+    std::string name;
+    cudaEvent_t a, b;
+  };
+  bool profiling = false;
+  const char* phase = "";
+  std::vector<ProfRec> prof;
+  std::vector<cudaEvent_t> ev_free;
+  cudaEvent_t pending = nullptr;
+
+  cudaEvent_t get_event() {
+    if (!ev_free.empty()) {
+      cudaEvent_t e = ev_free.back();
+      ev_free.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    HSVD_CUDA(cudaEventCreate(&e));
+    return e;
+  }
+  void launch_begin() {
+    if (!profiling) return;
+    pending = get_event();
+    HSVD_CUDA(cudaEventRecord(pending, stream));
   }
 
   void count(int n = 1) { launches += n; }
@@ -173,7 +205,20 @@ struct Ctx {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) throw Error(kCuda, std::string(what) + ": " + cudaGetErrorString(e));
     count();
+    if (profiling && pending) {
+      cudaEvent_t b = get_event();
+      HSVD_CUDA(cudaEventRecord(b, stream));
+      prof.push_back({std::string(phase) + ":" + what, pending, b});
+      pending = nullptr;
+    }
   }
+};
+
+struct PhaseScope {
+  Ctx& c;
+  const char* prev;
+  PhaseScope(Ctx& ctx, const char* p) : c(ctx), prev(ctx.phase) { c.phase = p; }
+  ~PhaseScope() { c.phase = prev; }
 };
 
 }  // namespace hsvdcu

@@ -93,11 +93,15 @@ std::vector<DFac> block_svd_batch(Ctx& ctx, const XView& x, const std::vector<Bl
     else  // P = X_b^T Z = Xt Z  (c x kk)
       proj_w.push_back({base, m.Z, m.P, x.ld, m.q, m.s, bl.c, m.kk, bl.d, 1.0, 0.0});
   }
+  ctx.phase = "leaf.gram";
   gemm_grouped(ctx, x.dt, x.dt, false, true, true, gram_t);
   gemm_grouped(ctx, x.dt, x.dt, true, false, true, gram_w);
+  ctx.phase = "leaf.eig";
   eig_topk(ctx, ej);
+  ctx.phase = "leaf.proj";
   gemm_grouped(ctx, x.dt, DType::F64, true, false, false, proj_t);
   gemm_grouped(ctx, x.dt, DType::F64, false, false, false, proj_w);
+  ctx.phase = "leaf.fin";
   std::vector<FinJob> fj;
   for (int b = 0; b < nb; ++b) {
     Tmp& m = t[b];
@@ -206,13 +210,17 @@ std::vector<DFac> merge_batch(Ctx& ctx, const std::vector<std::pair<DFac, DFac>>
     p1.push_back({a.B, m.Zh, m.P, a.ld, m.q, m.s, m.s, m.kk, m.k1, 1.0, 0.0});
     p2.push_back({b.B, m.Zh + m.k1, m.P, b.ld, m.q, m.s, m.s, m.kk, m.k2, 1.0, 1.0});
   }
+  ctx.phase = "merge.gram";
   gemm_grouped(ctx, DType::F64, DType::F64, true, false, true, gsy);
   gemm_grouped(ctx, DType::F64, DType::F64, true, false, false, gx);
   scale_sym(ctx, ss);
+  ctx.phase = "merge.eig";
   eig_topk(ctx, ej);
+  ctx.phase = "merge.proj";
   scale_rows(ctx, sr);
   gemm_grouped(ctx, DType::F64, DType::F64, false, false, false, p1);
   gemm_grouped(ctx, DType::F64, DType::F64, false, false, false, p2);
+  ctx.phase = "merge.fin";
   std::vector<FinJob> fj;
   for (int i = 0; i < np; ++i) {
     Tmp& m = t[i];
@@ -298,10 +306,15 @@ static std::vector<DFac> vrecover_batch(Ctx& ctx, const XView& x, const std::vec
     ej.push_back({m.H, m.r, m.r, m.kk, m.lam, m.Z, m.r});
     g3.push_back({m.Bt, m.Z, m.V, n, m.r, n, n, m.kk, m.r, 1.0, 0.0});
   }
+  ctx.phase = "vrec.proj";
   gemm_grouped(ctx, x.dt, DType::F64, false, false, false, g1);
+  ctx.phase = "vrec.gram";
   gemm_grouped(ctx, DType::F64, DType::F64, true, false, true, g2);
+  ctx.phase = "vrec.eig";
   eig_topk(ctx, ej);
+  ctx.phase = "vrec.back";
   gemm_grouped(ctx, DType::F64, DType::F64, false, false, false, g3);
+  ctx.phase = "vrec.fin";
   std::vector<FinJob> fj;
   for (int j = 0; j < ns; ++j) {
     Tmp& m = t[j];
@@ -367,6 +380,7 @@ DFac recover_left_vectors(Ctx& ctx, const XView& x, const double* v_r, long long
   if (r < 1) throw Error(kInvalid, "recover_left_vectors: v_r has no columns");
   double* H = ctx.arena.alloc_n<double>((size_t)r * r);
   double* dd = ctx.arena.alloc_n<double>(1);
+  ctx.phase = "urec.check";
   gemm_grouped(ctx, DType::F64, DType::F64, true, false, true,
                {{v_r, v_r, H, ldv, ldv, r, r, r, n, 1.0, 0.0}});
   ortho_defect(ctx, H, r, r, dd);
@@ -387,12 +401,17 @@ DFac recover_left_vectors(Ctx& ctx, const XView& x, const double* v_r, long long
   double* V = ctx.arena.alloc_n<double>((size_t)n * kk);
   int* d_rd = ctx.arena.alloc_n<int>(2);
   // Y = X V_r : Xt (n x m) transposed
+  ctx.phase = "urec.proj";
   gemm_grouped(ctx, x.dt, DType::F64, true, false, false,
                {{x.X, v_r, Y, x.ld, ldv, m, m, r, n, 1.0, 0.0}});
+  ctx.phase = "urec.gram";
   gemm_grouped(ctx, DType::F64, DType::F64, true, false, true, {{Y, Y, H, m, m, r, r, r, m, 1.0, 0.0}});
+  ctx.phase = "urec.eig";
   eig_topk(ctx, {{H, r, r, kk, lam, Z, r}});
+  ctx.phase = "urec.back";
   gemm_grouped(ctx, DType::F64, DType::F64, false, false, false,
                {{Y, Z, Yh, m, r, m, m, kk, r, 1.0, 0.0}});
+  ctx.phase = "urec.fin";
   finalize(ctx, {{Yh, m, m, kk, 0.0, 0, U, m, sig, perm, d_rd, d_rd + 1, 1}});
   gather_cols(ctx, {{Zp, r, Z, r, r, kk, perm}});
   gemm_grouped(ctx, DType::F64, DType::F64, false, false, false,

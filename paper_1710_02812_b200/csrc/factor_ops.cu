@@ -255,6 +255,7 @@ void finalize(Ctx& ctx, const std::vector<FinJob>& jobs) {
   for (auto& j : jobs) pmax = std::max(pmax, j.p);
   const size_t smem = (4 * (size_t)pmax + 32) * sizeof(double) + 2 * (size_t)pmax * sizeof(int) + 64;
   HSVD_CUDA(cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ctx.launch_begin();
   k_finalize<<<(unsigned)jobs.size(), FIN_THREADS, smem, ctx.stream>>>(stage(ctx, jobs));
   ctx.check_launch("k_finalize");
 }
@@ -263,6 +264,7 @@ void scale_sym(Ctx& ctx, const std::vector<ScaleSymJob>& jobs) {
   if (jobs.empty()) return;
   long long mx = 0;
   for (auto& j : jobs) mx = std::max(mx, (long long)j.q * j.q);
+  ctx.launch_begin();
   k_scale_sym<<<dim3(grid_for(mx), (unsigned)jobs.size()), 256, 0, ctx.stream>>>(stage(ctx, jobs));
   ctx.check_launch("k_scale_sym");
 }
@@ -271,6 +273,7 @@ void scale_rows(Ctx& ctx, const std::vector<ScaleRowsJob>& jobs) {
   if (jobs.empty()) return;
   long long mx = 0;
   for (auto& j : jobs) mx = std::max(mx, (long long)j.rows * j.cols);
+  ctx.launch_begin();
   k_scale_rows<<<dim3(grid_for(mx), (unsigned)jobs.size()), 256, 0, ctx.stream>>>(stage(ctx, jobs));
   ctx.check_launch("k_scale_rows");
 }
@@ -279,11 +282,13 @@ void gather_cols(Ctx& ctx, const std::vector<GatherJob>& jobs) {
   if (jobs.empty()) return;
   long long mx = 0;
   for (auto& j : jobs) mx = std::max(mx, (long long)j.rows * j.cols);
+  ctx.launch_begin();
   k_gather<<<dim3(grid_for(mx), (unsigned)jobs.size()), 256, 0, ctx.stream>>>(stage(ctx, jobs));
   ctx.check_launch("k_gather");
 }
 
 void ortho_defect(Ctx& ctx, const double* G, long long ld, int q, double* out) {
+  ctx.launch_begin();
   k_ortho_defect<<<1, 1024, 0, ctx.stream>>>(G, ld, q, out);
   ctx.check_launch("k_ortho_defect");
 }
@@ -292,6 +297,7 @@ void rowmajor_to_colmajor(Ctx& ctx, const double* src, long long lds, int rows, 
                           double* dst, long long ldd) {
   if (rows <= 0 || cols <= 0) return;
   dim3 grid(ceil_div(cols, 32), ceil_div(rows, 32));
+  ctx.launch_begin();
   k_transpose<<<grid, dim3(32, 8), 0, ctx.stream>>>(src, lds, rows, cols, dst, ldd, 1);
   ctx.check_launch("k_transpose");
 }
@@ -300,6 +306,7 @@ void colmajor_to_rowmajor(Ctx& ctx, const double* src, long long lds, int rows, 
                           double* dst, long long ldd) {
   if (rows <= 0 || cols <= 0) return;
   dim3 grid(ceil_div(cols, 32), ceil_div(rows, 32));
+  ctx.launch_begin();
   k_transpose<<<grid, dim3(32, 8), 0, ctx.stream>>>(src, lds, rows, cols, dst, ldd, 0);
   ctx.check_launch("k_transpose");
 }

@@ -193,6 +193,7 @@ template <typename TA, typename TB>
 void launch_typed(Ctx& ctx, bool ta, bool tb, dim3 grid, const GemmDesc* dd, int syrk,
                   int splits, double* ws, long long slot) {
   cudaStream_t s = ctx.stream;
+  ctx.launch_begin();
   if (!ta && !tb) k_gemm<TA, TB, false, false><<<grid, NT, 0, s>>>(dd, syrk, splits, ws, slot);
   else if (!ta && tb) k_gemm<TA, TB, false, true><<<grid, NT, 0, s>>>(dd, syrk, splits, ws, slot);
   else if (ta && !tb) k_gemm<TA, TB, true, false><<<grid, NT, 0, s>>>(dd, syrk, splits, ws, slot);
@@ -256,6 +257,7 @@ void gemm_grouped(Ctx& ctx, DType ta, DType tb, bool trans_a, bool trans_b, bool
   if (splits > 1) {
     const long long elems = (long long)maxM * maxN;
     int bx = static_cast<int>(std::min<long long>((elems + 255) / 256, 4096));
+    ctx.launch_begin();
     k_splitk_reduce<<<dim3(bx, count), 256, 0, ctx.stream>>>(dd, splits, sy, ws, slot);
     ctx.check_launch("k_splitk_reduce");
   }

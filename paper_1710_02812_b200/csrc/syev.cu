@@ -527,6 +527,7 @@ void eig_topk(Ctx& ctx, const std::vector<EigJob>& jobs_in) {
     const size_t smem = (4 * (size_t)nmax + TRD_THREADS + 64) * sizeof(double);
     HSVD_CUDA(cudaFuncSetAttribute(k_sytrd, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));
+    ctx.launch_begin();
     k_sytrd<<<count, TRD_THREADS, smem, ctx.stream>>>(dd);
     ctx.check_launch("k_sytrd");
   }
@@ -536,6 +537,7 @@ void eig_topk(Ctx& ctx, const std::vector<EigJob>& jobs_in) {
                         (size_t)kkmax * sizeof(int) + 64;
     HSVD_CUDA(cudaFuncSetAttribute(k_steig, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));
+    ctx.launch_begin();
     k_steig<<<count, EIG_THREADS, smem, ctx.stream>>>(dd);
     ctx.check_launch("k_steig");
   }
@@ -543,9 +545,11 @@ void eig_topk(Ctx& ctx, const std::vector<EigJob>& jobs_in) {
   if (nmax > 2) {
     const long long nn = (long long)nmax * nmax;
     int gx = static_cast<int>(std::min<long long>((nn + 255) / 256, 2048));
+    ctx.launch_begin();
     k_prep_v<<<dim3(gx, count), 256, 0, ctx.stream>>>(dd);
     ctx.check_launch("k_prep_v");
     const int nblk_max = ceil_div(nmax - 1, NB);
+    ctx.launch_begin();
     k_build_t<<<dim3(nblk_max, count), 256, 0, ctx.stream>>>(dd);
     ctx.check_launch("k_build_t");
     std::vector<double*> W(count), W2(count);

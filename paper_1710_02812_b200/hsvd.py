@@ -66,6 +66,7 @@ EXPORTED = [
     "hsvd_cu_version", "hsvd_cu_last_error", "hsvd_cu_last_error_dims",
     "hsvd_cu_ctx_create", "hsvd_cu_ctx_destroy", "hsvd_cu_ctx_stream",
     "hsvd_cu_launch_count", "hsvd_cu_arena_bytes", "hsvd_cu_synchronize",
+    "hsvd_cu_profile", "hsvd_cu_profile_report",
     "hsvd_cu_validate", "hsvd_cu_hierarchical_svd", "hsvd_cu_recover_left_vectors",
     "hsvd_cu_rank_k_svd", "hsvd_cu_svd_of_col_slices", "hsvd_cu_full_svd",
     "hsvd_cu_merge_pair", "hsvd_cu_tree_merge", "hsvd_cu_result_info",
@@ -98,6 +99,9 @@ def load_library(path: str = LIB_PATH):
         lib.hsvd_cu_arena_bytes.argtypes = [P]
         lib.hsvd_cu_arena_bytes.restype = I64
         lib.hsvd_cu_synchronize.argtypes = [P]
+        lib.hsvd_cu_profile.argtypes = [P, I32]
+        lib.hsvd_cu_profile_report.argtypes = [P, C.c_char_p, I64]
+        lib.hsvd_cu_profile_report.restype = I64
         lib.hsvd_cu_validate.argtypes = [C.POINTER(_Config)]
         xargs = [P, P, I32, I64, I64, I64, I32]
         lib.hsvd_cu_hierarchical_svd.argtypes = xargs + [C.POINTER(_Config), pp]
@@ -307,6 +311,23 @@ class Context:
     def synchronize(self):
         _check(self.lib.hsvd_cu_synchronize(self.handle))
 
+    def profile(self, enable: bool = True):
+        """Per-launch CUDA-event timing of the library's kernels."""
+        _check(self.lib.hsvd_cu_profile(self.handle, 1 if enable else 0))
+
+    def profile_report(self) -> dict:
+        """{'phase:kernel': (launches, total_ms)} since the last report."""
+        need = self.lib.hsvd_cu_profile_report(self.handle, None, 0)
+        if need < 0:
+            _raise(ECUDA)
+        buf = C.create_string_buffer(int(need) + 16)
+        self.lib.hsvd_cu_profile_report(self.handle, buf, len(buf))
+        out = {}
+        for line in buf.value.decode().splitlines():
+            name, cnt, ms = line.split("\t")
+            out[name] = (int(cnt), float(ms))
+        return out
+
 
 _default_ctx: Optional[Context] = None
 
@@ -429,6 +450,22 @@ def rank_k_svd(x, cfg: MatConfig, ctx: Optional[Context] = None, want_u: bool = 
     cc = cfg._c()
     _check(c.lib.hsvd_cu_rank_k_svd(c.handle, p, dt, m, n, ld, where, C.byref(cc), C.byref(h)))
     return _result(c, h, want_u=want_u)
+
+
+def rank_k_svd_device(x, cfg: MatConfig, ctx: Context) -> int:
+    """rank_k_svd with the result left in device memory (benchmarks): returns
+    the rank; no host copies are made."""
+    p, dt, m, n, ld, where, _keep = _matrix_arg(x)
+    h = C.c_void_p()
+    cc = cfg._c()
+    _check(ctx.lib.hsvd_cu_rank_k_svd(ctx.handle, p, dt, m, n, ld, where, C.byref(cc),
+                                      C.byref(h)))
+    try:
+        rank = C.c_int64()
+        _check(ctx.lib.hsvd_cu_result_info(h, C.byref(rank), None, None, None, None, None))
+        return int(rank.value)
+    finally:
+        ctx.lib.hsvd_cu_result_free(h)
 
 
 def svd_of_col_slices(x_slice, c: int, gamma: float, max_rank: Optional[int] = None,
