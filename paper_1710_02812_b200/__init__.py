@@ -9,6 +9,6 @@ from .hsvd import (  # noqa: F401
     COLUMN_CONCAT, ROW_CONCAT, BlockPlan, Context, DecompositionError, HsvdCudaError,
     MatConfig, MergeStats, SvdFactor, default_context, full_svd, hierarchical_svd,
     load_library, merge_pair_naive, merge_pair_qr, normalize_signs, partition,
-    rank_k_svd, reconstruct, recover_left_vectors, retained_count, svd_of_col_slices,
+    rank_k_svd, rank_k_svd_device, reconstruct, recover_left_vectors, retained_count, svd_of_col_slices,
     tree_merge, truncate_factor, validate, LIB_PATH, EXPORTED,
 )
