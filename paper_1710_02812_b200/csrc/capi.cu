@@ -276,10 +276,14 @@ int64_t hsvd_cu_profile_report(hsvd_cu_ctx* ctx, char* buf, int64_t len) {
       }
       agg[i].first += 1;
       agg[i].second += ms;
-      c.ev_free.push_back(r.a);
-      c.ev_free.push_back(r.b);
     }
-    c.prof.clear();
+    if (buf && len > 0) {  // a sizing query (buf == NULL) keeps the records
+      for (auto& r : c.prof) {
+        c.ev_free.push_back(r.a);
+        c.ev_free.push_back(r.b);
+      }
+      c.prof.clear();
+    }
     for (size_t i = 0; i < order.size(); ++i)
       out += order[i] + "\t" + std::to_string(agg[i].first) + "\t" + std::to_string(agg[i].second) + "\n";
     return HSVD_CU_OK;
