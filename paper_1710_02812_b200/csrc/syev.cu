@@ -45,6 +45,8 @@ struct EigDev {
   long long ldz;
   double* piv;   // n * kk scratch (LDL^T pivots)
   double* T;     // (nblocks * NB * NB) compact-WY T factors
+  double* VW;    // n x 2*NB panel [V | W] (blocked tridiagonalisation)
+  double* WV;    // n x 2*NB panel [W | V]
 };
 
 // ---------------------------------------------------------------------------
@@ -237,6 +239,170 @@ __global__ void __launch_bounds__(TRD_THREADS) k_sytrd(const EigDev* __restrict_
     for (int i = j + 2 + tid; i < n; i += nt) vs[i] = vn[i];
     if (tid == 0) s_tau = s_tau_next;
     __syncthreads();
+  }
+}
+
+// Blocked tridiagonalisation (LAPACK dlatrd 'L' algorithm): one launch per
+// panel of NB columns.  Per column: update it with the panel's earlier
+// (v, w) pairs, form the reflector, and compute w = tau*(A22 v - V(W^T v) -
+// W(V^T v)) - ... with A22 read-only (its panel-start value).  The trailing
+// rank-2*NB update A22 -= V W^T + W V^T follows as one symmetric DMMA GEMM.
+// Thread i owns rows i, i+LAT, i+2*LAT, ... (coalesced column reads).
+constexpr int LAT = 512;
+
+template <int R>
+__global__ void __launch_bounds__(LAT) k_latrd(const EigDev* __restrict__ jobs, int j0) {
+  const EigDev J = jobs[blockIdx.x];
+  const int n = J.n;
+  const int nref = n - 1;
+  if (j0 >= nref || n <= 2) return;
+  const int nbp = min(NB, nref - j0);
+  double* A = J.A;
+  const long long lda = J.lda;
+  const double* VW = J.VW;
+  const long long ldp = n;  // panel arrays are n x 2NB, ld n
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5, nwarps = LAT >> 5;
+  extern __shared__ double sm[];
+  double* vs = sm;                 // v by global row
+  double* vrow = vs + n;           // V[j, 0:t], W[j, 0:t]
+  double* c12 = vrow + 2 * NB;     // W^T v, V^T v
+  double* red = c12 + 2 * NB;
+  __shared__ double s_alpha, s_diag;
+
+  for (int t = 0; t < nbp; ++t) {
+    const int j = j0 + t;
+    if (tid < t) {
+      vrow[tid] = VW[j + (long long)tid * ldp];
+      vrow[NB + tid] = VW[j + (long long)(NB + tid) * ldp];
+    }
+    __syncthreads();
+    // (b) column j with the panel corrections
+    double a[R];
+    double part = 0.0;
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const int i = tid + q * LAT;
+      a[q] = 0.0;
+      if (i >= j && i < n) {
+        double s = A[i + (long long)j * lda];
+        for (int u = 0; u < t; ++u)
+          s -= VW[i + (long long)u * ldp] * vrow[NB + u] + VW[i + (long long)(NB + u) * ldp] * vrow[u];
+        a[q] = s;
+        if (i == j) s_diag = s;
+        if (i == j + 1) s_alpha = s;
+        if (i >= j + 2) part += s * s;
+      }
+    }
+    const double xn2 = block_sum(part, red);
+    const double alpha = s_alpha;
+    double tau = 0.0, beta = alpha, scal = 0.0;
+    if (xn2 > 0.0) {
+      const double nrm = sqrt(alpha * alpha + xn2);
+      beta = alpha >= 0.0 ? -nrm : nrm;
+      tau = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    if (tid == 0) {
+      J.d[j] = s_diag;
+      J.e[j] = beta;
+      J.tau[j] = tau;
+    }
+    double* Vt = J.VW + (long long)t * ldp;
+    double* Vt2 = J.WV + (long long)(NB + t) * ldp;
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const int i = tid + q * LAT;
+      if (i >= j + 1 && i < n) {
+        const double v = (i == j + 1) ? 1.0 : a[q] * scal;
+        vs[i] = v;
+        Vt[i] = v;
+        Vt2[i] = v;
+        if (i >= j + 2) A[i + (long long)j * lda] = v;
+      }
+    }
+    __syncthreads();
+    // (d) p = A22 v (A22 = A[j+1:, j+1:], read-only)
+    double p[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) p[q] = 0.0;
+    int qlo = 0;
+    while (qlo < R && tid + qlo * LAT < j + 1) ++qlo;
+    if (tau != 0.0) {
+      int k = j + 1;
+      for (; k + 3 < n; k += 4) {
+        const double v0 = vs[k], v1 = vs[k + 1], v2 = vs[k + 2], v3 = vs[k + 3];
+        const double* c0 = A + (long long)k * lda;
+        const double* c1 = c0 + lda;
+        const double* c2 = c1 + lda;
+        const double* c3 = c2 + lda;
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+          const int i = tid + q * LAT;
+          if (q >= qlo && i < n)
+            p[q] += __ldg(c0 + i) * v0 + __ldg(c1 + i) * v1 + __ldg(c2 + i) * v2 +
+                    __ldg(c3 + i) * v3;
+        }
+      }
+      for (; k < n; ++k) {
+        const double vk = vs[k];
+        const double* c0 = A + (long long)k * lda;
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+          const int i = tid + q * LAT;
+          if (q >= qlo && i < n) p[q] += __ldg(c0 + i) * vk;
+        }
+      }
+    }
+    // (e) panel corrections: p -= V (W^T v) + W (V^T v)
+    if (t > 0 && tau != 0.0) {
+      for (int u = warp; u < 2 * t; u += nwarps) {
+        const double* col = J.VW + (long long)(u < t ? NB + u : u - t) * ldp;
+        double s = 0.0;
+        for (int i = j + 1 + lane; i < n; i += 32) s += col[i] * vs[i];
+        s = warp_sum(s);
+        if (lane == 0) c12[u] = s;  // c12[0:t] = W^T v, c12[t:2t] = V^T v
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        const int i = tid + q * LAT;
+        if (q >= qlo && i < n) {
+          double s = p[q];
+          for (int u = 0; u < t; ++u)
+            s -= VW[i + (long long)u * ldp] * c12[u] + VW[i + (long long)(NB + u) * ldp] * c12[t + u];
+          p[q] = s;
+        }
+      }
+    }
+    // (f) w = tau p - 1/2 tau^2 (p.v) v
+    double dp = 0.0;
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const int i = tid + q * LAT;
+      if (q >= qlo && i < n) dp += p[q] * vs[i];
+    }
+    const double dot = tau * block_sum(dp, red);
+    const double al = -0.5 * tau * dot;
+    double* Wt = J.VW + (long long)(NB + t) * ldp;
+    double* Wt2 = J.WV + (long long)t * ldp;
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const int i = tid + q * LAT;
+      if (i >= j + 1 && i < n) {
+        const double w = tau * p[q] + al * vs[i];
+        Wt[i] = w;
+        Wt2[i] = w;
+      }
+    }
+    __syncthreads();
+  }
+  if (j0 + nbp == nref && tid == 0) {
+    const int i = n - 1;
+    double s = A[(long long)i * (lda + 1)];
+    for (int u = 0; u < nbp; ++u)
+      s -= 2.0 * VW[i + (long long)u * ldp] * VW[i + (long long)(NB + u) * ldp];
+    J.d[n - 1] = s;
   }
 }
 
@@ -487,6 +653,40 @@ __global__ void __launch_bounds__(256) k_build_t(const EigDev* __restrict__ jobs
   }
 }
 
+constexpr int kBlockedMinN = 512;
+
+template <int R>
+void launch_latrd_t(Ctx& ctx, int count, size_t smem, const EigDev* dd, int j0) {
+  static bool attr = false;
+  if (!attr) {
+    HSVD_CUDA(cudaFuncSetAttribute(k_latrd<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   64 * 1024));
+    attr = true;
+  }
+  ctx.launch_begin();
+  k_latrd<R><<<count, LAT, smem, ctx.stream>>>(dd, j0);
+  ctx.check_launch("k_latrd");
+}
+
+void launch_latrd(Ctx& ctx, int R, int count, size_t smem, const EigDev* dd, int j0) {
+  if (smem > 64 * 1024) throw Error(kInvalid, "k_latrd: n too large");
+  switch (R) {
+    case 1: return launch_latrd_t<1>(ctx, count, smem, dd, j0);
+    case 2: return launch_latrd_t<2>(ctx, count, smem, dd, j0);
+    case 3: return launch_latrd_t<3>(ctx, count, smem, dd, j0);
+    case 4: return launch_latrd_t<4>(ctx, count, smem, dd, j0);
+    case 5: return launch_latrd_t<5>(ctx, count, smem, dd, j0);
+    case 6: return launch_latrd_t<6>(ctx, count, smem, dd, j0);
+    case 7:
+    case 8: return launch_latrd_t<8>(ctx, count, smem, dd, j0);
+    case 9:
+    case 10: return launch_latrd_t<10>(ctx, count, smem, dd, j0);
+    default:
+      if (R <= 12) return launch_latrd_t<12>(ctx, count, smem, dd, j0);
+      throw Error(kInvalid, "k_latrd: n > 6144 not supported");
+  }
+}
+
 }  // namespace
 
 void eig_topk(Ctx& ctx, const std::vector<EigJob>& jobs_in) {
@@ -523,7 +723,31 @@ void eig_topk(Ctx& ctx, const std::vector<EigJob>& jobs_in) {
       static_cast<const EigDev*>(ctx.staging.put(dev.data(), dev.size() * sizeof(EigDev), ctx.stream));
 
   // 1. tridiagonalise
-  {
+  if (nmax >= kBlockedMinN) {
+    for (int g = 0; g < count; ++g) {
+      dev[g].VW = ctx.arena.alloc_n<double>((size_t)dev[g].n * 2 * NB);
+      dev[g].WV = ctx.arena.alloc_n<double>((size_t)dev[g].n * 2 * NB);
+    }
+    dd = static_cast<const EigDev*>(
+        ctx.staging.put(dev.data(), dev.size() * sizeof(EigDev), ctx.stream));
+    const int R = ceil_div(nmax, LAT);
+    const size_t smem = ((size_t)nmax + 4 * NB + 64) * sizeof(double);
+    std::vector<GemmDesc> upd;
+    for (int j0 = 0; j0 < nmax - 1; j0 += NB) {
+      launch_latrd(ctx, R, count, smem, dd, j0);
+      upd.clear();
+      for (int g = 0; g < count; ++g) {
+        const EigDev& e = dev[g];
+        const int nref = e.n - 1;
+        if (e.n <= 2 || j0 + NB >= nref) continue;
+        const int j1 = j0 + NB, m = e.n - j1;
+        upd.push_back({e.VW + j1, e.WV + j1, e.A + j1 + (long long)j1 * e.lda, e.n, e.n, e.lda, m,
+                       m, 2 * NB, -1.0, 1.0});
+      }
+      // A22 -= [V W] [W V]^T  (symmetric: lower tiles + mirror)
+      gemm_grouped(ctx, DType::F64, DType::F64, false, true, true, upd);
+    }
+  } else {
     const size_t smem = (4 * (size_t)nmax + TRD_THREADS + 64) * sizeof(double);
     HSVD_CUDA(cudaFuncSetAttribute(k_sytrd, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));

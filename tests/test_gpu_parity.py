@@ -56,6 +56,26 @@ CONFIG_CASES = {
 }
 
 
+CONFIG_CASES["cfg4_small"] = (8192, 1024, 128, lambda i: i ** -2.0, 1e-3, np.float32, 4, 1, 128)
+CONFIG_CASES["cfg2_leaf1250"] = (5000, 5000, 100, lambda i: i ** -1.5, 1e-3, np.float32, 4, 4, 100)
+
+
+@pytest.mark.parametrize("shape", [(700, 600), (600, 700), (1100, 1030)])
+def test_full_svd_blocked_eigensolver(shape, H):
+    """full_svd through the blocked (n >= 512) tridiagonalisation: every
+    singular value and both bases against LAPACK."""
+    rng = np.random.default_rng(shape[0] * 7 + shape[1])
+    a = rng.standard_normal(shape) * np.exp(-np.linspace(0, 8, shape[1]))[None, :]
+    got = H.full_svd(a)
+    ref = O.full_svd(a)
+    p = min(shape)
+    assert got.rank() == p
+    assert np.abs(got.sigma - ref.sigma).max() <= 1e-10 * ref.sigma[0]
+    assert O.orthonormality_defect(got.u) < 1e-10 and O.orthonormality_defect(got.v) < 1e-10
+    rec = (got.u * got.sigma) @ got.v.T
+    assert np.linalg.norm(rec - a) <= 1e-11 * np.linalg.norm(a)
+
+
 @pytest.mark.parametrize("name", sorted(CONFIG_CASES))
 def test_config_parity_with_oracle(name, H):
     m, n, r, spec, noise, dt, P, Q, k = CONFIG_CASES[name]
