@@ -328,31 +328,37 @@ __global__ void __launch_bounds__(LAT) k_latrd(const EigDev* __restrict__ jobs, 
     for (int q = 0; q < R; ++q) p[q] = 0.0;
     int qlo = 0;
     while (qlo < R && tid + qlo * LAT < j + 1) ++qlo;
-    if (tau != 0.0) {
-      int k = j + 1;
-      for (; k + 3 < n; k += 4) {
-        const double v0 = vs[k], v1 = vs[k + 1], v2 = vs[k + 2], v3 = vs[k + 3];
-        const double* c0 = A + (long long)k * lda;
-        const double* c1 = c0 + lda;
-        const double* c2 = c1 + lda;
-        const double* c3 = c2 + lda;
+    if (tau != 0.0 && qlo < R) {
+      // Rows outside [j+1, n) read a clamped valid row and are discarded, so
+      // the inner loop is branch-free and all U*R loads issue back to back.
+      int ic[R];
 #pragma unroll
-        for (int q = 0; q < R; ++q) {
-          const int i = tid + q * LAT;
-          if (q >= qlo && i < n)
-            p[q] += __ldg(c0 + i) * v0 + __ldg(c1 + i) * v1 + __ldg(c2 + i) * v2 +
-                    __ldg(c3 + i) * v3;
+      for (int q = 0; q < R; ++q) ic[q] = min(max(tid + q * LAT, j + 1), n - 1);
+      constexpr int U = (R <= 3) ? 8 : (R <= 6 ? 6 : 3);
+      int k = j + 1;
+      for (; k + U <= n; k += U) {
+        const double* c0 = A + (long long)k * lda;
+        double x[U][R];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int q = 0; q < R; ++q) x[u][q] = __ldg(c0 + (long long)u * lda + ic[q]);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const double vk = vs[k + u];
+#pragma unroll
+          for (int q = 0; q < R; ++q) p[q] = fma(x[u][q], vk, p[q]);
         }
       }
       for (; k < n; ++k) {
         const double vk = vs[k];
         const double* c0 = A + (long long)k * lda;
 #pragma unroll
-        for (int q = 0; q < R; ++q) {
-          const int i = tid + q * LAT;
-          if (q >= qlo && i < n) p[q] += __ldg(c0 + i) * vk;
-        }
+        for (int q = 0; q < R; ++q) p[q] = fma(__ldg(c0 + ic[q]), vk, p[q]);
       }
+#pragma unroll
+      for (int q = 0; q < R; ++q)
+        if (q < qlo || tid + q * LAT >= n) p[q] = 0.0;
     }
     // (e) panel corrections: p -= V (W^T v) + W (V^T v)
     if (t > 0 && tau != 0.0) {
