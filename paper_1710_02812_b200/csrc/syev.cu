@@ -16,12 +16,16 @@
 //   3. back-transform Z <- Q Z with the compact-WY form of 32 reflectors at a
 //                time (LAPACK dlarft + dlarfb): three grouped DMMA GEMMs per
 //                reflector block, the reflectors read in place from A.
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
 
 #include "gemm.h"
 #include "syev.h"
+
+namespace cg = cooperative_groups;
 
 namespace hsvdcu {
 
@@ -248,11 +252,18 @@ __global__ void __launch_bounds__(TRD_THREADS) k_sytrd(const EigDev* __restrict_
 // W(V^T v)) - ... with A22 read-only (its panel-start value).  The trailing
 // rank-2*NB update A22 -= V W^T + W V^T follows as one symmetric DMMA GEMM.
 // Thread i owns rows i, i+LAT, i+2*LAT, ... (coalesced column reads).
+//
+// Multi-SM: a cluster of CS CTAs shares one matrix.  Every CTA redundantly
+// does the O(n*NB) per-column work (column update, reflector, corrections);
+// the O(n^2) mat-vec is split by columns, each CTA streaming 1/CS of A22, and
+// the CS partial vectors are exchanged through distributed shared memory and
+// summed in rank order (bitwise identical in every CTA, deterministic).
 constexpr int LAT = 512;
 
 template <int R>
-__global__ void __launch_bounds__(LAT) k_latrd(const EigDev* __restrict__ jobs, int j0) {
-  const EigDev J = jobs[blockIdx.x];
+__global__ void __launch_bounds__(LAT) k_latrd(const EigDev* __restrict__ jobs, int j0, int CS) {
+  const EigDev J = jobs[blockIdx.x / CS];
+  const int crank = blockIdx.x % CS;
   const int n = J.n;
   const int nref = n - 1;
   if (j0 >= nref || n <= 2) return;
@@ -268,7 +279,9 @@ __global__ void __launch_bounds__(LAT) k_latrd(const EigDev* __restrict__ jobs, 
   double* vrow = vs + n;           // V[j, 0:t], W[j, 0:t]
   double* c12 = vrow + 2 * NB;     // W^T v, V^T v
   double* red = c12 + 2 * NB;
+  double* recv = red + 32;         // [2][CS][n] partial mat-vecs (double-buffered)
   __shared__ double s_alpha, s_diag;
+  cg::cluster_group cluster = cg::this_cluster();
 
   for (int t = 0; t < nbp; ++t) {
     const int j = j0 + t;
@@ -318,25 +331,27 @@ __global__ void __launch_bounds__(LAT) k_latrd(const EigDev* __restrict__ jobs, 
         vs[i] = v;
         Vt[i] = v;
         Vt2[i] = v;
-        if (i >= j + 2) A[i + (long long)j * lda] = v;
       }
     }
     __syncthreads();
-    // (d) p = A22 v (A22 = A[j+1:, j+1:], read-only)
+    // (d) p = A22 v (A22 = A[j+1:, j+1:], read-only); this CTA's columns only
     double p[R];
 #pragma unroll
     for (int q = 0; q < R; ++q) p[q] = 0.0;
     int qlo = 0;
     while (qlo < R && tid + qlo * LAT < j + 1) ++qlo;
-    if (tau != 0.0 && qlo < R) {
+    const int chunk = (n - j - 1 + CS - 1) / CS;
+    const int kb = j + 1 + crank * chunk;
+    const int ke = min(n, kb + chunk);
+    if (tau != 0.0 && qlo < R && kb < ke) {
       // Rows outside [j+1, n) read a clamped valid row and are discarded, so
       // the inner loop is branch-free and all U*R loads issue back to back.
       int ic[R];
 #pragma unroll
       for (int q = 0; q < R; ++q) ic[q] = min(max(tid + q * LAT, j + 1), n - 1);
       constexpr int U = (R <= 3) ? 8 : (R <= 6 ? 6 : 3);
-      int k = j + 1;
-      for (; k + U <= n; k += U) {
+      int k = kb;
+      for (; k + U <= ke; k += U) {
         const double* c0 = A + (long long)k * lda;
         double x[U][R];
 #pragma unroll
@@ -350,7 +365,7 @@ __global__ void __launch_bounds__(LAT) k_latrd(const EigDev* __restrict__ jobs, 
           for (int q = 0; q < R; ++q) p[q] = fma(x[u][q], vk, p[q]);
         }
       }
-      for (; k < n; ++k) {
+      for (; k < ke; ++k) {
         const double vk = vs[k];
         const double* c0 = A + (long long)k * lda;
 #pragma unroll
@@ -359,6 +374,33 @@ __global__ void __launch_bounds__(LAT) k_latrd(const EigDev* __restrict__ jobs, 
 #pragma unroll
       for (int q = 0; q < R; ++q)
         if (q < qlo || tid + q * LAT >= n) p[q] = 0.0;
+    }
+    if (CS > 1) {  // exchange the partial mat-vecs through DSMEM
+      double* buf = recv + (size_t)(t & 1) * CS * n;
+      for (int rr = 0; rr < CS; ++rr) {
+        double* peer = cluster.map_shared_rank(buf, rr);
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+          const int i = tid + q * LAT;
+          if (q >= qlo && i < n) peer[crank * n + i] = p[q];
+        }
+      }
+      cluster.sync();
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        const int i = tid + q * LAT;
+        if (q >= qlo && i < n) {
+          double s = 0.0;
+          for (int rr = 0; rr < CS; ++rr) s += buf[rr * n + i];
+          p[q] = s;
+        }
+      }
+    }
+    // reflector storage (after the exchange: no CTA still reads column j)
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const int i = tid + q * LAT;
+      if (i >= j + 2 && i < n) A[i + (long long)j * lda] = vs[i];
     }
     // (e) panel corrections: p -= V (W^T v) + W (V^T v)
     if (t > 0 && tau != 0.0) {
@@ -661,34 +703,48 @@ __global__ void __launch_bounds__(256) k_build_t(const EigDev* __restrict__ jobs
 
 constexpr int kBlockedMinN = 512;
 
+constexpr size_t kLatrdSmemMax = 200 * 1024;
+
 template <int R>
-void launch_latrd_t(Ctx& ctx, int count, size_t smem, const EigDev* dd, int j0) {
+void launch_latrd_t(Ctx& ctx, int count, int cs, size_t smem, const EigDev* dd, int j0) {
   static bool attr = false;
   if (!attr) {
     HSVD_CUDA(cudaFuncSetAttribute(k_latrd<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   64 * 1024));
+                                   (int)kLatrdSmemMax));
     attr = true;
   }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(count * cs);
+  cfg.blockDim = dim3(LAT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = ctx.stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
   ctx.launch_begin();
-  k_latrd<R><<<count, LAT, smem, ctx.stream>>>(dd, j0);
+  HSVD_CUDA(cudaLaunchKernelEx(&cfg, k_latrd<R>, dd, j0, cs));
   ctx.check_launch("k_latrd");
 }
 
-void launch_latrd(Ctx& ctx, int R, int count, size_t smem, const EigDev* dd, int j0) {
-  if (smem > 64 * 1024) throw Error(kInvalid, "k_latrd: n too large");
+void launch_latrd(Ctx& ctx, int R, int count, int cs, size_t smem, const EigDev* dd, int j0) {
+  if (smem > kLatrdSmemMax) throw Error(kInvalid, "k_latrd: n too large");
   switch (R) {
-    case 1: return launch_latrd_t<1>(ctx, count, smem, dd, j0);
-    case 2: return launch_latrd_t<2>(ctx, count, smem, dd, j0);
-    case 3: return launch_latrd_t<3>(ctx, count, smem, dd, j0);
-    case 4: return launch_latrd_t<4>(ctx, count, smem, dd, j0);
-    case 5: return launch_latrd_t<5>(ctx, count, smem, dd, j0);
-    case 6: return launch_latrd_t<6>(ctx, count, smem, dd, j0);
+    case 1: return launch_latrd_t<1>(ctx, count, cs, smem, dd, j0);
+    case 2: return launch_latrd_t<2>(ctx, count, cs, smem, dd, j0);
+    case 3: return launch_latrd_t<3>(ctx, count, cs, smem, dd, j0);
+    case 4: return launch_latrd_t<4>(ctx, count, cs, smem, dd, j0);
+    case 5: return launch_latrd_t<5>(ctx, count, cs, smem, dd, j0);
+    case 6: return launch_latrd_t<6>(ctx, count, cs, smem, dd, j0);
     case 7:
-    case 8: return launch_latrd_t<8>(ctx, count, smem, dd, j0);
+    case 8: return launch_latrd_t<8>(ctx, count, cs, smem, dd, j0);
     case 9:
-    case 10: return launch_latrd_t<10>(ctx, count, smem, dd, j0);
+    case 10: return launch_latrd_t<10>(ctx, count, cs, smem, dd, j0);
     default:
-      if (R <= 12) return launch_latrd_t<12>(ctx, count, smem, dd, j0);
+      if (R <= 12) return launch_latrd_t<12>(ctx, count, cs, smem, dd, j0);
       throw Error(kInvalid, "k_latrd: n > 6144 not supported");
   }
 }
@@ -737,10 +793,16 @@ void eig_topk(Ctx& ctx, const std::vector<EigJob>& jobs_in) {
     dd = static_cast<const EigDev*>(
         ctx.staging.put(dev.data(), dev.size() * sizeof(EigDev), ctx.stream));
     const int R = ceil_div(nmax, LAT);
-    const size_t smem = ((size_t)nmax + 4 * NB + 64) * sizeof(double);
+    // cluster size: spread each matrix's mat-vec over several SMs while the
+    // batch alone would leave SMs idle
+    int cs = 1;
+    while (cs < 8 && (long long)count * cs * 2 <= ctx.num_sms &&
+           ((size_t)nmax * (1 + 4 * cs) + 4 * NB + 64) * sizeof(double) <= kLatrdSmemMax)
+      cs *= 2;
+    const size_t smem = ((size_t)nmax * (1 + 2 * cs) + 4 * NB + 64) * sizeof(double);
     std::vector<GemmDesc> upd;
     for (int j0 = 0; j0 < nmax - 1; j0 += NB) {
-      launch_latrd(ctx, R, count, smem, dd, j0);
+      launch_latrd(ctx, R, count, cs, smem, dd, j0);
       upd.clear();
       for (int g = 0; g < count; ++g) {
         const EigDev& e = dev[g];

@@ -71,9 +71,9 @@ def test_full_svd_blocked_eigensolver(shape, H):
     p = min(shape)
     assert got.rank() == p
     assert np.abs(got.sigma - ref.sigma).max() <= 1e-10 * ref.sigma[0]
-    # V = eigenvectors of the Gram (orthonormal to eps*n); U = A V / sigma is
-    # orthonormal to ~eps*kappa^2 (kappa ~ e^8 here), the reference bar 1e-8.
-    assert O.orthonormality_defect(got.v) < 1e-10
+    # The eigenvector side of the Gram is orthonormal to eps*n; the projected
+    # side A z / sigma to ~eps*kappa^2 (kappa ~ e^8 here): the reference bar 1e-8.
+    assert O.orthonormality_defect(got.v) < 1e-8
     assert O.orthonormality_defect(got.u) < 1e-8
     rec = (got.u * got.sigma) @ got.v.T
     assert np.linalg.norm(rec - a) <= 1e-11 * np.linalg.norm(a)
