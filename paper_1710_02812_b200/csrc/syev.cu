@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
+#include <cstdlib>
 
 #include "gemm.h"
 #include "syev.h"
@@ -799,6 +800,7 @@ void eig_topk(Ctx& ctx, const std::vector<EigJob>& jobs_in) {
     while (cs < 8 && (long long)count * cs * 2 <= ctx.num_sms &&
            ((size_t)nmax * (1 + 4 * cs) + 4 * NB + 64) * sizeof(double) <= kLatrdSmemMax)
       cs *= 2;
+    if (const char* env = std::getenv("HSVD_LATRD_CS")) cs = std::max(1, std::atoi(env));
     const size_t smem = ((size_t)nmax * (1 + 2 * cs) + 4 * NB + 64) * sizeof(double);
     std::vector<GemmDesc> upd;
     for (int j0 = 0; j0 < nmax - 1; j0 += NB) {
