@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(TRD_THREADS) k_sytrd(const EigDev* __restrict_
 constexpr int LAT = 512;
 
 template <int R>
-__global__ void __launch_bounds__(LAT) k_latrd(const EigDev* __restrict__ jobs, int j0, int CS) {
+__global__ void __launch_bounds__(LAT, 1) k_latrd(const EigDev* __restrict__ jobs, int j0, int CS) {
   const EigDev J = jobs[blockIdx.x / CS];
   const int crank = blockIdx.x % CS;
   const int n = J.n;
