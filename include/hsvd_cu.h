@@ -127,6 +127,25 @@ int hsvd_cu_tree_merge(hsvd_cu_ctx* ctx, int orient, const hsvd_cu_factor_in* fa
                        int64_t count, double gamma, int64_t max_rank, int64_t* pair_merges,
                        hsvd_cu_result** out);
 
+/* ---- multi-GPU (one process / thread per GPU, rows sharded) ---------- */
+typedef struct hsvd_cu_group hsvd_cu_group;
+/* NCCL: rank 0 creates the 128-byte id and shares it; every rank inits. */
+int hsvd_cu_nccl_unique_id(void* out128);
+int hsvd_cu_ctx_init_nccl(hsvd_cu_ctx* ctx, int rank, int world, const void* id128);
+/* In-process group of contexts driven from separate host threads. */
+int hsvd_cu_thread_group_create(int world, hsvd_cu_group** out);
+void hsvd_cu_thread_group_free(hsvd_cu_group* g);
+int hsvd_cu_ctx_join_group(hsvd_cu_ctx* ctx, hsvd_cu_group* g, int rank);
+/* Rows [row0, row0 + m_local) that `rank` must hold: its contiguous row
+ * slices of partition(m_total, d) (hierarchy.cpp:11-18). */
+int hsvd_cu_shard_rows(int64_t m_total, int64_t d, int rank, int world, int64_t* row0,
+                       int64_t* m_local);
+/* rank_k_svd over row shards.  Result: U (this rank's m_local rows), sigma
+ * and V (replicated on every rank). */
+int hsvd_cu_rank_k_svd_sharded(hsvd_cu_ctx* ctx, const void* x, int dtype, int64_t m_local,
+                               int64_t n, int64_t ldx, int where, int64_t m_total, int64_t row0,
+                               const hsvd_cu_config* cfg, hsvd_cu_result** out);
+
 /* Result accessors. */
 int hsvd_cu_result_info(const hsvd_cu_result* res, int64_t* rank, int32_t* has_u, int32_t* has_v,
                         int64_t* u_rows, int64_t* v_rows, int32_t* degenerate);

@@ -5,6 +5,7 @@
 #include <string>
 
 #include "../../include/hsvd_cu.h"
+#include "comm.h"
 #include "engine.h"
 #include "factor_ops.h"
 
@@ -13,6 +14,11 @@ using namespace hsvdcu;
 struct hsvd_cu_ctx {
   Ctx c;
   long long generation = 0;
+  std::unique_ptr<Comm> comm;
+};
+
+struct hsvd_cu_group {
+  std::shared_ptr<ThreadGroup> g;
 };
 
 struct hsvd_cu_result {
@@ -430,6 +436,78 @@ int hsvd_cu_tree_merge(hsvd_cu_ctx* ctx, int orient, const hsvd_cu_factor_in* fa
     DFac f = tree_merge_many(ctx->c, {fs}, gamma, cap_of(max_rank), &pm).front();
     if (pair_merges) *pair_merges = pm;
     *out = make_result(ctx, f, orient == HSVD_CU_COLUMN_CONCAT, false);
+    return HSVD_CU_OK;
+  });
+}
+
+int hsvd_cu_nccl_unique_id(void* out128) {
+  return guarded([&] {
+    if (!out128) throw Error(kInvalid, "out is null");
+    nccl_unique_id(out128);
+    return HSVD_CU_OK;
+  });
+}
+
+int hsvd_cu_ctx_init_nccl(hsvd_cu_ctx* ctx, int rank, int world, const void* id128) {
+  return guarded([&] {
+    if (!ctx || !id128 || world < 1 || rank < 0 || rank >= world)
+      throw Error(kInvalid, "init_nccl: bad arguments");
+    ctx->comm = make_nccl_comm(rank, world, id128, ctx->c.device);
+    ctx->c.rank = rank;
+    ctx->c.world = world;
+    return HSVD_CU_OK;
+  });
+}
+
+int hsvd_cu_thread_group_create(int world, hsvd_cu_group** out) {
+  return guarded([&] {
+    if (!out) throw Error(kInvalid, "out is null");
+    auto* g = new hsvd_cu_group();
+    g->g = make_thread_group(world);
+    *out = g;
+    return HSVD_CU_OK;
+  });
+}
+
+void hsvd_cu_thread_group_free(hsvd_cu_group* g) { delete g; }
+
+int hsvd_cu_ctx_join_group(hsvd_cu_ctx* ctx, hsvd_cu_group* g, int rank) {
+  return guarded([&] {
+    if (!ctx || !g) throw Error(kInvalid, "join_group: null argument");
+    ctx->comm = make_thread_comm(g->g, rank);
+    ctx->c.rank = rank;
+    ctx->c.world = ctx->comm->size();
+    return HSVD_CU_OK;
+  });
+}
+
+int hsvd_cu_shard_rows(int64_t m_total, int64_t d, int rank, int world, int64_t* row0,
+                       int64_t* m_local) {
+  return guarded([&] {
+    if (m_total < 1 || world < 1 || rank < 0 || rank >= world)
+      throw Error(kInvalid, "shard_rows: bad arguments");
+    long long r0 = 0, ml = 0;
+    shard_rows(m_total, d, rank, world, &r0, &ml, nullptr, nullptr);
+    if (row0) *row0 = r0;
+    if (m_local) *m_local = ml;
+    return HSVD_CU_OK;
+  });
+}
+
+int hsvd_cu_rank_k_svd_sharded(hsvd_cu_ctx* ctx, const void* x, int dtype, int64_t m_local,
+                               int64_t n, int64_t ldx, int where, int64_t m_total, int64_t row0,
+                               const hsvd_cu_config* cfg, hsvd_cu_result** out) {
+  return guarded([&] {
+    if (!out) throw Error(kInvalid, "out is null");
+    *out = nullptr;
+    if (!ctx || !ctx->comm) throw Error(kInvalid, "sharded: context has no communicator");
+    if (n <= 0 || m_total <= 0) throw Error(kInvalid, "hierarchical_svd: matrix is empty");
+    check_cfg(cfg);
+    begin(ctx);
+    XView xv{x, dtype_of(dtype), ldx > 0 ? ldx : n, m_local, n};
+    if (m_local > 0) xv = stage_x(ctx->c, x, dtype, m_local, n, ldx, where);
+    DFac f = rank_k_svd_sharded(ctx->c, *ctx->comm, xv, m_total, row0, to_cfg(cfg));
+    *out = make_result(ctx, f, true, true);
     return HSVD_CU_OK;
   });
 }

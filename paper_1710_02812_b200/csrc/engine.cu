@@ -273,7 +273,7 @@ std::vector<DFac> tree_merge_many(Ctx& ctx, std::vector<std::vector<DFac>> trees
 // ---------------------------------------------------------------------------
 // V-recovery of each row slice: SVD of U_j^T X_j through its k x k Gram
 // ---------------------------------------------------------------------------
-static std::vector<DFac> vrecover_batch(Ctx& ctx, const XView& x, const std::vector<Slice>& rows,
+std::vector<DFac> vrecover_batch(Ctx& ctx, const XView& x, const std::vector<Slice>& rows,
                                         const std::vector<DFac>& us, double gamma, int cap) {
   const int ns = static_cast<int>(rows.size());
   std::vector<DFac> out(ns);

@@ -63,9 +63,22 @@ std::vector<DFac> merge_batch(Ctx& ctx, const std::vector<std::pair<DFac, DFac>>
 std::vector<DFac> tree_merge_many(Ctx& ctx, std::vector<std::vector<DFac>> trees, double gamma,
                                   int cap, long long* pair_merges);
 
-// hierarchy.cpp:65-94 -> (sigma, V); rows of x may be a shard of the full
-// matrix in multi-GPU mode (engine handles the cross-rank levels).
+// hierarchy.cpp:83-85 for every row slice: SVD of U_j^T X_j -> (sigma, V_j).
+std::vector<DFac> vrecover_batch(Ctx& ctx, const XView& x, const std::vector<Slice>& rows,
+                                 const std::vector<DFac>& us, double gamma, int cap);
+
+// hierarchy.cpp:65-94 -> (sigma, V).
 DFac hierarchical_svd(Ctx& ctx, const XView& x, const HsvdConfig& cfg);
+
+// Row-slice ownership of rank `rank` in a world of `world` ranks.
+void shard_rows(long long m_total, long long d, int rank, int world, long long* row0,
+                long long* m_local, int* first_slice, int* last_slice);
+
+class Comm;
+// hierarchical_svd + recover_left_vectors over row shards (one rank per GPU):
+// returns U (this rank's rows) in B, V (replicated) in B2.
+DFac rank_k_svd_sharded(Ctx& ctx, Comm& comm, const XView& x_local, long long m_total,
+                        long long row0, const HsvdConfig& cfg);
 
 // hierarchy.cpp:50-63
 DFac svd_of_col_slices(Ctx& ctx, const XView& x, long long c, double gamma, int cap);

@@ -44,8 +44,12 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize(const FinJob* __restri
   for (int c = warp; c < p; c += nwarps) {
     const double* col = J.P + (long long)c * J.ldp;
     double acc = 0.0;
-    for (int r = lane; r < s; r += 32) acc += col[r] * col[r];
-    acc = warp_sum(acc);
+    if (J.norms2) {
+      acc = J.norms2[c];
+    } else {
+      for (int r = lane; r < s; r += 32) acc += col[r] * col[r];
+      acc = warp_sum(acc);
+    }
     if (lane == 0) {
       double v = sqrt(acc);
       if (!isfinite(v)) {
@@ -105,10 +109,12 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize(const FinJob* __restri
   for (int i = 0; i < wr; ++i) {
     const double* src = J.P + (long long)perm[i] * J.ldp;
     double* dst = J.U + (long long)i * J.ldu;
-    const double inv = bad[i] ? 1.0 : 1.0 / sig_new[i];
+    double inv = bad[i] ? 1.0 : 1.0 / sig_new[i];
+    if (J.norms2) inv = sig_new[i] > 0.0 ? 1.0 / sig_new[i] : 0.0;
     for (int r = tid; r < s; r += nt) dst[r] = src[r] * inv;
   }
   __syncthreads();
+  if (J.norms2) return;  // sharded: completion would need a global Gram-Schmidt
   // 5. complete unstable / null directions (rare: rank-deficient inputs)
   for (int i = 0; i < wr; ++i) {
     if (!bad[i]) continue;
@@ -192,6 +198,18 @@ __global__ void k_gather(const GatherJob* __restrict__ jobs) {
     const int sj = J.perm ? J.perm[j] : j;
     J.dst[i + j * J.ldd] = J.src[i + (long long)sj * J.lds];
   }
+}
+
+__global__ void k_colnorms2(const double* __restrict__ P, long long ld, int rows, int cols,
+                            double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (c >= cols) return;
+  const double* col = P + (long long)c * ld;
+  double acc = 0.0;
+  for (int r = lane; r < rows; r += 32) acc += col[r] * col[r];
+  acc = warp_sum(acc);
+  if (lane == 0) out[c] = acc;
 }
 
 __global__ void k_ortho_defect(const double* G, long long ld, int q, double* out) {
@@ -285,6 +303,13 @@ void gather_cols(Ctx& ctx, const std::vector<GatherJob>& jobs) {
   ctx.launch_begin();
   k_gather<<<dim3(grid_for(mx), (unsigned)jobs.size()), 256, 0, ctx.stream>>>(stage(ctx, jobs));
   ctx.check_launch("k_gather");
+}
+
+void colnorms2(Ctx& ctx, const double* P, long long ld, int rows, int cols, double* out) {
+  if (cols <= 0) return;
+  ctx.launch_begin();
+  k_colnorms2<<<ceil_div(cols, 8), 256, 0, ctx.stream>>>(P, ld, rows, cols, out);
+  ctx.check_launch("k_colnorms2");
 }
 
 void ortho_defect(Ctx& ctx, const double* G, long long ld, int q, double* out) {

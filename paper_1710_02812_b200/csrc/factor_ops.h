@@ -29,6 +29,9 @@ struct FinJob {
   int* rank;      // 1
   int* degenerate;  // 1
   int write_all;
+  // Sharded mode: squared column norms summed over all ranks (P holds this
+  // rank's rows only).  Null directions are then not completed.
+  const double* norms2 = nullptr;
 };
 void finalize(Ctx& ctx, const std::vector<FinJob>& jobs);
 
@@ -62,6 +65,9 @@ struct GatherJob {
   const int* perm;
 };
 void gather_cols(Ctx& ctx, const std::vector<GatherJob>& jobs);
+
+// out[c] = sum_r P[r, c]^2   (rows x cols)
+void colnorms2(Ctx& ctx, const double* P, long long ld, int rows, int cols, double* out);
 
 // out[0] = max |G - I| over the q x q matrix
 void ortho_defect(Ctx& ctx, const double* G, long long ld, int q, double* out);

@@ -72,6 +72,9 @@ EXPORTED = [
     "hsvd_cu_merge_pair", "hsvd_cu_tree_merge", "hsvd_cu_result_info",
     "hsvd_cu_result_sigma", "hsvd_cu_result_u", "hsvd_cu_result_v",
     "hsvd_cu_result_device", "hsvd_cu_result_free",
+    "hsvd_cu_nccl_unique_id", "hsvd_cu_ctx_init_nccl", "hsvd_cu_thread_group_create",
+    "hsvd_cu_thread_group_free", "hsvd_cu_ctx_join_group", "hsvd_cu_shard_rows",
+    "hsvd_cu_rank_k_svd_sharded",
 ]
 
 
@@ -122,6 +125,14 @@ def load_library(path: str = LIB_PATH):
         lib.hsvd_cu_result_device.argtypes = [P, pp, pp, C.POINTER(I64), pp, C.POINTER(I64)]
         lib.hsvd_cu_result_free.argtypes = [P]
         lib.hsvd_cu_result_free.restype = None
+        lib.hsvd_cu_nccl_unique_id.argtypes = [P]
+        lib.hsvd_cu_ctx_init_nccl.argtypes = [P, I32, I32, P]
+        lib.hsvd_cu_thread_group_create.argtypes = [I32, pp]
+        lib.hsvd_cu_thread_group_free.argtypes = [P]
+        lib.hsvd_cu_thread_group_free.restype = None
+        lib.hsvd_cu_ctx_join_group.argtypes = [P, P, I32]
+        lib.hsvd_cu_shard_rows.argtypes = [I64, I64, I32, I32, C.POINTER(I64), C.POINTER(I64)]
+        lib.hsvd_cu_rank_k_svd_sharded.argtypes = xargs + [I64, I64, C.POINTER(_Config), pp]
         _lib = lib
         return lib
 
@@ -327,6 +338,80 @@ class Context:
             name, cnt, ms = line.split("\t")
             out[name] = (int(cnt), float(ms))
         return out
+
+
+    # --- multi-GPU ---------------------------------------------------------
+    def init_nccl(self, rank: int, world: int, unique_id: bytes):
+        """Joins an NCCL communicator (one rank per GPU)."""
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        _check(self.lib.hsvd_cu_ctx_init_nccl(self.handle, int(rank), int(world), buf))
+
+    def join_group(self, group: "ThreadGroup", rank: int):
+        """Joins an in-process thread group (several contexts, host threads)."""
+        _check(self.lib.hsvd_cu_ctx_join_group(self.handle, group.handle, int(rank)))
+
+
+def nccl_unique_id() -> bytes:
+    lib = load_library()
+    buf = C.create_string_buffer(128)
+    _check(lib.hsvd_cu_nccl_unique_id(buf))
+    return buf.raw
+
+
+class ThreadGroup:
+    """In-process communicator group (hsvd_cu_group): lets several host
+    threads, each with its own Context, run the sharded pipeline together."""
+
+    def __init__(self, world: int):
+        self.lib = load_library()
+        h = C.c_void_p()
+        _check(self.lib.hsvd_cu_thread_group_create(int(world), C.byref(h)))
+        self.handle = h
+        self.world = world
+
+    def __del__(self):  # pragma: no cover
+        try:
+            if self.handle:
+                self.lib.hsvd_cu_thread_group_free(self.handle)
+        except Exception:
+            pass
+
+
+def shard_rows(m_total: int, d: int, rank: int, world: int):
+    """(row0, m_local): the contiguous row slices rank `rank` must hold."""
+    lib = load_library()
+    r0, ml = C.c_int64(), C.c_int64()
+    _check(lib.hsvd_cu_shard_rows(int(m_total), int(d), int(rank), int(world), C.byref(r0),
+                                  C.byref(ml)))
+    return int(r0.value), int(ml.value)
+
+
+def rank_k_svd_sharded(x_local, m_total: int, row0: int, cfg: MatConfig, ctx: Context,
+                       want_u: bool = True, fetch: bool = True):
+    """Sharded rank-k HSVD: this rank holds rows [row0, row0 + len(x_local)).
+    Returns SvdFactor with u = this rank's rows of U (or the rank if not fetch)."""
+    validate(cfg)
+    if x_local is None or (hasattr(x_local, "shape") and x_local.shape[0] == 0):
+        n = x_local.shape[1] if x_local is not None else 0
+        p, dt, m, ld, where, _keep = None, F64, 0, n, HOST, None
+        if x_local is not None and type(x_local).__module__.startswith("torch"):
+            dt = F32 if str(x_local.dtype) == "torch.float32" else F64
+        elif x_local is not None:
+            dt = F32 if np.asarray(x_local).dtype == np.float32 else F64
+    else:
+        p, dt, m, n, ld, where, _keep = _matrix_arg(x_local)
+    h = C.c_void_p()
+    cc = cfg._c()
+    _check(ctx.lib.hsvd_cu_rank_k_svd_sharded(ctx.handle, p, dt, m, n, ld, where, int(m_total),
+                                              int(row0), C.byref(cc), C.byref(h)))
+    if not fetch:
+        try:
+            rank = C.c_int64()
+            _check(ctx.lib.hsvd_cu_result_info(h, C.byref(rank), None, None, None, None, None))
+            return int(rank.value)
+        finally:
+            ctx.lib.hsvd_cu_result_free(h)
+    return _result(ctx, h, want_u=want_u)
 
 
 _default_ctx: Optional[Context] = None

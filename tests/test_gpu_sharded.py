@@ -1,0 +1,58 @@
+"""The sharded (multi-GPU) device pipeline, driven on one B200 by an
+in-process thread group: every rank is a host thread with its own context
+and stream; ranks exchange through host-synchronised device copies (no
+device-side waits between ranks).  The result must equal the single-context
+rank_k_svd: the row-phase tree keeps the reference pairing, so sigma and V
+agree to roundoff of the all-reduced Gram."""
+import threading
+
+import numpy as np
+import pytest
+
+import hsvd_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _run_group(H, x, cfg, world):
+    grp = H.ThreadGroup(world)
+    out = [None] * world
+    err = []
+
+    def body(rank):
+        try:
+            ctx = H.Context(0)
+            ctx.join_group(grp, rank)
+            r0, ml = H.shard_rows(x.shape[0], cfg.row_block_rows, rank, world)
+            out[rank] = (r0, ml, H.rank_k_svd_sharded(x[r0:r0 + ml], x.shape[0], r0, cfg, ctx))
+        except Exception as e:  # pragma: no cover
+            err.append(repr(e))
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    assert not err, err
+    return out
+
+
+@pytest.mark.parametrize("world,P,Q", [(1, 4, 2), (2, 4, 2), (3, 8, 2), (4, 6, 1)])
+def test_sharded_equals_single(world, P, Q):
+    import paper_1710_02812_b200 as H
+    rng = np.random.default_rng(11 + world)
+    m, n, k = 1536, 768, 40
+    x = ((np.linalg.qr(rng.standard_normal((m, 60)))[0] * (1.0 / np.arange(1, 61))) @
+         np.linalg.qr(rng.standard_normal((n, 60)))[0].T +
+         1e-3 * rng.standard_normal((m, n))).astype(np.float32)
+    cfg = H.MatConfig(gamma=1e-12, row_block_rows=m // P, col_block_cols=n // Q, max_rank=k)
+    single = H.rank_k_svd(x, cfg)
+    res = _run_group(H, x, cfg, world)
+    u = np.vstack([r[2].u for r in res if r[1] > 0])
+    assert sum(r[1] for r in res) == m
+    for r0, ml, f in res:
+        assert f.rank() == single.rank() == k
+        assert np.abs(f.sigma - single.sigma).max() <= 1e-11 * single.sigma[0]
+        assert O.largest_principal_angle(single.v, f.v) < 1e-9
+    assert O.largest_principal_angle(single.u, u) < 1e-9
+    assert O.orthonormality_defect(u) < 1e-8
