@@ -56,3 +56,20 @@ def test_sharded_equals_single(world, P, Q):
         assert O.largest_principal_angle(single.v, f.v) < 1e-9
     assert O.largest_principal_angle(single.u, u) < 1e-9
     assert O.orthonormality_defect(u) < 1e-8
+
+
+def test_nccl_world1_path():
+    """The NCCL communicator (dlopen'd libnccl) at world size 1 runs the same
+    sharded code path as the multi-GPU bench."""
+    import paper_1710_02812_b200 as H
+    rng = np.random.default_rng(3)
+    m, n, k = 1024, 512, 24
+    x = (rng.standard_normal((m, 30)) @ rng.standard_normal((30, n)) +
+         1e-3 * rng.standard_normal((m, n))).astype(np.float32)
+    cfg = H.MatConfig(gamma=1e-12, row_block_rows=m // 4, col_block_cols=n // 2, max_rank=k)
+    single = H.rank_k_svd(x, cfg)
+    ctx = H.Context(0)
+    ctx.init_nccl(0, 1, H.nccl_unique_id())
+    f = H.rank_k_svd_sharded(x, m, 0, cfg, ctx)
+    assert np.abs(f.sigma - single.sigma).max() <= 1e-11 * single.sigma[0]
+    assert O.largest_principal_angle(single.u, f.u) < 1e-9
