@@ -20,38 +20,68 @@ namespace hsvdcu {
 namespace {
 
 constexpr int FIN_THREADS = 256;
+constexpr int NORM_CHUNK = 8192;  // rows per partial column norm
 
-__global__ void __launch_bounds__(FIN_THREADS) k_finalize(const FinJob* __restrict__ jobs) {
-  const FinJob J = jobs[blockIdx.x];
-  const int s = J.s, p = J.p;
+// Scratch of one finalisation (allocated by finalize()).
+struct FinDev {
+  FinJob j;
+  double* part;   // nchunk x p partial squared norms
+  int nchunk;
+  double* scale;  // p: 1/sigma (1 for columns needing completion)
+  int* info;      // [0] columns to write, [1] any column needs completion
+};
+
+// 1. partial squared column norms: block (chunk, column, job)
+__global__ void k_colnorm_part(const FinDev* __restrict__ jobs) {
+  const FinDev F = jobs[blockIdx.z];
+  const int c = blockIdx.y, ch = blockIdx.x;
+  if (c >= F.j.p || ch >= F.nchunk || F.j.norms2) return;
+  const double* col = F.j.P + (long long)c * F.j.ldp;
+  const int r0 = ch * NORM_CHUNK, r1 = min(F.j.s, r0 + NORM_CHUNK);
+  double acc = 0.0;
+  for (int r = r0 + threadIdx.x; r < r1; r += blockDim.x) acc += col[r] * col[r];
+  __shared__ double red[32];
+  acc = block_sum(acc, red);
+  if (threadIdx.x == 0) F.part[(long long)ch * F.j.p + c] = acc;
+}
+
+// 3. U[:, i] = P[:, perm[i]] * scale[i] for the written columns
+__global__ void k_scale_gather(const FinDev* __restrict__ jobs) {
+  const FinDev F = jobs[blockIdx.z];
+  const int i = blockIdx.y;
+  if (i >= F.info[0]) return;
+  const int src = F.j.perm[i];
+  const double sc = F.scale[i];
+  const double* in = F.j.P + (long long)src * F.j.ldp;
+  double* out = F.j.U + (long long)i * F.j.ldu;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < F.j.s; r += gridDim.x * blockDim.x)
+    out[r] = in[r] * sc;
+}
+
+// 2. sort, truncation count, scales (one CTA per job)
+__global__ void __launch_bounds__(FIN_THREADS) k_finalize(const FinDev* __restrict__ jobs) {
+  const FinDev F = jobs[blockIdx.x];
+  const FinJob J = F.j;
+  const int p = J.p;
   const int tid = threadIdx.x, nt = blockDim.x;
-  const int lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
   extern __shared__ double sm[];
   double* sig_old = sm;
   double* sig_new = sig_old + p;
-  double* dots = sig_new + p;
-  double* red = dots + p;
-  int* perm = reinterpret_cast<int*>(red + 32);
-  int* bad = perm + p;
-  __shared__ int s_keep, s_write;
+  int* perm = reinterpret_cast<int*>(sig_new + p);
   __shared__ double s_smax;
-
-  // 1. column norms
   __shared__ int s_nan;
   if (tid == 0) s_nan = 0;
   for (int i = tid; i < p; i += nt) perm[i] = i;
   __syncthreads();
-  for (int c = warp; c < p; c += nwarps) {
-    const double* col = J.P + (long long)c * J.ldp;
+  for (int c = tid; c < p; c += nt) {
     double acc = 0.0;
     if (J.norms2) {
       acc = J.norms2[c];
     } else {
-      for (int r = lane; r < s; r += 32) acc += col[r] * col[r];
-      acc = warp_sum(acc);
+      for (int ch = 0; ch < F.nchunk; ++ch) acc += F.part[(long long)ch * p + c];
     }
-    if (lane == 0) {
-      double v = sqrt(acc);
+    {
+      double v = std::sqrt(acc);
       if (!isfinite(v)) {
         v = -1.0;
         s_nan = 1;
@@ -90,32 +120,46 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize(const FinJob* __restri
       if (keep < 1) keep = 1;
     }
     if (J.cap > 0 && keep > J.cap) keep = J.cap;
-    s_keep = keep;
-    s_write = J.write_all ? p : keep;
     s_smax = smax;
     *J.rank = keep;
     *J.degenerate = deg;
+    F.info[0] = J.write_all ? p : keep;
+    F.info[1] = 0;
   }
   __syncthreads();
-  const int wr = s_write;
   const double smax = s_smax;
+  const int wr = F.info[0];
+  int anybad = 0;
   for (int i = tid; i < p; i += nt) {
     J.sigma[i] = sig_new[i];
-    if (J.perm) J.perm[i] = perm[i];
-    bad[i] = !(sig_new[i] > 1e-6 * smax) || smax == 0.0;
-  }
-  __syncthreads();
-  // 4. normalised columns
-  for (int i = 0; i < wr; ++i) {
-    const double* src = J.P + (long long)perm[i] * J.ldp;
-    double* dst = J.U + (long long)i * J.ldu;
-    double inv = bad[i] ? 1.0 : 1.0 / sig_new[i];
+    J.perm[i] = perm[i];
+    const bool bad = !(sig_new[i] > 1e-6 * smax) || smax == 0.0;
+    double inv = bad ? 1.0 : 1.0 / sig_new[i];
+    // sharded: completion would need a global Gram-Schmidt (zero column instead)
     if (J.norms2) inv = sig_new[i] > 0.0 ? 1.0 / sig_new[i] : 0.0;
-    for (int r = tid; r < s; r += nt) dst[r] = src[r] * inv;
+    F.scale[i] = inv;
+    if (bad && i < wr && !J.norms2) anybad = 1;
   }
+  if (anybad) atomicOr(&F.info[1], 1);
+}
+
+// 4. complete unstable / null directions in sigma order (rare: rank-deficient
+// inputs; the kernel exits at once otherwise)
+__global__ void __launch_bounds__(FIN_THREADS) k_complete(const FinDev* __restrict__ jobs) {
+  const FinDev F = jobs[blockIdx.x];
+  if (F.info[1] == 0) return;
+  const FinJob J = F.j;
+  const int s = J.s, p = J.p;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
+  extern __shared__ double sm[];
+  double* dots = sm;
+  double* red = dots + p;
+  int* bad = reinterpret_cast<int*>(red + 32);
+  const int wr = F.info[0];
+  const double smax = J.sigma[0];
+  for (int i = tid; i < p; i += nt) bad[i] = !(J.sigma[i] > 1e-6 * smax) || smax == 0.0;
   __syncthreads();
-  if (J.norms2) return;  // sharded: completion would need a global Gram-Schmidt
-  // 5. complete unstable / null directions (rare: rank-deficient inputs)
   for (int i = 0; i < wr; ++i) {
     if (!bad[i]) continue;
     double* ui = J.U + (long long)i * J.ldu;
@@ -269,13 +313,39 @@ int grid_for(long long elems) {
 
 void finalize(Ctx& ctx, const std::vector<FinJob>& jobs) {
   if (jobs.empty()) return;
-  int pmax = 0;
-  for (auto& j : jobs) pmax = std::max(pmax, j.p);
-  const size_t smem = (4 * (size_t)pmax + 32) * sizeof(double) + 2 * (size_t)pmax * sizeof(int) + 64;
+  int pmax = 0, chmax = 1, smax = 1;
+  std::vector<FinDev> dev(jobs.size());
+  for (size_t i = 0; i < jobs.size(); ++i) {
+    FinDev& f = dev[i];
+    f.j = jobs[i];
+    if (!f.j.perm) f.j.perm = ctx.arena.alloc_n<int>(f.j.p);
+    f.nchunk = std::max(1, ceil_div(f.j.s, NORM_CHUNK));
+    f.part = ctx.arena.alloc_n<double>((size_t)f.nchunk * f.j.p);
+    f.scale = ctx.arena.alloc_n<double>(f.j.p);
+    f.info = ctx.arena.alloc_n<int>(2);
+    pmax = std::max(pmax, f.j.p);
+    chmax = std::max(chmax, f.nchunk);
+    smax = std::max(smax, f.j.s);
+  }
+  const FinDev* dd = stage(ctx, dev);
+  const unsigned nj = (unsigned)dev.size();
+  ctx.launch_begin();
+  k_colnorm_part<<<dim3(chmax, pmax, nj), 256, 0, ctx.stream>>>(dd);
+  ctx.check_launch("k_colnorm_part");
+  const size_t smem = 2 * (size_t)pmax * sizeof(double) + (size_t)pmax * sizeof(int) + 64;
   HSVD_CUDA(cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   ctx.launch_begin();
-  k_finalize<<<(unsigned)jobs.size(), FIN_THREADS, smem, ctx.stream>>>(stage(ctx, jobs));
+  k_finalize<<<nj, FIN_THREADS, smem, ctx.stream>>>(dd);
   ctx.check_launch("k_finalize");
+  const int gx = std::min(ceil_div(smax, 256 * 4), 64);
+  ctx.launch_begin();
+  k_scale_gather<<<dim3(gx, pmax, nj), 256, 0, ctx.stream>>>(dd);
+  ctx.check_launch("k_scale_gather");
+  const size_t smem2 = ((size_t)pmax + 32) * sizeof(double) + (size_t)pmax * sizeof(int) + 64;
+  HSVD_CUDA(cudaFuncSetAttribute(k_complete, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+  ctx.launch_begin();
+  k_complete<<<nj, FIN_THREADS, smem2, ctx.stream>>>(dd);
+  ctx.check_launch("k_complete");
 }
 
 void scale_sym(Ctx& ctx, const std::vector<ScaleSymJob>& jobs) {

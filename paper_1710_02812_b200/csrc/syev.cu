@@ -49,7 +49,8 @@ struct EigDev {
   double* Z;
   long long ldz;
   double* piv;   // n * kk scratch (LDL^T pivots)
-  double* T;     // (nblocks * NB * NB) compact-WY T factors
+  double* T;     // (nblocks * NBT * NBT) compact-WY T factors
+  double* S;     // (nblocks * NBT * NBT) V^T V of each reflector block
   double* VW;    // n x 2*NB panel [V | W] (blocked tridiagonalisation)
   double* WV;    // n x 2*NB panel [W | V]
 };
@@ -659,46 +660,39 @@ __global__ void k_prep_v(const EigDev* __restrict__ jobs) {
   }
 }
 
-// T factor (dlarft, forward, columnwise) of every reflector block.
-__global__ void __launch_bounds__(256) k_build_t(const EigDev* __restrict__ jobs) {
+// T factor (dlarft, forward, columnwise) of every reflector block of NBT
+// reflectors, from S = V^T V (computed by a grouped DMMA GEMM beforehand).
+constexpr int NBT = 128;
+
+__global__ void __launch_bounds__(NBT) k_build_t(const EigDev* __restrict__ jobs) {
   const EigDev J = jobs[blockIdx.y];
   const int b = blockIdx.x;
   const int nref = J.n - 1;
-  const int j0 = b * NB;
+  const int j0 = b * NBT;
   if (j0 >= nref) return;
-  const int nb = min(NB, nref - j0);
-  __shared__ double S[NB][NB + 1];
-  __shared__ double T[NB][NB + 1];
-  __shared__ double tau[NB];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-  if (tid < NB) tau[tid] = tid < nb ? J.tau[j0 + tid] : 0.0;
-  // S = V^T V over rows j0+1..n-1 (V stored in A columns j0..j0+nb-1)
-  for (int pq = warp; pq < nb * nb; pq += nwarps) {
-    const int p = pq / nb, q = pq % nb;
-    if (p > q) continue;
-    const double* vp = J.A + (long long)(j0 + p) * J.lda;
-    const double* vq = J.A + (long long)(j0 + q) * J.lda;
-    double s = 0.0;
-    for (int r = j0 + 1 + q + lane; r < J.n; r += 32) s += vp[r] * vq[r];
-    s = warp_sum(s);
-    if (lane == 0) S[p][q] = s;
-  }
-  for (int e = tid; e < NB * NB; e += blockDim.x) T[e / NB][e % NB] = 0.0;
+  const int nb = min(NBT, nref - j0);
+  extern __shared__ double sm[];
+  double* T = sm;                      // NBT x (NBT+1), row i at T[i*(NBT+1)]
+  double* tau = T + NBT * (NBT + 1);
+  const double* S = J.S + (long long)b * NBT * NBT;  // column-major, ld NBT
+  const int tid = threadIdx.x;
+  tau[tid] = tid < nb ? J.tau[j0 + tid] : 0.0;
+  for (int e = tid; e < NBT * (NBT + 1); e += blockDim.x) T[e] = 0.0;
   __syncthreads();
   for (int t = 0; t < nb; ++t) {
     // T[i,t] = -tau_t * sum_{l=i}^{t-1} T[i,l] S[l,t]
     if (tid < t) {
       double s = 0.0;
-      for (int l = tid; l < t; ++l) s += T[tid][l] * S[l][t];
-      T[tid][t] = -tau[t] * s;
+      for (int l = tid; l < t; ++l) s += T[tid * (NBT + 1) + l] * S[l + t * NBT];
+      T[tid * (NBT + 1) + t] = -tau[t] * s;
     }
-    if (tid == 0) T[t][t] = tau[t];
+    if (tid == 0) T[t * (NBT + 1) + t] = tau[t];
     __syncthreads();
   }
-  double* out = J.T + (long long)b * NB * NB;
-  for (int e = tid; e < NB * NB; e += blockDim.x) {
-    const int i = e % NB, j = e / NB;  // column-major
-    out[e] = T[i][j];
+  double* out = J.T + (long long)b * NBT * NBT;
+  for (int e = tid; e < NBT * NBT; e += blockDim.x) {
+    const int i = e % NBT, j = e / NBT;  // column-major
+    out[e] = T[i * (NBT + 1) + j];
   }
 }
 
@@ -777,8 +771,9 @@ void eig_topk(Ctx& ctx, const std::vector<EigJob>& jobs_in) {
     d.Z = j.Z;
     d.ldz = j.ldz;
     d.piv = ctx.arena.alloc_n<double>((size_t)j.n * j.kk);
-    const int nblk = std::max(1, ceil_div(j.n - 1, NB));
-    d.T = ctx.arena.alloc_n<double>((size_t)nblk * NB * NB);
+    const int nblk = std::max(1, ceil_div(j.n - 1, NBT));
+    d.T = ctx.arena.alloc_n<double>((size_t)nblk * NBT * NBT);
+    d.S = ctx.arena.alloc_n<double>((size_t)nblk * NBT * NBT);
     nmax = std::max(nmax, j.n);
     kkmax = std::max(kkmax, j.kk);
   }
@@ -842,18 +837,33 @@ void eig_topk(Ctx& ctx, const std::vector<EigJob>& jobs_in) {
     ctx.launch_begin();
     k_prep_v<<<dim3(gx, count), 256, 0, ctx.stream>>>(dd);
     ctx.check_launch("k_prep_v");
-    const int nblk_max = ceil_div(nmax - 1, NB);
+    const int nblk_max = ceil_div(nmax - 1, NBT);
+    // S_b = V_b^T V_b for every block of every matrix (one grouped launch)
+    std::vector<GemmDesc> ds;
+    for (int g = 0; g < count; ++g) {
+      const EigDev& e = dev[g];
+      if (e.n <= 2) continue;
+      for (int b = 0; b * NBT < e.n - 1; ++b) {
+        const int j0 = b * NBT, nb = std::min(NBT, e.n - 1 - j0), m = e.n - j0 - 1;
+        const double* V = e.A + j0 + 1 + (long long)j0 * e.lda;
+        ds.push_back({V, V, e.S + (long long)b * NBT * NBT, e.lda, e.lda, NBT, nb, nb, m, 1.0,
+                      0.0});
+      }
+    }
+    gemm_grouped(ctx, DType::F64, DType::F64, true, false, true, ds);
+    const size_t tsm = ((size_t)NBT * (NBT + 1) + NBT) * sizeof(double);
+    HSVD_CUDA(cudaFuncSetAttribute(k_build_t, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
     ctx.launch_begin();
-    k_build_t<<<dim3(nblk_max, count), 256, 0, ctx.stream>>>(dd);
+    k_build_t<<<dim3(nblk_max, count), NBT, tsm, ctx.stream>>>(dd);
     ctx.check_launch("k_build_t");
     std::vector<double*> W(count), W2(count);
     for (int g = 0; g < count; ++g) {
-      W[g] = ctx.arena.alloc_n<double>((size_t)NB * jobs[g].kk);
-      W2[g] = ctx.arena.alloc_n<double>((size_t)NB * jobs[g].kk);
+      W[g] = ctx.arena.alloc_n<double>((size_t)NBT * jobs[g].kk);
+      W2[g] = ctx.arena.alloc_n<double>((size_t)NBT * jobs[g].kk);
     }
     std::vector<GemmDesc> d1, d2, d3;
     for (int b = nblk_max - 1; b >= 0; --b) {
-      const int j0 = b * NB;
+      const int j0 = b * NBT;
       d1.clear();
       d2.clear();
       d3.clear();
@@ -862,16 +872,16 @@ void eig_topk(Ctx& ctx, const std::vector<EigJob>& jobs_in) {
         const int nref = e.n - 1;
         if (j0 >= nref || e.n <= 2) continue;
         const int m = e.n - j0 - 1;
-        const int nb = std::min(NB, nref - j0);
+        const int nb = std::min(NBT, nref - j0);
         const double* V = e.A + j0 + 1 + (long long)j0 * e.lda;
         double* Zs = e.Z + j0 + 1;
         // W = V^T Zs   (nb x kk)
-        d1.push_back({V, Zs, W[g], e.lda, e.ldz, NB, nb, e.kk, m, 1.0, 0.0});
+        d1.push_back({V, Zs, W[g], e.lda, e.ldz, NBT, nb, e.kk, m, 1.0, 0.0});
         // W2 = T W
-        d2.push_back({e.T + (long long)b * NB * NB, W[g], W2[g], NB, NB, NB, nb, e.kk, nb, 1.0,
-                      0.0});
+        d2.push_back({e.T + (long long)b * NBT * NBT, W[g], W2[g], NBT, NBT, NBT, nb, e.kk, nb,
+                      1.0, 0.0});
         // Zs -= V W2
-        d3.push_back({V, W2[g], Zs, e.lda, NB, e.ldz, m, e.kk, nb, -1.0, 1.0});
+        d3.push_back({V, W2[g], Zs, e.lda, NBT, e.ldz, m, e.kk, nb, -1.0, 1.0});
       }
       if (d1.empty()) continue;
       gemm_grouped(ctx, DType::F64, DType::F64, true, false, false, d1);
