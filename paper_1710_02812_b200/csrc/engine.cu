@@ -32,6 +32,21 @@ void check_decomp(const std::vector<int>& deg, const std::vector<std::pair<long 
 
 }  // namespace
 
+// B (rows x k) nearly orthonormal -> B R^{-1} with B^T B = R^T R.
+double* reorthonormalize(Ctx& ctx, const double* B, long long ld, int rows, int k) {
+  const char* ph = ctx.phase;
+  ctx.phase = "reorth";
+  double* C = ctx.arena.alloc_n<double>((size_t)k * k);
+  double* Ri = ctx.arena.alloc_n<double>((size_t)k * k);
+  double* out = ctx.arena.alloc_n<double>((size_t)rows * k);
+  gemm_grouped(ctx, DType::F64, DType::F64, true, false, true, {{B, B, C, ld, ld, k, k, k, rows, 1.0, 0.0}});
+  chol_inverse(ctx, C, k, Ri);
+  gemm_grouped(ctx, DType::F64, DType::F64, false, false, false,
+               {{B, Ri, out, ld, k, rows, rows, k, k, 1.0, 0.0}});
+  ctx.phase = ph;
+  return out;
+}
+
 std::vector<Slice> partition(long long extent, long long block) {
   if (block < 1 || block > extent) block = extent;
   std::vector<Slice> out;
@@ -372,7 +387,10 @@ DFac hierarchical_svd(Ctx& ctx, const XView& x, const HsvdConfig& cfg) {
   for (int j = 0; j < P; ++j) trees[j].assign(leaves.begin() + j * Q, leaves.begin() + (j + 1) * Q);
   std::vector<DFac> us = tree_merge_many(ctx, trees, cfg.gamma, cfg.cap, nullptr);
   std::vector<DFac> vs = vrecover_batch(ctx, x, rows, us, cfg.gamma, cfg.cap);
-  return tree_merge_many(ctx, {vs}, cfg.gamma, cfg.cap, nullptr).front();
+  DFac root = tree_merge_many(ctx, {vs}, cfg.gamma, cfg.cap, nullptr).front();
+  root.B = reorthonormalize(ctx, root.B, root.ld, root.dim, root.rank);
+  root.ld = root.dim;
+  return root;
 }
 
 DFac recover_left_vectors(Ctx& ctx, const XView& x, const double* v_r, long long ldv, int r) {
@@ -423,7 +441,7 @@ DFac recover_left_vectors(Ctx& ctx, const XView& x, const double* v_r, long long
                 "SVD did not converge for a " + std::to_string(m) + "x" + std::to_string(r) + " matrix",
                 m, r);
   DFac f;
-  f.B = U;
+  f.B = reorthonormalize(ctx, U, m, m, kk);
   f.ld = m;
   f.dim = m;
   f.rank = kk;

@@ -67,6 +67,9 @@ std::vector<DFac> tree_merge_many(Ctx& ctx, std::vector<std::vector<DFac>> trees
 std::vector<DFac> vrecover_batch(Ctx& ctx, const XView& x, const std::vector<Slice>& rows,
                                  const std::vector<DFac>& us, double gamma, int cap);
 
+// Nearly orthonormal B (rows x k) -> B R^{-1}, B^T B = R^T R (new buffer).
+double* reorthonormalize(Ctx& ctx, const double* B, long long ld, int rows, int k);
+
 // hierarchy.cpp:65-94 -> (sigma, V).
 DFac hierarchical_svd(Ctx& ctx, const XView& x, const HsvdConfig& cfg);
 

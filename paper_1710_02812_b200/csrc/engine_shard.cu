@@ -178,7 +178,8 @@ DFac rank_k_svd_sharded(Ctx& ctx, Comm& comm, const XView& xl, long long m_total
   HSVD_CUDA(cudaMemcpyAsync(&hr, hb, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
   HSVD_CUDA(cudaStreamSynchronize(ctx.stream));
   const int r = static_cast<int>(hr);
-  double* vr = (me == root) ? cur[0].f.B : ctx.arena.alloc_n<double>((size_t)n * r);
+  double* vr = (me == root) ? reorthonormalize(ctx, cur[0].f.B, cur[0].f.ld, n, r)
+                            : ctx.arena.alloc_n<double>((size_t)n * r);
   comm.bcast(ctx, vr, (size_t)n * r * sizeof(double), root);
 
   // 4. U-recovery with all-reduced Gram and column norms (hierarchy.cpp:96-112)
@@ -234,8 +235,21 @@ DFac rank_k_svd_sharded(Ctx& ctx, Comm& comm, const XView& xl, long long m_total
   if (rd[1] == 2)
     throw Error(kDecomposition, "SVD did not converge for a " + std::to_string(m_total) + "x" +
                                     std::to_string(r) + " matrix", m_total, r);
+  // U orthonormal to eps: C = sum over ranks of U_g^T U_g = R^T R, U_g <- U_g R^{-1}
+  double* C = ctx.arena.alloc_n<double>((size_t)kk * kk);
+  double* Ri = ctx.arena.alloc_n<double>((size_t)kk * kk);
+  double* U2 = ctx.arena.alloc_n<double>((size_t)std::max(ml, 1) * kk);
+  ctx.phase = "reorth";
+  if (ml > 0)
+    gemm_grouped(ctx, DType::F64, DType::F64, true, false, true, {{U, U, C, ml, ml, kk, kk, kk, ml, 1.0, 0.0}});
+  else
+    HSVD_CUDA(cudaMemsetAsync(C, 0, (size_t)kk * kk * sizeof(double), ctx.stream));
+  comm.allreduce_sum(ctx, C, (size_t)kk * kk);
+  chol_inverse(ctx, C, kk, Ri);
+  if (ml > 0)
+    gemm_grouped(ctx, DType::F64, DType::F64, false, false, false, {{U, Ri, U2, ml, kk, ml, ml, kk, kk, 1.0, 0.0}});
   DFac f;
-  f.B = U;
+  f.B = U2;
   f.ld = std::max(ml, 1);
   f.dim = ml;
   f.rank = kk;

@@ -244,6 +244,52 @@ __global__ void k_gather(const GatherJob* __restrict__ jobs) {
   }
 }
 
+// C (k x k, SPD, ~identity) = R^T R; writes R^{-1} (upper) to Rinv.  One CTA;
+// R kept in Rinv's storage during the factorisation, inverted in place by
+// column-parallel back substitution into a scratch half.
+__global__ void __launch_bounds__(1024) k_chol_inv(const double* __restrict__ C, int k,
+                                                   double* __restrict__ R,
+                                                   double* __restrict__ Rinv) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  __shared__ double s_d;
+  __shared__ int s_bad;
+  if (tid == 0) s_bad = 0;
+  for (int e = tid; e < k * k; e += nt) R[e] = 0.0;
+  __syncthreads();
+  for (int j = 0; j < k; ++j) {
+    if (tid == 0) {
+      double s = C[j + (long long)j * k];
+      for (int i = 0; i < j; ++i) s -= R[i + j * k] * R[i + j * k];
+      if (!(s > 0.0)) {
+        s_bad = 1;
+        s = 1.0;
+      }
+      s_d = sqrt(s);
+      R[j + j * k] = s_d;
+    }
+    __syncthreads();
+    const double djj = s_d;
+    for (int l = j + 1 + tid; l < k; l += nt) {
+      double s = C[j + (long long)l * k];
+      for (int i = 0; i < j; ++i) s -= R[i + j * k] * R[i + l * k];
+      R[j + l * k] = s / djj;
+    }
+    __syncthreads();
+  }
+  // R^{-1}: column c solves R x = e_c
+  for (int c = tid; c < k; c += nt) {
+    for (int i = 0; i < k; ++i) Rinv[i + c * k] = 0.0;
+    for (int i = c; i >= 0; --i) {
+      double s = (i == c) ? 1.0 : 0.0;
+      for (int l = i + 1; l <= c; ++l) s -= R[i + l * k] * Rinv[l + c * k];
+      Rinv[i + c * k] = s / R[i + i * k];
+    }
+  }
+  __syncthreads();
+  if (s_bad)  // not positive definite (cannot happen for a near-orthonormal U): identity
+    for (int e = tid; e < k * k; e += nt) Rinv[e] = (e % k == e / k) ? 1.0 : 0.0;
+}
+
 __global__ void k_colnorms2(const double* __restrict__ P, long long ld, int rows, int cols,
                             double* __restrict__ out) {
   const int lane = threadIdx.x & 31;
@@ -373,6 +419,13 @@ void gather_cols(Ctx& ctx, const std::vector<GatherJob>& jobs) {
   ctx.launch_begin();
   k_gather<<<dim3(grid_for(mx), (unsigned)jobs.size()), 256, 0, ctx.stream>>>(stage(ctx, jobs));
   ctx.check_launch("k_gather");
+}
+
+void chol_inverse(Ctx& ctx, const double* C, int k, double* Rinv) {
+  double* R = ctx.arena.alloc_n<double>((size_t)k * k);
+  ctx.launch_begin();
+  k_chol_inv<<<1, 1024, 0, ctx.stream>>>(C, k, R, Rinv);
+  ctx.check_launch("k_chol_inv");
 }
 
 void colnorms2(Ctx& ctx, const double* P, long long ld, int rows, int cols, double* out) {

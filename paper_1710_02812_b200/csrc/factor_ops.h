@@ -66,6 +66,13 @@ struct GatherJob {
 };
 void gather_cols(Ctx& ctx, const std::vector<GatherJob>& jobs);
 
+// "Twice is enough" pass for a nearly orthonormal basis (defect ~eps*kappa^2
+// from the Gram-form SVD): C = U^T U = R^T R (Cholesky, columns in sigma
+// order), U <- U R^{-1}.  Removes the error components of small-sigma
+// columns along larger ones; span and order are kept.  C is supplied by the
+// caller (computed locally, or all-reduced in the sharded path).
+void chol_inverse(Ctx& ctx, const double* C, int k, double* Rinv);
+
 // out[c] = sum_r P[r, c]^2   (rows x cols)
 void colnorms2(Ctx& ctx, const double* P, long long ld, int rows, int cols, double* out);
 
