@@ -781,7 +781,9 @@ void eig_topk(Ctx& ctx, const std::vector<EigJob>& jobs_in) {
       static_cast<const EigDev*>(ctx.staging.put(dev.data(), dev.size() * sizeof(EigDev), ctx.stream));
 
   // 1. tridiagonalise
-  if (nmax >= kBlockedMinN) {
+  int blocked_min = kBlockedMinN;
+  if (const char* env = std::getenv("HSVD_BLOCKED_MIN_N")) blocked_min = std::atoi(env);
+  if (nmax >= blocked_min) {
     for (int g = 0; g < count; ++g) {
       dev[g].VW = ctx.arena.alloc_n<double>((size_t)dev[g].n * 2 * NB);
       dev[g].WV = ctx.arena.alloc_n<double>((size_t)dev[g].n * 2 * NB);
