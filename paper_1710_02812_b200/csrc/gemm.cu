@@ -47,8 +47,13 @@ __global__ void __launch_bounds__(NT) k_gemm(const GemmDesc* __restrict__ descs,
   const int kb = split * kchunk;
   const int ke = min(d.K, kb + kchunk);
 
-  __shared__ __align__(16) double As[2][BK][BM + PAD];
-  __shared__ __align__(16) double Bs[2][BK][BN + PAD];
+  // operand tiles, reused as the 64x64 output staging tile in the epilogue
+  constexpr int A_ELEMS = 2 * BK * (BM + PAD), B_ELEMS = 2 * BK * (BN + PAD);
+  constexpr int T_LD = BN + 1;
+  static_assert(A_ELEMS + B_ELEMS >= BM * T_LD, "epilogue tile must fit");
+  __shared__ __align__(16) double smem_raw[A_ELEMS + B_ELEMS];
+  double (*As)[BK][BM + PAD] = reinterpret_cast<double (*)[BK][BM + PAD]>(smem_raw);
+  double (*Bs)[BK][BN + PAD] = reinterpret_cast<double (*)[BK][BN + PAD]>(smem_raw + A_ELEMS);
 
   const TA* A = static_cast<const TA*>(d.A);
   const TB* B = static_cast<const TB*>(d.B);
@@ -141,30 +146,42 @@ __global__ void __launch_bounds__(NT) k_gemm(const GemmDesc* __restrict__ descs,
     }
   }
 
-  // epilogue
+  // epilogue: stage the tile in shared memory so both the store and the
+  // SYRK mirror store are coalesced along the contiguous dimension
   const bool to_ws = ws != nullptr;
   double* out = to_ws ? ws + (long long)blockIdx.z * ws_slot : d.C;
   const long long ldo = to_ws ? (long long)d.M : d.ldc;
+  double* tile = smem_raw;  // [BM][T_LD], tile[ml * T_LD + nl]
+  __syncthreads();
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int m = m0 + wm + i * 8 + grp;
-    if (m >= d.M) continue;
+  for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < 4; ++j)
 #pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        const int n = n0 + wn + j * 8 + 2 * tig + r;
-        if (n >= d.N) continue;
-        double v = acc[i][j][r];
-        if (to_ws) {
-          out[m + n * ldo] = v;
-        } else {
-          v *= d.alpha;
-          if (d.beta != 0.0) v += d.beta * out[m + n * ldo];
-          out[m + n * ldo] = v;
-          if (syrk && tm != tn) out[n + m * ldo] = v;
-        }
-      }
+      for (int r = 0; r < 2; ++r)
+        tile[(wm + i * 8 + grp) * T_LD + wn + j * 8 + 2 * tig + r] = acc[i][j][r];
+  __syncthreads();
+  const double alpha = d.alpha, beta = d.beta;
+  for (int idx = tid; idx < BM * BN; idx += NT) {
+    const int ml = idx & (BM - 1), nl = idx >> 6;
+    const int m = m0 + ml, n = n0 + nl;
+    if (m >= d.M || n >= d.N) continue;
+    double v = tile[ml * T_LD + nl];
+    if (!to_ws) {
+      v *= alpha;
+      if (beta != 0.0) v += beta * out[m + (long long)n * ldo];
+    }
+    out[m + (long long)n * ldo] = v;
+  }
+  if (syrk && !to_ws && tm != tn) {
+    for (int idx = tid; idx < BM * BN; idx += NT) {
+      const int nl = idx & (BN - 1), ml = idx >> 6;
+      const int m = m0 + ml, n = n0 + nl;
+      if (m >= d.M || n >= d.N) continue;
+      double v = alpha * tile[ml * T_LD + nl];
+      // the mirrored element of a symmetric result: C(n, m) uses C(n, m)'s own beta term
+      if (beta != 0.0) v += beta * out[n + (long long)m * ldo];
+      out[n + (long long)m * ldo] = v;
     }
   }
 }

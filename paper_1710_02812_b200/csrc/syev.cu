@@ -696,7 +696,7 @@ __global__ void __launch_bounds__(NBT) k_build_t(const EigDev* __restrict__ jobs
   }
 }
 
-constexpr int kBlockedMinN = 512;
+constexpr int kBlockedMinN = 128;
 
 constexpr size_t kLatrdSmemMax = 200 * 1024;
 
