@@ -151,29 +151,40 @@ __global__ void __launch_bounds__(NT) k_gemm(const GemmDesc* __restrict__ descs,
   const bool to_ws = ws != nullptr;
   double* out = to_ws ? ws + (long long)blockIdx.z * ws_slot : d.C;
   const long long ldo = to_ws ? (long long)d.M : d.ldc;
-  double* tile = smem_raw;  // [BM][T_LD], tile[ml * T_LD + nl]
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int r = 0; r < 2; ++r)
-        tile[(wm + i * 8 + grp) * T_LD + wn + j * 8 + 2 * tig + r] = acc[i][j][r];
-  __syncthreads();
   const double alpha = d.alpha, beta = d.beta;
-  for (int idx = tid; idx < BM * BN; idx += NT) {
-    const int ml = idx & (BM - 1), nl = idx >> 6;
-    const int m = m0 + ml, n = n0 + nl;
-    if (m >= d.M || n >= d.N) continue;
-    double v = tile[ml * T_LD + nl];
-    if (!to_ws) {
-      v *= alpha;
-      if (beta != 0.0) v += beta * out[m + (long long)n * ldo];
+  // direct store: each warp instruction writes 4 columns x 8 consecutive rows
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int m = m0 + wm + i * 8 + grp;
+    if (m >= d.M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int n = n0 + wn + j * 8 + 2 * tig + r;
+        if (n >= d.N) continue;
+        double v = acc[i][j][r];
+        if (!to_ws) {
+          v *= alpha;
+          if (beta != 0.0) v += beta * out[m + (long long)n * ldo];
+        }
+        out[m + (long long)n * ldo] = v;
+      }
     }
-    out[m + (long long)n * ldo] = v;
   }
   if (syrk && !to_ws && tm != tn) {
+    // mirrored tile staged through shared memory so the transposed store is
+    // coalesced along its contiguous dimension
+    double* tile = smem_raw;  // [BM][T_LD], tile[ml * T_LD + nl]
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+          tile[(wm + i * 8 + grp) * T_LD + wn + j * 8 + 2 * tig + r] = acc[i][j][r];
+    __syncthreads();
     for (int idx = tid; idx < BM * BN; idx += NT) {
       const int nl = idx & (BN - 1), ml = idx >> 6;
       const int m = m0 + ml, n = n0 + nl;
