@@ -3,6 +3,7 @@
 #include <nccl.h>
 
 #include <condition_variable>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -154,12 +155,25 @@ struct ThreadGroup {
 
 namespace {
 
+bool trace_on() {
+  static const bool on = std::getenv("HSVD_TRACE") != nullptr;
+  return on;
+}
+#define TRACE(...)                                  \
+  do {                                              \
+    if (trace_on()) {                               \
+      std::fprintf(stderr, __VA_ARGS__);            \
+      std::fflush(stderr);                          \
+    }                                               \
+  } while (0)
+
 class ThreadComm : public Comm {
  public:
   ThreadComm(std::shared_ptr<ThreadGroup> g, int rank) : g_(std::move(g)), rank_(rank) {}
   int rank() const override { return rank_; }
   int size() const override { return g_->world; }
   void send(Ctx& c, const void* buf, size_t bytes, int peer) override {
+    TRACE("[r%d] send %zu -> %d: sync\n", rank_, bytes, peer);
     HSVD_CUDA(cudaStreamSynchronize(c.stream));
     std::unique_lock<std::mutex> lk(g_->mu);
     auto& s = g_->slots[rank_ * g_->world + peer];
@@ -172,38 +186,61 @@ class ThreadComm : public Comm {
     g_->cv.wait(lk, [&] { return s.consumed; });
     s.posted = false;
     g_->cv.notify_all();
+    TRACE("[r%d] send -> %d done\n", rank_, peer);
   }
   void recv(Ctx& c, void* buf, size_t bytes, int peer) override {
+    TRACE("[r%d] recv %zu <- %d: sync\n", rank_, bytes, peer);
     HSVD_CUDA(cudaStreamSynchronize(c.stream));
-    std::unique_lock<std::mutex> lk(g_->mu);
-    auto& s = g_->slots[peer * g_->world + rank_];
-    g_->cv.wait(lk, [&] { return s.posted && !s.consumed; });
-    if (s.bytes != bytes) throw Error(kNccl, "thread comm: size mismatch");
-    HSVD_CUDA(cudaMemcpy(buf, s.ptr, bytes, cudaMemcpyDeviceToDevice));
-    s.consumed = true;
+    const void* src = nullptr;
+    {
+      std::unique_lock<std::mutex> lk(g_->mu);
+      auto& s = g_->slots[peer * g_->world + rank_];
+      g_->cv.wait(lk, [&] { return s.posted && !s.consumed; });
+      if (s.bytes != bytes) throw Error(kNccl, "thread comm: size mismatch");
+      src = s.ptr;
+    }
+    // copy outside the lock (the sender is parked until `consumed`)
+    HSVD_CUDA(cudaMemcpyAsync(buf, src, bytes, cudaMemcpyDeviceToDevice, c.stream));
+    HSVD_CUDA(cudaStreamSynchronize(c.stream));
+    {
+      std::lock_guard<std::mutex> lk(g_->mu);
+      g_->slots[peer * g_->world + rank_].consumed = true;
+    }
     g_->cv.notify_all();
+    TRACE("[r%d] recv <- %d done\n", rank_, peer);
   }
   void bcast(Ctx& c, void* buf, size_t bytes, int root) override {
+    TRACE("[r%d] bcast root %d\n", rank_, root);
     HSVD_CUDA(cudaStreamSynchronize(c.stream));
     if (rank_ == root) {
       std::lock_guard<std::mutex> lk(g_->mu);
       g_->coll[root] = buf;
     }
     g_->barrier();
-    if (rank_ != root) HSVD_CUDA(cudaMemcpy(buf, g_->coll[root], bytes, cudaMemcpyDeviceToDevice));
+    if (rank_ != root) {
+      HSVD_CUDA(cudaMemcpyAsync(buf, g_->coll[root], bytes, cudaMemcpyDeviceToDevice, c.stream));
+      HSVD_CUDA(cudaStreamSynchronize(c.stream));
+    }
     g_->barrier();
+    TRACE("[r%d] bcast done\n", rank_);
   }
   void allreduce_sum(Ctx& c, double* buf, size_t count) override {
+    TRACE("[r%d] allreduce %zu\n", rank_, count);
     HSVD_CUDA(cudaStreamSynchronize(c.stream));
     auto& mine = g_->hostbuf[rank_];
     mine.resize(count);
-    HSVD_CUDA(cudaMemcpy(mine.data(), buf, count * sizeof(double), cudaMemcpyDeviceToHost));
+    HSVD_CUDA(cudaMemcpyAsync(mine.data(), buf, count * sizeof(double), cudaMemcpyDeviceToHost,
+                              c.stream));
+    HSVD_CUDA(cudaStreamSynchronize(c.stream));
     g_->barrier();
     std::vector<double> sum(count, 0.0);
     for (int r = 0; r < g_->world; ++r)  // fixed rank order: deterministic
       for (size_t i = 0; i < count; ++i) sum[i] += g_->hostbuf[r][i];
     g_->barrier();
-    HSVD_CUDA(cudaMemcpy(buf, sum.data(), count * sizeof(double), cudaMemcpyHostToDevice));
+    HSVD_CUDA(cudaMemcpyAsync(buf, sum.data(), count * sizeof(double), cudaMemcpyHostToDevice,
+                              c.stream));
+    HSVD_CUDA(cudaStreamSynchronize(c.stream));
+    TRACE("[r%d] allreduce done\n", rank_);
   }
   void barrier(Ctx& c) override {
     HSVD_CUDA(cudaStreamSynchronize(c.stream));
