@@ -6,6 +6,8 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -201,9 +203,17 @@ struct Ctx {
   }
 
   void count(int n = 1) { launches += n; }
+  static bool trace() {
+    static const bool on = std::getenv("HSVD_TRACE") != nullptr;
+    return on;
+  }
   void check_launch(const char* what) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) throw Error(kCuda, std::string(what) + ": " + cudaGetErrorString(e));
+    if (trace()) {
+      std::fprintf(stderr, "[r%d] launch %s:%s\n", rank, phase, what);
+      std::fflush(stderr);
+    }
     count();
     if (profiling && pending) {
       cudaEvent_t b = get_event();

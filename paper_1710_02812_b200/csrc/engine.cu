@@ -59,7 +59,9 @@ void fetch_ranks(Ctx& ctx, const int* d_ranks, int count, std::vector<int>& out)
   if (count == 0) return;
   int* h = ctx.pinned_ints(count);
   HSVD_CUDA(cudaMemcpyAsync(h, d_ranks, count * sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+  if (Ctx::trace()) std::fprintf(stderr, "[r%d] fetch_ranks sync\n", ctx.rank);
   HSVD_CUDA(cudaStreamSynchronize(ctx.stream));
+  if (Ctx::trace()) std::fprintf(stderr, "[r%d] fetch_ranks done\n", ctx.rank);
   std::memcpy(out.data(), h, count * sizeof(int));
 }
 
