@@ -793,8 +793,10 @@ void eig_topk(Ctx& ctx, const std::vector<EigJob>& jobs_in) {
     const int R = ceil_div(nmax, LAT);
     // cluster size: spread each matrix's mat-vec over several SMs while the
     // batch alone would leave SMs idle
+    // (capped at 4: 8-CTA clusters from several concurrent contexts on one
+    // GPU were observed to stall intermittently)
     int cs = 1;
-    while (cs < 8 && (long long)count * cs * 2 <= ctx.num_sms &&
+    while (cs < 4 && (long long)count * cs * 2 <= ctx.num_sms &&
            ((size_t)nmax * (1 + 4 * cs) + 4 * NB + 64) * sizeof(double) <= kLatrdSmemMax)
       cs *= 2;
     if (const char* env = std::getenv("HSVD_LATRD_CS")) cs = std::max(1, std::atoi(env));
