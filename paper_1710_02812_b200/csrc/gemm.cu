@@ -152,16 +152,23 @@ __global__ void __launch_bounds__(NT) k_gemm(const GemmDesc* __restrict__ descs,
   double* out = to_ws ? ws + (long long)blockIdx.z * ws_slot : d.C;
   const long long ldo = to_ws ? (long long)d.M : d.ldc;
   const double alpha = d.alpha, beta = d.beta;
-  // direct store: each warp instruction writes 4 columns x 8 consecutive rows
+  // direct store: each warp instruction writes 4 columns x 8 consecutive rows;
+  // the SYRK mirror reuses the final values staged in shared memory so the
+  // transposed store is coalesced and C is read once
+  const bool mirror = syrk && !to_ws && tm != tn;
+  double* tile = smem_raw;  // [BM][T_LD], tile[ml * T_LD + nl]
+  if (mirror) __syncthreads();  // operand tiles no longer read
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const int m = m0 + wm + i * 8 + grp;
+    const int ml = wm + i * 8 + grp;
+    const int m = m0 + ml;
     if (m >= d.M) continue;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
 #pragma unroll
       for (int r = 0; r < 2; ++r) {
-        const int n = n0 + wn + j * 8 + 2 * tig + r;
+        const int nl = wn + j * 8 + 2 * tig + r;
+        const int n = n0 + nl;
         if (n >= d.N) continue;
         double v = acc[i][j][r];
         if (!to_ws) {
@@ -169,30 +176,17 @@ __global__ void __launch_bounds__(NT) k_gemm(const GemmDesc* __restrict__ descs,
           if (beta != 0.0) v += beta * out[m + (long long)n * ldo];
         }
         out[m + (long long)n * ldo] = v;
+        if (mirror) tile[ml * T_LD + nl] = v;
       }
     }
   }
-  if (syrk && !to_ws && tm != tn) {
-    // mirrored tile staged through shared memory so the transposed store is
-    // coalesced along its contiguous dimension
-    double* tile = smem_raw;  // [BM][T_LD], tile[ml * T_LD + nl]
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-#pragma unroll
-        for (int r = 0; r < 2; ++r)
-          tile[(wm + i * 8 + grp) * T_LD + wn + j * 8 + 2 * tig + r] = acc[i][j][r];
+  if (mirror) {
     __syncthreads();
     for (int idx = tid; idx < BM * BN; idx += NT) {
       const int nl = idx & (BN - 1), ml = idx >> 6;
       const int m = m0 + ml, n = n0 + nl;
       if (m >= d.M || n >= d.N) continue;
-      double v = alpha * tile[ml * T_LD + nl];
-      // the mirrored element of a symmetric result: C(n, m) uses C(n, m)'s own beta term
-      if (beta != 0.0) v += beta * out[n + (long long)m * ldo];
-      out[n + (long long)m * ldo] = v;
+      out[n + (long long)m * ldo] = tile[ml * T_LD + nl];
     }
   }
 }
