@@ -127,6 +127,12 @@ int hsvd_cu_tree_merge(hsvd_cu_ctx* ctx, int orient, const hsvd_cu_factor_in* fa
                        int64_t count, double gamma, int64_t max_rank, int64_t* pair_merges,
                        hsvd_cu_result** out);
 
+/* Building block: top-kk eigenpairs of a symmetric n x n matrix (host,
+ * column-major), the device eigensolver every SVD of the path runs on.
+ * lam (kk, descending), z (n x kk, column-major). */
+int hsvd_cu_syevx_topk(hsvd_cu_ctx* ctx, const double* a, int64_t n, int64_t kk, double* lam,
+                       double* z);
+
 /* ---- multi-GPU (one process / thread per GPU, rows sharded) ---------- */
 typedef struct hsvd_cu_group hsvd_cu_group;
 /* NCCL: rank 0 creates the 128-byte id and shares it; every rank inits. */

@@ -8,6 +8,7 @@
 #include "comm.h"
 #include "engine.h"
 #include "factor_ops.h"
+#include "syev.h"
 
 using namespace hsvdcu;
 
@@ -436,6 +437,25 @@ int hsvd_cu_tree_merge(hsvd_cu_ctx* ctx, int orient, const hsvd_cu_factor_in* fa
     DFac f = tree_merge_many(ctx->c, {fs}, gamma, cap_of(max_rank), &pm).front();
     if (pair_merges) *pair_merges = pm;
     *out = make_result(ctx, f, orient == HSVD_CU_COLUMN_CONCAT, false);
+    return HSVD_CU_OK;
+  });
+}
+
+int hsvd_cu_syevx_topk(hsvd_cu_ctx* ctx, const double* a, int64_t n, int64_t kk, double* lam,
+                       double* z) {
+  return guarded([&] {
+    if (!a || !lam || !z || n < 1 || kk < 1 || kk > n)
+      throw Error(kInvalid, "syevx_topk: bad arguments");
+    begin(ctx);
+    Ctx& c = ctx->c;
+    double* A = c.arena.alloc_n<double>((size_t)n * n);
+    double* L = c.arena.alloc_n<double>(kk);
+    double* Z = c.arena.alloc_n<double>((size_t)n * kk);
+    HSVD_CUDA(cudaMemcpyAsync(A, a, (size_t)n * n * 8, cudaMemcpyHostToDevice, c.stream));
+    eig_topk(c, {{A, n, (int)n, (int)kk, L, Z, n}});
+    HSVD_CUDA(cudaMemcpyAsync(lam, L, kk * 8, cudaMemcpyDeviceToHost, c.stream));
+    HSVD_CUDA(cudaMemcpyAsync(z, Z, (size_t)n * kk * 8, cudaMemcpyDeviceToHost, c.stream));
+    HSVD_CUDA(cudaStreamSynchronize(c.stream));
     return HSVD_CU_OK;
   });
 }

@@ -36,6 +36,9 @@ constexpr int TRD_THREADS = 1024;
 constexpr int TRD_QMAX = 8;  // rows per thread when n > 1024 (n <= 8192)
 constexpr int EIG_THREADS = 256;
 constexpr int NB = 32;       // reflectors per compact-WY block
+constexpr int B2 = 32;       // bandwidth of the two-stage reduction
+constexpr int LDBB = 2 * B2 + 1;  // band storage: diagonals 0..2*B2 (chase fill)
+constexpr int INV_WARPS = 8;      // warps (= LU workspace slots) per band inverse iteration CTA
 
 struct EigDev {
   double* A;
@@ -53,6 +56,18 @@ struct EigDev {
   double* S;     // (nblocks * NBT * NBT) V^T V of each reflector block
   double* VW;    // n x 2*NB panel [V | W] (blocked tridiagonalisation)
   double* WV;    // n x 2*NB panel [W | V]
+  // two-stage path
+  int vals_only;     // k_steig: eigenvalues (+ shifts, clusters) only
+  double* shifts;    // kk perturbed inverse-iteration shifts
+  int* cstarts;      // kk cluster starts
+  double* band;      // (2*B2+1) x n lower band, chased to tridiagonal
+  double* band0;     // copy of the band after stage 1 (inverse iteration)
+  double* Tp;        // npanels x B2 x B2 panel T factors
+  double* Y;         // n x B2
+  double* P1;        // B2 x B2
+  double* Mb;        // B2 x B2
+  double* lu;        // per-warp band LU workspace (INV_WARPS slots per matrix)
+  long long lu_slot;  // doubles per slot
 };
 
 // ---------------------------------------------------------------------------
@@ -569,6 +584,14 @@ __global__ void __launch_bounds__(EIG_THREADS) k_steig(const EigDev* __restrict_
   }
   __syncthreads();
 
+  if (J.vals_only) {  // two-stage path: vectors come from the band matrix
+    for (int t = tid; t < kk; t += nt) {
+      J.lam[t] = lam[t];
+      J.shifts[t] = shift[t];
+      J.cstarts[t] = cstart[t];
+    }
+    return;
+  }
   const double tiny = eps * tnorm;
   // start vectors (deterministic pseudo-random, dstein uses dlarnv uniform(-1,1))
   for (int t = tid; t < kk; t += nt) {
@@ -646,28 +669,17 @@ __global__ void __launch_bounds__(EIG_THREADS) k_steig(const EigDev* __restrict_
 // 3. compact-WY preparation: V in place in A, T per block of NB reflectors
 // ---------------------------------------------------------------------------
 
-// Zero the upper triangle and diagonal of A, unit subdiagonal: column j of
-// A (rows j+1..) becomes reflector v_j.
-__global__ void k_prep_v(const EigDev* __restrict__ jobs) {
-  const EigDev J = jobs[blockIdx.y];
-  const int n = J.n;
-  const long long total = (long long)n * n;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    const int i = (int)(e % n), j = (int)(e / n);
-    if (i <= j) J.A[i + j * J.lda] = 0.0;
-    else if (i == j + 1) J.A[i + j * J.lda] = 1.0;
-  }
-}
+// (V is made explicit in place by k_prep_v_off: column j of A, rows
+// j+off.., becomes reflector v_j.)
 
 // T factor (dlarft, forward, columnwise) of every reflector block of NBT
 // reflectors, from S = V^T V (computed by a grouped DMMA GEMM beforehand).
 constexpr int NBT = 128;
 
-__global__ void __launch_bounds__(NBT) k_build_t(const EigDev* __restrict__ jobs) {
+__global__ void __launch_bounds__(NBT) k_build_t(const EigDev* __restrict__ jobs, int off) {
   const EigDev J = jobs[blockIdx.y];
   const int b = blockIdx.x;
-  const int nref = J.n - 1;
+  const int nref = J.n - off;
   const int j0 = b * NBT;
   if (j0 >= nref) return;
   const int nb = min(NBT, nref - j0);
@@ -693,6 +705,423 @@ __global__ void __launch_bounds__(NBT) k_build_t(const EigDev* __restrict__ jobs
   for (int e = tid; e < NBT * NBT; e += blockDim.x) {
     const int i = e % NBT, j = e / NBT;  // column-major
     out[e] = T[i * (NBT + 1) + j];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Two-stage reduction (large n): dense -> band B2 by panel QR + DMMA GEMMs,
+// band -> tridiagonal by Householder bulge chasing (eigenvalues only),
+// eigenvectors by inverse iteration on the band matrix, back-transform
+// through the stage-1 reflectors (tools/proto/two_stage.py is the numpy
+// model of every step; the pipelined chase order was checked there to give
+// the sequential result bit for bit).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double& band_at(double* bb, int i, int j) {
+  return bb[(i - j) + (long long)j * LDBB];
+}
+
+// Panel j0: copy the diagonal block to the band, Householder QR of the
+// panel below the band (R -> band, explicit V in place and in VW/WV), T.
+__global__ void __launch_bounds__(512) k_panel_qr(const EigDev* __restrict__ jobs, int j0) {
+  const EigDev J = jobs[blockIdx.x];
+  const int n = J.n;
+  if (j0 >= n) return;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
+  double* A = J.A;
+  const long long lda = J.lda;
+  const int jb = min(B2, n - j0);
+  const int r0 = j0 + B2;
+  const int m = n - r0;
+  __shared__ double beta_s[B2];
+  __shared__ double red[32];
+  __shared__ double S[B2][B2 + 1];
+  __shared__ double T[B2][B2 + 1];
+  __shared__ double tau_s[B2];
+  for (int e = tid; e < jb * jb; e += nt) {
+    const int t = e / jb, i = e % jb;
+    if (i >= t) band_at(J.band, j0 + i, j0 + t) = A[(j0 + i) + (long long)(j0 + t) * lda];
+  }
+  if (m <= 0) return;
+  const int nr = m >= 2 ? min(jb, m - 1) : 0;
+  double* P = A + r0 + (long long)j0 * lda;
+  for (int t = 0; t < nr; ++t) {
+    double* pt = P + (long long)t * lda;
+    double part = 0.0;
+    for (int i = t + 1 + tid; i < m; i += nt) part += pt[i] * pt[i];
+    const double xn2 = block_sum(part, red);
+    const double alpha = pt[t];
+    double tau = 0.0, beta = alpha, scal = 0.0;
+    if (xn2 > 0.0) {
+      const double nrm = sqrt(alpha * alpha + xn2);
+      beta = alpha >= 0.0 ? -nrm : nrm;
+      tau = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    for (int i = t + 1 + tid; i < m; i += nt) pt[i] *= scal;
+    if (tid == 0) {
+      beta_s[t] = beta;
+      tau_s[t] = tau;
+      J.tau[j0 + t] = tau;
+    }
+    __syncthreads();
+    if (tau != 0.0) {
+      for (int u = t + 1 + warp; u < jb; u += nwarps) {
+        double* pu = P + (long long)u * lda;
+        double s = 0.0;
+        for (int i = t + 1 + lane; i < m; i += 32) s += pt[i] * pu[i];
+        s = warp_sum(s) + pu[t];
+        s *= tau;
+        if (lane == 0) pu[t] -= s;
+        for (int i = t + 1 + lane; i < m; i += 32) pu[i] -= s * pt[i];
+      }
+    }
+    __syncthreads();
+  }
+  if (tid < B2 && tid >= nr) {
+    tau_s[tid] = 0.0;
+    if (tid < jb) J.tau[j0 + tid] = 0.0;
+  }
+  __syncthreads();
+  // R -> band (rows r0+i, columns j0+t, i <= t)
+  for (int e = tid; e < jb * jb; e += nt) {
+    const int t = e / jb, i = e % jb;
+    if (i <= t && i < m)
+      band_at(J.band, r0 + i, j0 + t) = (i == t && t < nr) ? beta_s[t] : P[i + (long long)t * lda];
+  }
+  __syncthreads();
+  // explicit V (unit lower trapezoidal) in place and in the VW / WV panels
+  for (int t = 0; t < jb; ++t) {
+    double* pt = P + (long long)t * lda;
+    for (int i = tid; i < m; i += nt) {
+      const double v = t >= nr ? 0.0 : (i < t ? 0.0 : (i == t ? 1.0 : pt[i]));
+      pt[i] = v;
+      J.VW[(r0 + i) + (long long)t * n] = v;
+      J.WV[(r0 + i) + (long long)(B2 + t) * n] = v;
+    }
+  }
+  __syncthreads();
+  // T (dlarft forward columnwise) from S = V^T V
+  for (int pq = warp; pq < B2 * B2; pq += nwarps) {
+    const int p = pq / B2, q = pq % B2;
+    if (p > q) continue;
+    double s = 0.0;
+    if (q < nr) {
+      const double* vp = P + (long long)p * lda;
+      const double* vq = P + (long long)q * lda;
+      for (int i = q + lane; i < m; i += 32) s += vp[i] * vq[i];
+      s = warp_sum(s);
+    }
+    if (lane == 0) S[p][q] = s;
+  }
+  for (int e = tid; e < B2 * (B2 + 1); e += nt) (&T[0][0])[e] = 0.0;
+  __syncthreads();
+  for (int t = 0; t < B2; ++t) {
+    if (tid < t) {
+      double s = 0.0;
+      for (int l = tid; l < t; ++l) s += T[tid][l] * S[l][t];
+      T[tid][t] = -tau_s[t] * s;
+    }
+    if (tid == 0) T[t][t] = tau_s[t];
+    __syncthreads();
+  }
+  double* out = J.Tp + (long long)(j0 / B2) * B2 * B2;
+  for (int e = tid; e < B2 * B2; e += nt) out[e] = T[e % B2][e / B2];
+}
+
+// WV[:, 0:B2] = W (= VW[:, B2:2B2]) for the rows below the panel
+__global__ void k_copy_w(const EigDev* __restrict__ jobs, int j0) {
+  const EigDev J = jobs[blockIdx.y];
+  const int n = J.n, r0 = j0 + B2;
+  if (r0 > n - 2) return;
+  const long long total = (long long)(n - r0) * B2;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int i = r0 + (int)(e % (n - r0)), t = (int)(e / (n - r0));
+    J.WV[i + (long long)t * n] = J.VW[i + (long long)(B2 + t) * n];
+  }
+}
+
+// Band -> tridiagonal by Householder bulge chasing (eigenvalues only).
+// One CTA per matrix; warp w runs sweeps w, w+W, ...; sweep s may do step
+// k only after sweep s-1 finished step k+3 (or the whole sweep), which
+// reproduces the sequential result exactly.
+__device__ __forceinline__ unsigned long long prog_encode(int s, unsigned steps) {
+  return ((unsigned long long)(unsigned)(s + 1) << 32) | steps;
+}
+constexpr unsigned kSweepDone = 0x7fffffffu;
+
+__global__ void __launch_bounds__(512) k_chase(const EigDev* __restrict__ jobs) {
+  const EigDev J = jobs[blockIdx.x];
+  const int n = J.n;
+  double* bb = J.band;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, W = blockDim.x >> 5;
+  __shared__ unsigned long long prog[32];
+  if (tid < W) prog[tid] = prog_encode(tid - W, kSweepDone);
+  __syncthreads();
+  volatile unsigned long long* vprog = prog;
+  const int nsweeps = n - 2;
+  for (int s = warp; s < nsweeps; s += W) {
+    const int pslot = (warp - 1 + W) % W;
+    for (int k = 0;; ++k) {
+      const int r0 = s + 1 + k * B2;
+      if (r0 >= n) break;
+      const int r1 = min(n, r0 + B2), L = r1 - r0;
+      if (L < 2) break;
+      if (s > 0) {  // wait for sweep s-1 to be 3 steps ahead (or done)
+        const unsigned need = (unsigned)(k + 3);
+        while (true) {
+          const unsigned long long v = vprog[pslot];
+          const int vs = (int)(v >> 32) - 1;
+          const unsigned st = (unsigned)(v & 0xffffffffu);
+          if (vs > s - 1 || (vs == s - 1 && (st >= need))) break;
+          __nanosleep(64);
+        }
+        __threadfence_block();
+      }
+      const int c = k == 0 ? s : s + 1 + (k - 1) * B2;
+      double x = lane < L ? band_at(bb, r0 + lane, c) : 0.0;
+      const double xn2 = warp_sum(lane >= 1 ? x * x : 0.0);
+      const double alpha = __shfl_sync(0xffffffffu, x, 0);
+      if (xn2 == 0.0) break;  // no bulge left in this sweep
+      const double nrm = sqrt(alpha * alpha + xn2);
+      const double beta = alpha >= 0.0 ? -nrm : nrm;
+      const double tau = (beta - alpha) / beta;
+      const double scal = 1.0 / (alpha - beta);
+      const double v = lane == 0 ? 1.0 : (lane < L ? x * scal : 0.0);
+      if (lane < L) band_at(bb, r0 + lane, c) = lane == 0 ? beta : 0.0;
+      // rows R x columns (c, r0): left application
+      for (int l = c + 1; l < r0; ++l) {
+        const double y = lane < L ? band_at(bb, r0 + lane, l) : 0.0;
+        const double dt = tau * warp_sum(v * y);
+        if (lane < L) band_at(bb, r0 + lane, l) = y - dt * v;
+      }
+      // R x R: two-sided (symmetric, lower storage)
+      double p = 0.0;
+      for (int j = 0; j < L; ++j) {
+        const double vj = __shfl_sync(0xffffffffu, v, j);
+        double a = 0.0;
+        if (lane < L) a = lane >= j ? band_at(bb, r0 + lane, r0 + j) : band_at(bb, r0 + j, r0 + lane);
+        p += a * vj;
+      }
+      p *= tau;
+      const double al = -0.5 * tau * warp_sum(p * v);
+      const double w = p + al * v;
+      for (int j = 0; j < L; ++j) {
+        const double vj = __shfl_sync(0xffffffffu, v, j);
+        const double wj = __shfl_sync(0xffffffffu, w, j);
+        if (lane < L && lane >= j) band_at(bb, r0 + lane, r0 + j) -= v * wj + w * vj;
+      }
+      // rows after R x R: right application (creates the next bulge)
+      const int na = min(n, r0 + 2 * B2) - r1;
+      double y = 0.0;
+      for (int j = 0; j < L; ++j) {
+        const double vj = __shfl_sync(0xffffffffu, v, j);
+        if (lane < na) y += band_at(bb, r1 + lane, r0 + j) * vj;
+      }
+      y *= tau;
+      for (int j = 0; j < L; ++j) {
+        const double vj = __shfl_sync(0xffffffffu, v, j);
+        if (lane < na) band_at(bb, r1 + lane, r0 + j) -= y * vj;
+      }
+      __syncwarp();
+      __threadfence_block();
+      if (lane == 0) vprog[warp] = prog_encode(s, (unsigned)(k + 1));
+    }
+    __syncwarp();
+    __threadfence_block();
+    if (lane == 0) vprog[warp] = prog_encode(s, kSweepDone);
+  }
+  __syncthreads();
+  for (int i = tid; i < n; i += blockDim.x) {
+    J.d[i] = band_at(bb, i, i);
+    if (i < n - 1) J.e[i] = band_at(bb, i + 1, i);
+  }
+}
+
+// Eigenvectors of the band matrix (band0, bandwidth B2) by inverse
+// iteration: per warp, band LU with partial pivoting of (B - shift I) kept
+// in a (B2+1) x (2*B2+1) shared-memory window (U rows and multipliers
+// streamed to the warp's workspace), three solves; then Gram-Schmidt inside
+// clusters (as k_steig).
+__device__ __forceinline__ double band_full(const double* b0, int n, int i, int j) {
+  if (i < 0 || j < 0 || i >= n || j >= n) return 0.0;
+  const int d = i - j;
+  if (d > B2 || d < -B2) return 0.0;
+  return d >= 0 ? b0[d + (long long)j * LDBB] : b0[-d + (long long)i * LDBB];
+}
+
+__global__ void __launch_bounds__(INV_WARPS * 32) k_band_invit(const EigDev* __restrict__ jobs) {
+  const EigDev J = jobs[blockIdx.x];
+  const int n = J.n, kk = J.kk;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nt = blockDim.x;
+  constexpr int WR = B2 + 1, WC = 2 * B2 + 1;  // window rows / columns
+  extern __shared__ double sm[];
+  double* win = sm + (size_t)warp * WR * WC;
+  double* dots = sm + (size_t)INV_WARPS * WR * WC;
+  double* red = dots + kk;
+  const double* b0 = J.band0;
+  const double eps = DBL_EPSILON;
+  // ||B||_inf for the pivot guard
+  double nb = 0.0;
+  for (int i = tid; i < n; i += nt) {
+    double s = 0.0;
+    for (int j = max(0, i - B2); j <= min(n - 1, i + B2); ++j) s += fabs(band_full(b0, n, i, j));
+    nb = fmax(nb, s);
+  }
+  const double bnorm = block_max(nb, red);
+  const double tiny = eps * fmax(bnorm, DBL_MIN);
+  // workspace of this warp: U rows (n x WC), multipliers (n x B2), pivots, y
+  double* U = J.lu + ((size_t)blockIdx.x * INV_WARPS + warp) * (size_t)J.lu_slot;
+  double* Lm = U + (size_t)n * WC;
+  double* piv = Lm + (size_t)n * B2;  // stored as doubles
+  double* yv = piv + n;
+  for (int t = warp; t < kk; t += INV_WARPS) {
+    const double sh = J.shifts[t];
+    // --- factorisation: window rows are slots (row % WR), columns (col % WC)
+    for (int e = lane; e < WR * WC; e += 32) win[e] = 0.0;
+    __syncwarp();
+    for (int i = 0; i <= B2 && i < n; ++i)
+      for (int c = lane; c <= 2 * B2; c += 32)
+        if (c < n) win[(i % WR) * WC + (c % WC)] = band_full(b0, n, i, c) - (i == c ? sh : 0.0);
+    __syncwarp();
+    for (int j = 0; j < n; ++j) {
+      const int nw = min(B2 + 1, n - j);  // candidate rows j..j+nw-1
+      double a = lane < nw ? fabs(win[((j + lane) % WR) * WC + (j % WC)]) : -1.0;
+      int p = lane;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ao = __shfl_xor_sync(0xffffffffu, a, o);
+        const int po = __shfl_xor_sync(0xffffffffu, p, o);
+        if (ao > a || (ao == a && po < p)) {
+          a = ao;
+          p = po;
+        }
+      }
+      const int sj = (j % WR) * WC, sp = ((j + p) % WR) * WC;
+      if (p != 0)
+        for (int c = lane; c < WC; c += 32) {
+          const double tmp = win[sj + c];
+          win[sj + c] = win[sp + c];
+          win[sp + c] = tmp;
+        }
+      __syncwarp();
+      double u = win[sj + (j % WC)];
+      if (fabs(u) < tiny) u = u < 0.0 ? -tiny : tiny;
+      if (lane == 0) {
+        piv[j] = (double)p;
+        win[sj + (j % WC)] = u;
+      }
+      // multipliers and elimination of rows j+1..j+nw-1 over columns j+1..j+2B2
+      const int ncol = min(2 * B2, n - 1 - j);
+      for (int i = 1; i < nw; ++i) {
+        const int si = ((j + i) % WR) * WC;
+        const double l = win[si + (j % WC)] / u;
+        for (int cc = 1 + lane; cc <= ncol; cc += 32) win[si + ((j + cc) % WC)] -= l * win[sj + ((j + cc) % WC)];
+        if (lane == 0) Lm[(size_t)j * B2 + (i - 1)] = l;
+      }
+      __syncwarp();
+      for (int cc = lane; cc < WC; cc += 32)
+        U[(size_t)j * WC + cc] = (cc <= ncol) ? win[sj + ((j + cc) % WC)] : 0.0;
+      __syncwarp();
+      // recycle the slot of row j for row j+B2+1; column j+2B2+1 enters
+      const int rn = j + B2 + 1;
+      const int cnew = (j + 2 * B2 + 1) % WC;
+      for (int i = 1; i < nw; ++i)
+        if (lane == 0) win[((j + i) % WR) * WC + cnew] = 0.0;
+      for (int c = lane; c < WC; c += 32) win[sj + c] = 0.0;
+      __syncwarp();
+      if (rn < n)
+        for (int cc = lane; cc < WC; cc += 32) {
+          const int col = j + 1 + cc;
+          if (col < n) win[sj + (col % WC)] = band_full(b0, n, rn, col) - (rn == col ? sh : 0.0);
+        }
+      __syncwarp();
+    }
+    // --- three solves from a deterministic start vector
+    double* z = J.Z + (long long)t * J.ldz;
+    for (int r = lane; r < n; r += 32) {
+      const unsigned h = hash32((unsigned)r * 2654435761u ^ hash32((unsigned)t + 0x9e3779b9u));
+      yv[r] = ((double)h / 4294967296.0) * 2.0 - 1.0;
+    }
+    __syncwarp();
+    for (int it = 0; it < 3; ++it) {
+      // forward: row swaps + L
+      for (int j = 0; j < n; ++j) {
+        const int p = (int)piv[j];
+        if (p != 0 && lane == 0) {
+          const double tmp = yv[j];
+          yv[j] = yv[j + p];
+          yv[j + p] = tmp;
+        }
+        __syncwarp();
+        const double yj = yv[j];
+        const int nw = min(B2 + 1, n - j);
+        if (lane + 1 < nw) yv[j + 1 + lane] -= Lm[(size_t)j * B2 + lane] * yj;
+        __syncwarp();
+      }
+      // backward: U x = y
+      for (int j = n - 1; j >= 0; --j) {
+        const double* ur = U + (size_t)j * WC;
+        double s = 0.0;
+        for (int cc = 1 + lane; cc < WC; cc += 32)
+          if (j + cc < n) s += ur[cc] * yv[j + cc];
+        s = warp_sum(s);
+        if (lane == 0) yv[j] = (yv[j] - s) / ur[0];
+        __syncwarp();
+      }
+      double s2 = 0.0;
+      for (int r = lane; r < n; r += 32) s2 += yv[r] * yv[r];
+      s2 = warp_sum(s2);
+      double sc = s2 > 0.0 && isfinite(s2) ? 1.0 / sqrt(s2) : 0.0;
+      for (int r = lane; r < n; r += 32) yv[r] = sc == 0.0 ? (r == t % n ? 1.0 : 0.0) : yv[r] * sc;
+      __syncwarp();
+    }
+    for (int r = lane; r < n; r += 32) z[r] = yv[r];
+  }
+  __syncthreads();
+  // Gram-Schmidt (twice) inside clusters, in eigenvalue order
+  const int nwarps = nt >> 5;
+  for (int t = 0; t < kk; ++t) {
+    const int cs = J.cstarts[t];
+    if (cs == t) continue;
+    double* zt = J.Z + (long long)t * J.ldz;
+    for (int rep = 0; rep < 2; ++rep) {
+      for (int c = cs + warp; c < t; c += nwarps) {
+        const double* zc = J.Z + (long long)c * J.ldz;
+        double s = 0.0;
+        for (int r = lane; r < n; r += 32) s += zc[r] * zt[r];
+        s = warp_sum(s);
+        if (lane == 0) dots[c - cs] = s;
+      }
+      __syncthreads();
+      for (int r = tid; r < n; r += nt) {
+        double a = zt[r];
+        for (int c = cs; c < t; ++c) a -= dots[c - cs] * J.Z[r + (long long)c * J.ldz];
+        zt[r] = a;
+      }
+      __syncthreads();
+    }
+    double part = 0.0;
+    for (int r = tid; r < n; r += nt) part += zt[r] * zt[r];
+    const double nrm2 = block_sum(part, red);
+    const double sc = nrm2 > 0.0 ? 1.0 / sqrt(nrm2) : 0.0;
+    for (int r = tid; r < n; r += nt) zt[r] *= sc;
+    __syncthreads();
+  }
+}
+
+// Zero the band rows of the reflector columns: V column j has its unit at
+// row j + off (off = 1 one-stage, B2 two-stage).
+__global__ void k_prep_v_off(const EigDev* __restrict__ jobs, int off) {
+  const EigDev J = jobs[blockIdx.y];
+  const int n = J.n;
+  const long long total = (long long)n * n;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e % n), j = (int)(e / n);
+    if (i < j + off) J.A[i + j * J.lda] = 0.0;
+    else if (i == j + off) J.A[i + j * J.lda] = 1.0;
   }
 }
 
@@ -744,6 +1173,162 @@ void launch_latrd(Ctx& ctx, int R, int count, int cs, size_t smem, const EigDev*
   }
 }
 
+constexpr int kTwoStageMinN = 1 << 30;  // enabled by HSVD_TWO_STAGE_MIN_N until validated
+
+// Z <- Q Z with Q = H_0 H_1 ... (reflector of column j: unit at row j + off,
+// stored in A column j), in compact-WY blocks of NBT reflectors.
+void back_transform(Ctx& ctx, const std::vector<EigJob>& jobs, const std::vector<EigDev>& dev,
+                    const EigDev* dd, int nmax, int off) {
+  const int count = static_cast<int>(dev.size());
+  if (nmax <= off + 1) return;
+  const long long nn = (long long)nmax * nmax;
+  int gx = static_cast<int>(std::min<long long>((nn + 255) / 256, 2048));
+  ctx.launch_begin();
+  k_prep_v_off<<<dim3(gx, count), 256, 0, ctx.stream>>>(dd, off);
+  ctx.check_launch("k_prep_v");
+  const int nblk_max = ceil_div(nmax - off, NBT);
+  // S_b = V_b^T V_b for every block of every matrix (one grouped launch)
+  std::vector<GemmDesc> ds;
+  for (int g = 0; g < count; ++g) {
+    const EigDev& e = dev[g];
+    if (e.n <= off + 1) continue;
+    for (int b = 0; b * NBT < e.n - off; ++b) {
+      const int j0 = b * NBT, nb = std::min(NBT, e.n - off - j0), m = e.n - j0 - off;
+      const double* V = e.A + j0 + off + (long long)j0 * e.lda;
+      ds.push_back({V, V, e.S + (long long)b * NBT * NBT, e.lda, e.lda, NBT, nb, nb, m, 1.0, 0.0});
+    }
+  }
+  gemm_grouped(ctx, DType::F64, DType::F64, true, false, true, ds);
+  const size_t tsm = ((size_t)NBT * (NBT + 1) + NBT) * sizeof(double);
+  HSVD_CUDA(cudaFuncSetAttribute(k_build_t, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
+  ctx.launch_begin();
+  k_build_t<<<dim3(nblk_max, count), NBT, tsm, ctx.stream>>>(dd, off);
+  ctx.check_launch("k_build_t");
+  std::vector<double*> W(count), W2(count);
+  for (int g = 0; g < count; ++g) {
+    W[g] = ctx.arena.alloc_n<double>((size_t)NBT * jobs[g].kk);
+    W2[g] = ctx.arena.alloc_n<double>((size_t)NBT * jobs[g].kk);
+  }
+  std::vector<GemmDesc> d1, d2, d3;
+  for (int b = nblk_max - 1; b >= 0; --b) {
+    const int j0 = b * NBT;
+    d1.clear();
+    d2.clear();
+    d3.clear();
+    for (int g = 0; g < count; ++g) {
+      const EigDev& e = dev[g];
+      const int nref = e.n - off;
+      if (j0 >= nref || e.n <= off + 1) continue;
+      const int m = e.n - j0 - off;
+      const int nb = std::min(NBT, nref - j0);
+      const double* V = e.A + j0 + off + (long long)j0 * e.lda;
+      double* Zs = e.Z + j0 + off;
+      d1.push_back({V, Zs, W[g], e.lda, e.ldz, NBT, nb, e.kk, m, 1.0, 0.0});  // W = V^T Zs
+      d2.push_back({e.T + (long long)b * NBT * NBT, W[g], W2[g], NBT, NBT, NBT, nb, e.kk, nb, 1.0,
+                    0.0});                                                    // W2 = T W
+      d3.push_back({V, W2[g], Zs, e.lda, NBT, e.ldz, m, e.kk, nb, -1.0, 1.0});  // Zs -= V W2
+    }
+    if (d1.empty()) continue;
+    gemm_grouped(ctx, DType::F64, DType::F64, true, false, false, d1);
+    gemm_grouped(ctx, DType::F64, DType::F64, false, false, false, d2);
+    gemm_grouped(ctx, DType::F64, DType::F64, false, false, false, d3);
+  }
+}
+
+void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& dev, int nmax,
+               int kkmax) {
+  const int count = static_cast<int>(dev.size());
+  const int npan = ceil_div(nmax, B2);
+  size_t lu_slot_max = 0;
+  for (int g = 0; g < count; ++g) {
+    EigDev& d = dev[g];
+    const int n = d.n;
+    d.band = ctx.arena.alloc_n<double>((size_t)LDBB * n);
+    d.band0 = ctx.arena.alloc_n<double>((size_t)LDBB * n);
+    d.Tp = ctx.arena.alloc_n<double>((size_t)ceil_div(n, B2) * B2 * B2);
+    d.VW = ctx.arena.alloc_n<double>((size_t)n * 2 * B2);
+    d.WV = ctx.arena.alloc_n<double>((size_t)n * 2 * B2);
+    d.Y = ctx.arena.alloc_n<double>((size_t)n * B2);
+    d.P1 = ctx.arena.alloc_n<double>((size_t)B2 * B2);
+    d.Mb = ctx.arena.alloc_n<double>((size_t)B2 * B2);
+    d.shifts = ctx.arena.alloc_n<double>(d.kk);
+    d.cstarts = ctx.arena.alloc_n<int>(d.kk);
+    d.vals_only = 1;
+    HSVD_CUDA(cudaMemsetAsync(d.band, 0, (size_t)LDBB * n * sizeof(double), ctx.stream));
+    lu_slot_max = std::max(lu_slot_max, (size_t)n * (2 * B2 + 1 + B2 + 2));
+  }
+  // band LU workspaces (INV_WARPS slots per matrix; slot size of the largest n)
+  double* lu = ctx.arena.alloc_n<double>(lu_slot_max * INV_WARPS * count);
+  for (int g = 0; g < count; ++g) {  // indexed by blockIdx.x in the kernel
+    dev[g].lu = lu;
+    dev[g].lu_slot = (long long)lu_slot_max;
+  }
+  const EigDev* dd =
+      static_cast<const EigDev*>(ctx.staging.put(dev.data(), dev.size() * sizeof(EigDev), ctx.stream));
+
+  // stage 1: dense -> band
+  std::vector<GemmDesc> g1, g2, g3, g4, g5, g6;
+  for (int p = 0; p < npan; ++p) {
+    const int j0 = p * B2, r0 = j0 + B2;
+    ctx.launch_begin();
+    k_panel_qr<<<count, 512, 0, ctx.stream>>>(dd, j0);
+    ctx.check_launch("k_panel_qr");
+    g1.clear(); g2.clear(); g3.clear(); g4.clear(); g5.clear(); g6.clear();
+    for (int g = 0; g < count; ++g) {
+      const EigDev& e = dev[g];
+      const int n = e.n;
+      if (r0 > n - 2) continue;
+      const int m = n - r0;
+      double* A22 = e.A + r0 + (long long)r0 * e.lda;
+      const double* V = e.A + r0 + (long long)j0 * e.lda;
+      const double* Tp = e.Tp + (long long)p * B2 * B2;
+      double* X = e.VW + r0 + (long long)B2 * n;
+      g1.push_back({A22, V, e.Y + r0, e.lda, e.lda, n, m, B2, m, 1.0, 0.0});       // Y = A22 V
+      g2.push_back({e.Y + r0, Tp, X, n, B2, n, m, B2, B2, 1.0, 0.0});               // X = Y T
+      g3.push_back({V, X, e.P1, e.lda, n, B2, B2, B2, m, 1.0, 0.0});                // P1 = V^T X
+      g4.push_back({Tp, e.P1, e.Mb, B2, B2, B2, B2, B2, B2, 1.0, 0.0});             // M = T^T P1
+      g5.push_back({V, e.Mb, X, e.lda, B2, n, m, B2, B2, -0.5, 1.0});               // W = X - V M/2
+      g6.push_back({e.VW + r0, e.WV + r0, A22, n, n, e.lda, m, m, 2 * B2, -1.0, 1.0});  // syr2k
+    }
+    if (g1.empty()) continue;
+    gemm_grouped(ctx, DType::F64, DType::F64, false, false, false, g1);
+    gemm_grouped(ctx, DType::F64, DType::F64, false, false, false, g2);
+    gemm_grouped(ctx, DType::F64, DType::F64, true, false, false, g3);
+    gemm_grouped(ctx, DType::F64, DType::F64, true, false, false, g4);
+    gemm_grouped(ctx, DType::F64, DType::F64, false, false, false, g5);
+    ctx.launch_begin();
+    k_copy_w<<<dim3(256, count), 256, 0, ctx.stream>>>(dd, j0);
+    ctx.check_launch("k_copy_w");
+    gemm_grouped(ctx, DType::F64, DType::F64, false, true, true, g6);
+  }
+  for (int g = 0; g < count; ++g)
+    HSVD_CUDA(cudaMemcpyAsync(dev[g].band0, dev[g].band, (size_t)LDBB * dev[g].n * sizeof(double),
+                              cudaMemcpyDeviceToDevice, ctx.stream));
+  // stage 2: band -> tridiagonal (values), eigenvalues by bisection
+  ctx.launch_begin();
+  k_chase<<<count, 512, 0, ctx.stream>>>(dd);
+  ctx.check_launch("k_chase");
+  {
+    const size_t smem = (3 * (size_t)nmax + 3 * (size_t)kkmax + 32) * sizeof(double) +
+                        (size_t)kkmax * sizeof(int) + 64;
+    HSVD_CUDA(cudaFuncSetAttribute(k_steig, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ctx.launch_begin();
+    k_steig<<<count, EIG_THREADS, smem, ctx.stream>>>(dd);
+    ctx.check_launch("k_steig");
+  }
+  // eigenvectors of the band matrix
+  {
+    const size_t smem = ((size_t)INV_WARPS * (B2 + 1) * (2 * B2 + 1) + kkmax + 64) * sizeof(double);
+    HSVD_CUDA(cudaFuncSetAttribute(k_band_invit, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem));
+    ctx.launch_begin();
+    k_band_invit<<<count, INV_WARPS * 32, smem, ctx.stream>>>(dd);
+    ctx.check_launch("k_band_invit");
+  }
+  // back through the stage-1 reflectors
+  back_transform(ctx, jobs, dev, dd, nmax, B2);
+}
+
 }  // namespace
 
 void eig_topk(Ctx& ctx, const std::vector<EigJob>& jobs_in) {
@@ -780,6 +1365,13 @@ void eig_topk(Ctx& ctx, const std::vector<EigJob>& jobs_in) {
   const EigDev* dd =
       static_cast<const EigDev*>(ctx.staging.put(dev.data(), dev.size() * sizeof(EigDev), ctx.stream));
 
+  int two_stage_min = kTwoStageMinN;
+  if (const char* env = std::getenv("HSVD_TWO_STAGE_MIN_N")) two_stage_min = std::atoi(env);
+  if (nmax >= two_stage_min) {
+    two_stage(ctx, jobs, dev, nmax, kkmax);
+    ctx.arena.release(mk);
+    return;
+  }
   // 1. tridiagonalise
   int blocked_min = kBlockedMinN;
   if (const char* env = std::getenv("HSVD_BLOCKED_MIN_N")) blocked_min = std::atoi(env);
@@ -835,64 +1427,7 @@ void eig_topk(Ctx& ctx, const std::vector<EigJob>& jobs_in) {
     ctx.check_launch("k_steig");
   }
   // 3. back-transform Z <- Q Z (blocks applied last to first)
-  if (nmax > 2) {
-    const long long nn = (long long)nmax * nmax;
-    int gx = static_cast<int>(std::min<long long>((nn + 255) / 256, 2048));
-    ctx.launch_begin();
-    k_prep_v<<<dim3(gx, count), 256, 0, ctx.stream>>>(dd);
-    ctx.check_launch("k_prep_v");
-    const int nblk_max = ceil_div(nmax - 1, NBT);
-    // S_b = V_b^T V_b for every block of every matrix (one grouped launch)
-    std::vector<GemmDesc> ds;
-    for (int g = 0; g < count; ++g) {
-      const EigDev& e = dev[g];
-      if (e.n <= 2) continue;
-      for (int b = 0; b * NBT < e.n - 1; ++b) {
-        const int j0 = b * NBT, nb = std::min(NBT, e.n - 1 - j0), m = e.n - j0 - 1;
-        const double* V = e.A + j0 + 1 + (long long)j0 * e.lda;
-        ds.push_back({V, V, e.S + (long long)b * NBT * NBT, e.lda, e.lda, NBT, nb, nb, m, 1.0,
-                      0.0});
-      }
-    }
-    gemm_grouped(ctx, DType::F64, DType::F64, true, false, true, ds);
-    const size_t tsm = ((size_t)NBT * (NBT + 1) + NBT) * sizeof(double);
-    HSVD_CUDA(cudaFuncSetAttribute(k_build_t, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
-    ctx.launch_begin();
-    k_build_t<<<dim3(nblk_max, count), NBT, tsm, ctx.stream>>>(dd);
-    ctx.check_launch("k_build_t");
-    std::vector<double*> W(count), W2(count);
-    for (int g = 0; g < count; ++g) {
-      W[g] = ctx.arena.alloc_n<double>((size_t)NBT * jobs[g].kk);
-      W2[g] = ctx.arena.alloc_n<double>((size_t)NBT * jobs[g].kk);
-    }
-    std::vector<GemmDesc> d1, d2, d3;
-    for (int b = nblk_max - 1; b >= 0; --b) {
-      const int j0 = b * NBT;
-      d1.clear();
-      d2.clear();
-      d3.clear();
-      for (int g = 0; g < count; ++g) {
-        const EigDev& e = dev[g];
-        const int nref = e.n - 1;
-        if (j0 >= nref || e.n <= 2) continue;
-        const int m = e.n - j0 - 1;
-        const int nb = std::min(NBT, nref - j0);
-        const double* V = e.A + j0 + 1 + (long long)j0 * e.lda;
-        double* Zs = e.Z + j0 + 1;
-        // W = V^T Zs   (nb x kk)
-        d1.push_back({V, Zs, W[g], e.lda, e.ldz, NBT, nb, e.kk, m, 1.0, 0.0});
-        // W2 = T W
-        d2.push_back({e.T + (long long)b * NBT * NBT, W[g], W2[g], NBT, NBT, NBT, nb, e.kk, nb,
-                      1.0, 0.0});
-        // Zs -= V W2
-        d3.push_back({V, W2[g], Zs, e.lda, NBT, e.ldz, m, e.kk, nb, -1.0, 1.0});
-      }
-      if (d1.empty()) continue;
-      gemm_grouped(ctx, DType::F64, DType::F64, true, false, false, d1);
-      gemm_grouped(ctx, DType::F64, DType::F64, false, false, false, d2);
-      gemm_grouped(ctx, DType::F64, DType::F64, false, false, false, d3);
-    }
-  }
+  back_transform(ctx, jobs, dev, dd, nmax, 1);
   ctx.arena.release(mk);
 }
 

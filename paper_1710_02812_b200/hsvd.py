@@ -74,7 +74,7 @@ EXPORTED = [
     "hsvd_cu_result_device", "hsvd_cu_result_free",
     "hsvd_cu_nccl_unique_id", "hsvd_cu_ctx_init_nccl", "hsvd_cu_thread_group_create",
     "hsvd_cu_thread_group_free", "hsvd_cu_ctx_join_group", "hsvd_cu_shard_rows",
-    "hsvd_cu_rank_k_svd_sharded",
+    "hsvd_cu_rank_k_svd_sharded", "hsvd_cu_syevx_topk",
 ]
 
 
@@ -133,6 +133,7 @@ def load_library(path: str = LIB_PATH):
         lib.hsvd_cu_ctx_join_group.argtypes = [P, P, I32]
         lib.hsvd_cu_shard_rows.argtypes = [I64, I64, I32, I32, C.POINTER(I64), C.POINTER(I64)]
         lib.hsvd_cu_rank_k_svd_sharded.argtypes = xargs + [I64, I64, C.POINTER(_Config), pp]
+        lib.hsvd_cu_syevx_topk.argtypes = [P, P, I64, I64, P, P]
         _lib = lib
         return lib
 
@@ -551,6 +552,19 @@ def rank_k_svd_device(x, cfg: MatConfig, ctx: Context) -> int:
         return int(rank.value)
     finally:
         ctx.lib.hsvd_cu_result_free(h)
+
+
+def syevx_topk(a, kk: int, ctx: Optional[Context] = None):
+    """Top-kk eigenpairs of a symmetric matrix on the device eigensolver
+    (the building block of every SVD in the path): (lam desc, Z n x kk)."""
+    cx = _ctx(ctx)
+    a = np.asfortranarray(np.asarray(a, dtype=np.float64))
+    n = a.shape[0]
+    lam = np.empty(kk)
+    z = np.empty((kk, n))  # column-major n x kk == row-major kk x n
+    _check(cx.lib.hsvd_cu_syevx_topk(cx.handle, a.ctypes.data, n, int(kk), lam.ctypes.data,
+                                     z.ctypes.data))
+    return lam, z.T.copy()
 
 
 def svd_of_col_slices(x_slice, c: int, gamma: float, max_rank: Optional[int] = None,
