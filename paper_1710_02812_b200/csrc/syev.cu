@@ -851,12 +851,17 @@ __device__ __forceinline__ unsigned long long prog_encode(int s, unsigned steps)
 }
 constexpr unsigned kSweepDone = 0x7fffffffu;
 
-__global__ void __launch_bounds__(512) k_chase(const EigDev* __restrict__ jobs) {
+constexpr int CHASE_WARPS = 8;
+static_assert(B2 == 32, "k_chase maps one band row per lane");
+
+__global__ void __launch_bounds__(CHASE_WARPS * 32, 1) k_chase(const EigDev* __restrict__ jobs) {
   const EigDev J = jobs[blockIdx.x];
   const int n = J.n;
   double* bb = J.band;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, W = blockDim.x >> 5;
   __shared__ unsigned long long prog[32];
+  __shared__ double vsh[CHASE_WARPS][B2];
+  __shared__ double wsh[CHASE_WARPS][B2];
   if (tid < W) prog[tid] = prog_encode(tid - W, kSweepDone);
   __syncthreads();
   volatile unsigned long long* vprog = prog;
@@ -880,7 +885,21 @@ __global__ void __launch_bounds__(512) k_chase(const EigDev* __restrict__ jobs) 
         __threadfence_block();
       }
       const int c = k == 0 ? s : s + 1 + (k - 1) * B2;
-      double x = lane < L ? band_at(bb, r0 + lane, c) : 0.0;
+      const int nl = r0 - c - 1;                 // left-block columns (0 or B2-1)
+      const int na = min(n, r0 + 2 * B2) - r1;   // rows after R
+      // all loads of the step issued together (one memory round trip)
+      const double x = lane < L ? band_at(bb, r0 + lane, c) : 0.0;
+      double yl[B2 - 1], ar[B2], ya[B2];
+#pragma unroll
+      for (int l = 0; l < B2 - 1; ++l)
+        yl[l] = (l < nl && lane < L) ? band_at(bb, r0 + lane, c + 1 + l) : 0.0;
+#pragma unroll
+      for (int j = 0; j < B2; ++j)
+        ar[j] = (j < L && lane < L)
+                    ? (lane >= j ? band_at(bb, r0 + lane, r0 + j) : band_at(bb, r0 + j, r0 + lane))
+                    : 0.0;
+#pragma unroll
+      for (int j = 0; j < B2; ++j) ya[j] = (j < L && lane < na) ? band_at(bb, r1 + lane, r0 + j) : 0.0;
       const double xn2 = warp_sum(lane >= 1 ? x * x : 0.0);
       const double alpha = __shfl_sync(0xffffffffu, x, 0);
       if (xn2 == 0.0) break;  // no bulge left in this sweep
@@ -889,41 +908,54 @@ __global__ void __launch_bounds__(512) k_chase(const EigDev* __restrict__ jobs) 
       const double tau = (beta - alpha) / beta;
       const double scal = 1.0 / (alpha - beta);
       const double v = lane == 0 ? 1.0 : (lane < L ? x * scal : 0.0);
+      vsh[warp][lane] = v;
       if (lane < L) band_at(bb, r0 + lane, c) = lane == 0 ? beta : 0.0;
-      // rows R x columns (c, r0): left application
-      for (int l = c + 1; l < r0; ++l) {
-        const double y = lane < L ? band_at(bb, r0 + lane, l) : 0.0;
-        const double dt = tau * warp_sum(v * y);
-        if (lane < L) band_at(bb, r0 + lane, l) = y - dt * v;
+      // left block: dots d_l = sum_i v_i y_il by a transposing butterfly
+      // (lane l ends with d_l), then y_il -= tau v_i d_l
+      if (nl > 0) {
+        double t[B2];
+#pragma unroll
+        for (int l = 0; l < B2 - 1; ++l) t[l] = v * yl[l];
+        t[B2 - 1] = 0.0;
+#pragma unroll
+        for (int ofs = 16; ofs >= 1; ofs >>= 1) {
+          const bool up = (lane & ofs) != 0;
+#pragma unroll
+          for (int j = 0; j < ofs; ++j) {
+            const double send = up ? t[j] : t[j + ofs];
+            const double got = __shfl_xor_sync(0xffffffffu, send, ofs);
+            t[j] = (up ? t[j + ofs] : t[j]) + got;
+          }
+        }
+        const double dl = tau * t[0];
+#pragma unroll
+        for (int l = 0; l < B2 - 1; ++l) {
+          const double d = __shfl_sync(0xffffffffu, dl, l);
+          if (l < nl && lane < L) band_at(bb, r0 + lane, c + 1 + l) = yl[l] - d * v;
+        }
       }
+      __syncwarp();
       // R x R: two-sided (symmetric, lower storage)
       double p = 0.0;
-      for (int j = 0; j < L; ++j) {
-        const double vj = __shfl_sync(0xffffffffu, v, j);
-        double a = 0.0;
-        if (lane < L) a = lane >= j ? band_at(bb, r0 + lane, r0 + j) : band_at(bb, r0 + j, r0 + lane);
-        p += a * vj;
-      }
+#pragma unroll
+      for (int j = 0; j < B2; ++j) p += ar[j] * vsh[warp][j];
       p *= tau;
       const double al = -0.5 * tau * warp_sum(p * v);
       const double w = p + al * v;
-      for (int j = 0; j < L; ++j) {
-        const double vj = __shfl_sync(0xffffffffu, v, j);
-        const double wj = __shfl_sync(0xffffffffu, w, j);
-        if (lane < L && lane >= j) band_at(bb, r0 + lane, r0 + j) -= v * wj + w * vj;
-      }
+      wsh[warp][lane] = w;
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < B2; ++j)
+        if (j < L && lane < L && lane >= j)
+          band_at(bb, r0 + lane, r0 + j) = ar[j] - (v * wsh[warp][j] + w * vsh[warp][j]);
       // rows after R x R: right application (creates the next bulge)
-      const int na = min(n, r0 + 2 * B2) - r1;
       double y = 0.0;
-      for (int j = 0; j < L; ++j) {
-        const double vj = __shfl_sync(0xffffffffu, v, j);
-        if (lane < na) y += band_at(bb, r1 + lane, r0 + j) * vj;
-      }
+#pragma unroll
+      for (int j = 0; j < B2; ++j) y += ya[j] * vsh[warp][j];
       y *= tau;
-      for (int j = 0; j < L; ++j) {
-        const double vj = __shfl_sync(0xffffffffu, v, j);
-        if (lane < na) band_at(bb, r1 + lane, r0 + j) -= y * vj;
-      }
+#pragma unroll
+      for (int j = 0; j < B2; ++j)
+        if (j < L && lane < na) band_at(bb, r1 + lane, r0 + j) = ya[j] - y * vsh[warp][j];
       __syncwarp();
       __threadfence_block();
       if (lane == 0) vprog[warp] = prog_encode(s, (unsigned)(k + 1));
@@ -985,9 +1017,21 @@ __global__ void __launch_bounds__(INV_WARPS * 32) k_band_invit(const EigDev* __r
       for (int c = lane; c <= 2 * B2; c += 32)
         if (c < n) win[(i % WR) * WC + (c % WC)] = band_full(b0, n, i, c) - (i == c ? sh : 0.0);
     __syncwarp();
+    // row j+B2+1 (entering at step j) prefetched one step ahead
+    double pre[3];
+    auto fetch_row = [&](int rn, int jj) {
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const int cc = lane + 32 * q, col = jj + 1 + cc;
+        pre[q] = (rn < n && cc < WC && col < n) ? band_full(b0, n, rn, col) - (rn == col ? sh : 0.0)
+                                                : 0.0;
+      }
+    };
+    fetch_row(B2 + 1, 0);
     for (int j = 0; j < n; ++j) {
-      const int nw = min(B2 + 1, n - j);  // candidate rows j..j+nw-1
-      double a = lane < nw ? fabs(win[((j + lane) % WR) * WC + (j % WC)]) : -1.0;
+      const int nw = min(B2 + 1, n - j);  // candidate rows j..j+nw-1 (row j+lane on lane)
+      const int cj = j % WC;
+      double a = lane < nw ? fabs(win[((j + lane) % WR) * WC + cj]) : -1.0;
       int p = lane;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
@@ -1006,36 +1050,35 @@ __global__ void __launch_bounds__(INV_WARPS * 32) k_band_invit(const EigDev* __r
           win[sp + c] = tmp;
         }
       __syncwarp();
-      double u = win[sj + (j % WC)];
+      double u = win[sj + cj];
       if (fabs(u) < tiny) u = u < 0.0 ? -tiny : tiny;
+      const int ncol = min(2 * B2, n - 1 - j);
+      // lane i (1..nw-1) eliminates row j+i over columns j+1..j+ncol
+      if (lane >= 1 && lane < nw) {
+        const int si = ((j + lane) % WR) * WC;
+        const double l = win[si + cj] / u;
+        for (int cc = 1; cc <= ncol; ++cc) {
+          const int col = (j + cc) % WC;
+          win[si + col] -= l * win[sj + col];
+        }
+        Lm[(size_t)j * B2 + (lane - 1)] = l;
+        win[si + cj] = 0.0;  // column j leaves; slot becomes column j+2B2+1
+      }
       if (lane == 0) {
         piv[j] = (double)p;
-        win[sj + (j % WC)] = u;
-      }
-      // multipliers and elimination of rows j+1..j+nw-1 over columns j+1..j+2B2
-      const int ncol = min(2 * B2, n - 1 - j);
-      for (int i = 1; i < nw; ++i) {
-        const int si = ((j + i) % WR) * WC;
-        const double l = win[si + (j % WC)] / u;
-        for (int cc = 1 + lane; cc <= ncol; cc += 32) win[si + ((j + cc) % WC)] -= l * win[sj + ((j + cc) % WC)];
-        if (lane == 0) Lm[(size_t)j * B2 + (i - 1)] = l;
+        win[sj + cj] = u;
       }
       __syncwarp();
       for (int cc = lane; cc < WC; cc += 32)
         U[(size_t)j * WC + cc] = (cc <= ncol) ? win[sj + ((j + cc) % WC)] : 0.0;
       __syncwarp();
-      // recycle the slot of row j for row j+B2+1; column j+2B2+1 enters
-      const int rn = j + B2 + 1;
-      const int cnew = (j + 2 * B2 + 1) % WC;
-      for (int i = 1; i < nw; ++i)
-        if (lane == 0) win[((j + i) % WR) * WC + cnew] = 0.0;
-      for (int c = lane; c < WC; c += 32) win[sj + c] = 0.0;
-      __syncwarp();
-      if (rn < n)
-        for (int cc = lane; cc < WC; cc += 32) {
-          const int col = j + 1 + cc;
-          if (col < n) win[sj + (col % WC)] = band_full(b0, n, rn, col) - (rn == col ? sh : 0.0);
-        }
+      // the slot of row j now holds row j+B2+1 (columns j+1..j+2B2+1)
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const int cc = lane + 32 * q;
+        if (cc < WC) win[sj + ((j + 1 + cc) % WC)] = pre[q];
+      }
+      fetch_row(j + B2 + 2, j + 1);
       __syncwarp();
     }
     // --- three solves from a deterministic start vector
@@ -1306,7 +1349,7 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
                               cudaMemcpyDeviceToDevice, ctx.stream));
   // stage 2: band -> tridiagonal (values), eigenvalues by bisection
   ctx.launch_begin();
-  k_chase<<<count, 512, 0, ctx.stream>>>(dd);
+  k_chase<<<count, CHASE_WARPS * 32, 0, ctx.stream>>>(dd);
   ctx.check_launch("k_chase");
   {
     const size_t smem = (3 * (size_t)nmax + 3 * (size_t)kkmax + 32) * sizeof(double) +
