@@ -110,7 +110,11 @@ class Staging {
     if (dev_) cudaFree(dev_);
   }
   // Copies `bytes` from src into the ring and returns the device address.
-  void* put(const void* src, size_t bytes, cudaStream_t s) {
+  // The device copy is only valid until the ring wraps (one launch): arrays
+  // read by several launches go through put_to() into arena memory.
+  void* put(const void* src, size_t bytes, cudaStream_t s) { return put_to(nullptr, src, bytes, s); }
+  // Same, with the device destination `dst` (nullptr = the ring's own copy).
+  void* put_to(void* dst, const void* src, size_t bytes, cudaStream_t s) {
     size_t b = (bytes + 255) & ~size_t(255);
     if (b > size_) throw Error(kInvalid, "staging ring too small");
     if (off_ + b > size_) {
@@ -118,7 +122,7 @@ class Staging {
       off_ = 0;
     }
     char* h = static_cast<char*>(host_) + off_;
-    char* d = static_cast<char*>(dev_) + off_;
+    char* d = dst ? static_cast<char*>(dst) : static_cast<char*>(dev_) + off_;
     std::memcpy(h, src, bytes);
     HSVD_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s));
     off_ += b;

@@ -1031,8 +1031,16 @@ __global__ void __launch_bounds__(INV_WARPS * 32) k_band_invit(const EigDev* __r
     for (int j = 0; j < n; ++j) {
       const int nw = min(B2 + 1, n - j);  // candidate rows j..j+nw-1 (row j+lane on lane)
       const int cj = j % WC;
+      // lane i holds candidate row j+i; lane 0 also row j+B2 (WR = 33 rows)
       double a = lane < nw ? fabs(win[((j + lane) % WR) * WC + cj]) : -1.0;
       int p = lane;
+      if (lane == 0 && nw == WR) {
+        const double a2 = fabs(win[((j + B2) % WR) * WC + cj]);
+        if (a2 > a) {
+          a = a2;
+          p = B2;
+        }
+      }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         const double ao = __shfl_xor_sync(0xffffffffu, a, o);
@@ -1062,8 +1070,20 @@ __global__ void __launch_bounds__(INV_WARPS * 32) k_band_invit(const EigDev* __r
           win[si + col] -= l * win[sj + col];
         }
         Lm[(size_t)j * B2 + (lane - 1)] = l;
-        win[si + cj] = 0.0;  // column j leaves; slot becomes column j+2B2+1
       }
+      if (nw == WR) {  // row j+B2: columns split over the lanes
+        const int si = ((j + B2) % WR) * WC;
+        const double l = win[si + cj] / u;
+        for (int cc = 1 + lane; cc <= ncol; cc += 32) {
+          const int col = (j + cc) % WC;
+          win[si + col] -= l * win[sj + col];
+        }
+        if (lane == 0) Lm[(size_t)j * B2 + (B2 - 1)] = l;
+      }
+      __syncwarp();
+      // column j leaves; its slot becomes column j+2B2+1
+      if (lane >= 1 && lane < nw) win[((j + lane) % WR) * WC + cj] = 0.0;
+      if (lane == 0 && nw == WR) win[((j + B2) % WR) * WC + cj] = 0.0;
       if (lane == 0) {
         piv[j] = (double)p;
         win[sj + cj] = u;
@@ -1278,6 +1298,14 @@ void back_transform(Ctx& ctx, const std::vector<EigJob>& jobs, const std::vector
   }
 }
 
+// The job array is read by every launch of the solver, so it lives in arena
+// memory rather than in the staging ring (which later launches recycle).
+const EigDev* upload_jobs(Ctx& ctx, const std::vector<EigDev>& dev) {
+  const size_t bytes = dev.size() * sizeof(EigDev);
+  return static_cast<const EigDev*>(
+      ctx.staging.put_to(ctx.arena.alloc(bytes), dev.data(), bytes, ctx.stream));
+}
+
 void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& dev, int nmax,
                int kkmax) {
   const int count = static_cast<int>(dev.size());
@@ -1307,7 +1335,7 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
     dev[g].lu_slot = (long long)lu_slot_max;
   }
   const EigDev* dd =
-      static_cast<const EigDev*>(ctx.staging.put(dev.data(), dev.size() * sizeof(EigDev), ctx.stream));
+      upload_jobs(ctx, dev);
 
   // stage 1: dense -> band
   std::vector<GemmDesc> g1, g2, g3, g4, g5, g6;
@@ -1406,7 +1434,7 @@ void eig_topk(Ctx& ctx, const std::vector<EigJob>& jobs_in) {
     kkmax = std::max(kkmax, j.kk);
   }
   const EigDev* dd =
-      static_cast<const EigDev*>(ctx.staging.put(dev.data(), dev.size() * sizeof(EigDev), ctx.stream));
+      upload_jobs(ctx, dev);
 
   int two_stage_min = kTwoStageMinN;
   if (const char* env = std::getenv("HSVD_TWO_STAGE_MIN_N")) two_stage_min = std::atoi(env);
@@ -1423,8 +1451,7 @@ void eig_topk(Ctx& ctx, const std::vector<EigJob>& jobs_in) {
       dev[g].VW = ctx.arena.alloc_n<double>((size_t)dev[g].n * 2 * NB);
       dev[g].WV = ctx.arena.alloc_n<double>((size_t)dev[g].n * 2 * NB);
     }
-    dd = static_cast<const EigDev*>(
-        ctx.staging.put(dev.data(), dev.size() * sizeof(EigDev), ctx.stream));
+    dd = upload_jobs(ctx, dev);
     const int R = ceil_div(nmax, LAT);
     // cluster size: spread each matrix's mat-vec over several SMs while the
     // batch alone would leave SMs idle
