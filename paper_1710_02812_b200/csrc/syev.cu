@@ -38,7 +38,7 @@ constexpr int EIG_THREADS = 256;
 constexpr int NB = 32;       // reflectors per compact-WY block
 constexpr int B2 = 32;       // bandwidth of the two-stage reduction
 constexpr int LDBB = 2 * B2 + 1;  // band storage: diagonals 0..2*B2 (chase fill)
-constexpr int INV_WARPS = 8;      // warps (= LU workspace slots) per band inverse iteration CTA
+constexpr int INV_WARPS = 4;      // warps (= LU workspace slots) per band inverse iteration CTA
 
 struct EigDev {
   double* A;
@@ -66,7 +66,7 @@ struct EigDev {
   double* Y;         // n x B2
   double* P1;        // B2 x B2
   double* Mb;        // B2 x B2
-  double* lu;        // per-warp band LU workspace (INV_WARPS slots per matrix)
+  double* lu;        // per-warp band LU workspace (cpm * INV_WARPS slots per matrix)
   long long lu_slot;  // doubles per slot
 };
 
@@ -972,10 +972,14 @@ __global__ void __launch_bounds__(CHASE_WARPS * 32, 1) k_chase(const EigDev* __r
 }
 
 // Eigenvectors of the band matrix (band0, bandwidth B2) by inverse
-// iteration: per warp, band LU with partial pivoting of (B - shift I) kept
-// in a (B2+1) x (2*B2+1) shared-memory window (U rows and multipliers
-// streamed to the warp's workspace), three solves; then Gram-Schmidt inside
-// clusters (as k_steig).
+// iteration, one warp per shift on a (cpm x count) grid.  The warp factors
+// (B - shift I) = P L U with partial pivoting in a (B2+1) x (2*B2+1)
+// shared-memory window (entering band rows prefetched two steps ahead),
+// streaming U rows and multipliers to its workspace; then three
+// forward/backward solves.  The solves keep the live part of the vector in
+// a 128-entry shared ring and prefetch U / L rows and vector entries one
+// INV_PF-step chunk ahead, so their step chain never waits on HBM.
+// k_band_mgs orthogonalises inside eigenvalue clusters afterwards.
 __device__ __forceinline__ double band_full(const double* b0, int n, int i, int j) {
   if (i < 0 || j < 0 || i >= n || j >= n) return 0.0;
   const int d = i - j;
@@ -983,17 +987,24 @@ __device__ __forceinline__ double band_full(const double* b0, int n, int i, int 
   return d >= 0 ? b0[d + (long long)j * LDBB] : b0[-d + (long long)i * LDBB];
 }
 
-__global__ void __launch_bounds__(INV_WARPS * 32) k_band_invit(const EigDev* __restrict__ jobs) {
-  const EigDev J = jobs[blockIdx.x];
+constexpr int INV_PF = 8;      // solve prefetch chunk (steps)
+constexpr int INV_RING = 128;  // vector ring entries per warp (>= 2*B2+1)
+
+__device__ __forceinline__ double invit_start(int r, int t) {
+  const unsigned h = hash32((unsigned)r * 2654435761u ^ hash32((unsigned)t + 0x9e3779b9u));
+  return ((double)h / 4294967296.0) * 2.0 - 1.0;
+}
+
+__global__ void __launch_bounds__(INV_WARPS * 32, 3) k_band_invit(const EigDev* __restrict__ jobs) {
+  const EigDev J = jobs[blockIdx.y];
   const int n = J.n, kk = J.kk;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nt = blockDim.x;
   constexpr int WR = B2 + 1, WC = 2 * B2 + 1;  // window rows / columns
   extern __shared__ double sm[];
   double* win = sm + (size_t)warp * WR * WC;
-  double* dots = sm + (size_t)INV_WARPS * WR * WC;
-  double* red = dots + kk;
+  double* yw = sm + (size_t)INV_WARPS * WR * WC + (size_t)warp * INV_RING;
+  double* red = sm + (size_t)INV_WARPS * (WR * WC + INV_RING);
   const double* b0 = J.band0;
-  const double eps = DBL_EPSILON;
   // ||B||_inf for the pivot guard
   double nb = 0.0;
   for (int i = tid; i < n; i += nt) {
@@ -1002,24 +1013,26 @@ __global__ void __launch_bounds__(INV_WARPS * 32) k_band_invit(const EigDev* __r
     nb = fmax(nb, s);
   }
   const double bnorm = block_max(nb, red);
-  const double tiny = eps * fmax(bnorm, DBL_MIN);
-  // workspace of this warp: U rows (n x WC), multipliers (n x B2), pivots, y
-  double* U = J.lu + ((size_t)blockIdx.x * INV_WARPS + warp) * (size_t)J.lu_slot;
+  const double tiny = DBL_EPSILON * fmax(bnorm, DBL_MIN);
+  const int gw = blockIdx.x * INV_WARPS + warp, nw_total = gridDim.x * INV_WARPS;
+  // workspace of this warp: U rows (n x WC), multipliers (n x B2), pivots,
+  // forward result F, iterate X
+  double* U = J.lu + ((size_t)blockIdx.y * nw_total + gw) * (size_t)J.lu_slot;
   double* Lm = U + (size_t)n * WC;
-  double* piv = Lm + (size_t)n * B2;  // stored as doubles
-  double* yv = piv + n;
-  for (int t = warp; t < kk; t += INV_WARPS) {
+  int* piv = reinterpret_cast<int*>(Lm + (size_t)n * B2);
+  double* F = Lm + (size_t)n * B2 + n;
+  double* X = F + n;
+  for (int t = gw; t < kk; t += nw_total) {
     const double sh = J.shifts[t];
-    // --- factorisation: window rows are slots (row % WR), columns (col % WC)
+    // ---- factorisation: window rows are slots (row % WR), columns (col % WC)
     for (int e = lane; e < WR * WC; e += 32) win[e] = 0.0;
     __syncwarp();
     for (int i = 0; i <= B2 && i < n; ++i)
       for (int c = lane; c <= 2 * B2; c += 32)
         if (c < n) win[(i % WR) * WC + (c % WC)] = band_full(b0, n, i, c) - (i == c ? sh : 0.0);
     __syncwarp();
-    // row j+B2+1 (entering at step j) prefetched one step ahead
-    double pre[3];
-    auto fetch_row = [&](int rn, int jj) {
+    double preA[3], preB[3];
+    auto fetch_row = [&](double* pre, int rn, int jj) {
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
         const int cc = lane + 32 * q, col = jj + 1 + cc;
@@ -1027,11 +1040,12 @@ __global__ void __launch_bounds__(INV_WARPS * 32) k_band_invit(const EigDev* __r
                                                 : 0.0;
       }
     };
-    fetch_row(B2 + 1, 0);
+    fetch_row(preA, B2 + 1, 0);
+    fetch_row(preB, B2 + 2, 1);
     for (int j = 0; j < n; ++j) {
-      const int nw = min(B2 + 1, n - j);  // candidate rows j..j+nw-1 (row j+lane on lane)
+      const int nw = min(WR, n - j);  // candidate rows j..j+nw-1
       const int cj = j % WC;
-      // lane i holds candidate row j+i; lane 0 also row j+B2 (WR = 33 rows)
+      // lane i holds candidate row j+i; lane 0 also row j+B2
       double a = lane < nw ? fabs(win[((j + lane) % WR) * WC + cj]) : -1.0;
       int p = lane;
       if (lane == 0 && nw == WR) {
@@ -1060,23 +1074,25 @@ __global__ void __launch_bounds__(INV_WARPS * 32) k_band_invit(const EigDev* __r
       __syncwarp();
       double u = win[sj + cj];
       if (fabs(u) < tiny) u = u < 0.0 ? -tiny : tiny;
+      const double ru = 1.0 / u;
       const int ncol = min(2 * B2, n - 1 - j);
-      // lane i (1..nw-1) eliminates row j+i over columns j+1..j+ncol
+      // columns j+1..j+ncol sit in slots cj+1..WC-1 then 0..(cj+ncol-WC)
+      const int hi1 = min(WC - 1, cj + ncol), hi2 = cj + ncol - WC;
+      // lane i (1..nw-1) eliminates row j+i
       if (lane >= 1 && lane < nw) {
         const int si = ((j + lane) % WR) * WC;
-        const double l = win[si + cj] / u;
-        for (int cc = 1; cc <= ncol; ++cc) {
-          const int col = (j + cc) % WC;
-          win[si + col] -= l * win[sj + col];
-        }
+        const double l = win[si + cj] * ru;
+        for (int c = cj + 1; c <= hi1; ++c) win[si + c] -= l * win[sj + c];
+        for (int c = 0; c <= hi2; ++c) win[si + c] -= l * win[sj + c];
         Lm[(size_t)j * B2 + (lane - 1)] = l;
       }
-      if (nw == WR) {  // row j+B2: columns split over the lanes
+      if (nw == WR) {  // row j+B2: its columns split over the lanes
         const int si = ((j + B2) % WR) * WC;
-        const double l = win[si + cj] / u;
+        const double l = win[si + cj] * ru;
         for (int cc = 1 + lane; cc <= ncol; cc += 32) {
-          const int col = (j + cc) % WC;
-          win[si + col] -= l * win[sj + col];
+          int c = cj + cc;
+          c -= c >= WC ? WC : 0;
+          win[si + c] -= l * win[sj + c];
         }
         if (lane == 0) Lm[(size_t)j * B2 + (B2 - 1)] = l;
       }
@@ -1085,92 +1101,259 @@ __global__ void __launch_bounds__(INV_WARPS * 32) k_band_invit(const EigDev* __r
       if (lane >= 1 && lane < nw) win[((j + lane) % WR) * WC + cj] = 0.0;
       if (lane == 0 && nw == WR) win[((j + B2) % WR) * WC + cj] = 0.0;
       if (lane == 0) {
-        piv[j] = (double)p;
+        piv[j] = p;
         win[sj + cj] = u;
       }
       __syncwarp();
-      for (int cc = lane; cc < WC; cc += 32)
-        U[(size_t)j * WC + cc] = (cc <= ncol) ? win[sj + ((j + cc) % WC)] : 0.0;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const int cc = lane + 32 * q;
+        if (cc < WC) {
+          int c = cj + cc;
+          c -= c >= WC ? WC : 0;
+          U[(size_t)j * WC + cc] = (cc <= ncol) ? win[sj + c] : 0.0;
+        }
+      }
       __syncwarp();
       // the slot of row j now holds row j+B2+1 (columns j+1..j+2B2+1)
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
         const int cc = lane + 32 * q;
-        if (cc < WC) win[sj + ((j + 1 + cc) % WC)] = pre[q];
+        if (cc < WC) {
+          int c = cj + 1 + cc;
+          c -= c >= WC ? WC : 0;
+          win[sj + c] = preA[q];
+        }
       }
-      fetch_row(j + B2 + 2, j + 1);
+#pragma unroll
+      for (int q = 0; q < 3; ++q) preA[q] = preB[q];
+      fetch_row(preB, j + B2 + 3, j + 2);
       __syncwarp();
-    }
-    // --- three solves from a deterministic start vector
-    double* z = J.Z + (long long)t * J.ldz;
-    for (int r = lane; r < n; r += 32) {
-      const unsigned h = hash32((unsigned)r * 2654435761u ^ hash32((unsigned)t + 0x9e3779b9u));
-      yv[r] = ((double)h / 4294967296.0) * 2.0 - 1.0;
     }
     __syncwarp();
+    // ---- three solves; iterate it reads X scaled by sc (it = 0: start vector)
+    double sc = 1.0;
+    bool unit = false;  // previous iterate degenerate: restart from e_t
     for (int it = 0; it < 3; ++it) {
-      // forward: row swaps + L
-      for (int j = 0; j < n; ++j) {
-        const int p = (int)piv[j];
-        if (p != 0 && lane == 0) {
-          const double tmp = yv[j];
-          yv[j] = yv[j + p];
-          yv[j + p] = tmp;
-        }
-        __syncwarp();
-        const double yj = yv[j];
-        const int nw = min(B2 + 1, n - j);
-        if (lane + 1 < nw) yv[j + 1 + lane] -= Lm[(size_t)j * B2 + lane] * yj;
-        __syncwarp();
-      }
-      // backward: U x = y
-      for (int j = n - 1; j >= 0; --j) {
-        const double* ur = U + (size_t)j * WC;
-        double s = 0.0;
-        for (int cc = 1 + lane; cc < WC; cc += 32)
-          if (j + cc < n) s += ur[cc] * yv[j + cc];
-        s = warp_sum(s);
-        if (lane == 0) yv[j] = (yv[j] - s) / ur[0];
-        __syncwarp();
-      }
-      double s2 = 0.0;
-      for (int r = lane; r < n; r += 32) s2 += yv[r] * yv[r];
-      s2 = warp_sum(s2);
-      double sc = s2 > 0.0 && isfinite(s2) ? 1.0 / sqrt(s2) : 0.0;
-      for (int r = lane; r < n; r += 32) yv[r] = sc == 0.0 ? (r == t % n ? 1.0 : 0.0) : yv[r] * sc;
+      auto input = [&](int r) -> double {
+        if (r >= n) return 0.0;
+        if (it == 0) return invit_start(r, t);
+        if (unit) return r == t % n ? 1.0 : 0.0;
+        return X[r] * sc;
+      };
+      // forward: y <- L^-1 P y.  Ring holds y[j..j+B2] before step j.
+      for (int r = lane; r <= B2; r += 32) yw[r] = input(r);
       __syncwarp();
+      {
+        // chunk j0..j0+INV_PF-1: lane d holds the pivot and the entering
+        // entry of step j0+d, every lane its multiplier of each step
+        double Lc[INV_PF], Ln[INV_PF];
+        int pc, pn;
+        double ec, en;
+        auto load = [&](int j0, double* Lx, int& px, double& ex) {
+#pragma unroll
+          for (int d = 0; d < INV_PF; ++d) {
+            const int j = j0 + d;
+            Lx[d] = j < n ? Lm[(size_t)j * B2 + lane] : 0.0;
+          }
+          const int jl = j0 + lane;
+          px = (lane < INV_PF && jl < n) ? piv[jl] : 0;
+          ex = lane < INV_PF ? input(jl + B2 + 1) : 0.0;
+        };
+        load(0, Lc, pc, ec);
+        for (int j0 = 0; j0 < n; j0 += INV_PF) {
+          load(j0 + INV_PF, Ln, pn, en);
+#pragma unroll
+          for (int d = 0; d < INV_PF; ++d) {
+            const int j = j0 + d;
+            const int p = __shfl_sync(0xffffffffu, pc, d);
+            const double e = __shfl_sync(0xffffffffu, ec, d);
+            if (j < n) {
+              if (p != 0 && lane == 0) {
+                const double tmp = yw[j & (INV_RING - 1)];
+                yw[j & (INV_RING - 1)] = yw[(j + p) & (INV_RING - 1)];
+                yw[(j + p) & (INV_RING - 1)] = tmp;
+              }
+              __syncwarp();
+              const double yj = yw[j & (INV_RING - 1)];
+              if (j + 1 + lane < n) yw[(j + 1 + lane) & (INV_RING - 1)] -= Lc[d] * yj;
+              if (lane == 0) {
+                F[j] = yj;
+                yw[(j + B2 + 1) & (INV_RING - 1)] = e;
+              }
+              __syncwarp();
+            }
+          }
+#pragma unroll
+          for (int d = 0; d < INV_PF; ++d) Lc[d] = Ln[d];
+          pc = pn;
+          ec = en;
+        }
+      }
+      __syncwarp();
+      // backward: U x = F.  Ring holds x[j+1..j+2B2] before step j.
+      for (int r = lane; r < INV_RING; r += 32) yw[r] = 0.0;
+      __syncwarp();
+      double nrm2 = 0.0;
+      {
+        // chunk j0, j0-1, ..: lane d holds 1/U[j0-d][0] and F[j0-d]
+        double Ac[INV_PF], Bc[INV_PF], An[INV_PF], Bn[INV_PF];
+        double rc, fc, rn, fn;
+        auto load = [&](int j0, double* Ax, double* Bx, double& rx, double& fx) {
+#pragma unroll
+          for (int d = 0; d < INV_PF; ++d) {
+            const int j = j0 - d;
+            const double* ur = U + (size_t)(j >= 0 ? j : 0) * WC;
+            Ax[d] = j >= 0 ? ur[1 + lane] : 0.0;
+            Bx[d] = j >= 0 ? ur[33 + lane] : 0.0;  // lanes 0..31 -> cc 33..64
+          }
+          const int jl = j0 - lane;
+          const bool ok = lane < INV_PF && jl >= 0;
+          rx = ok ? 1.0 / U[(size_t)jl * WC] : 0.0;
+          fx = ok ? F[jl] : 0.0;
+        };
+        load(n - 1, Ac, Bc, rc, fc);
+        for (int j0 = n - 1; j0 >= 0; j0 -= INV_PF) {
+          load(j0 - INV_PF, An, Bn, rn, fn);
+#pragma unroll
+          for (int d = 0; d < INV_PF; ++d) {
+            const int j = j0 - d;
+            const double rj = __shfl_sync(0xffffffffu, rc, d);
+            const double fj = __shfl_sync(0xffffffffu, fc, d);
+            if (j >= 0) {
+              double s = Ac[d] * yw[(j + 1 + lane) & (INV_RING - 1)] +
+                         Bc[d] * yw[(j + 33 + lane) & (INV_RING - 1)];
+              s = warp_sum(s);
+              const double x = (fj - s) * rj;
+              // (ring slots of x[j+2B2+1..] are only reused for indices
+              // that are written before they are read)
+              if (lane == 0) {
+                yw[j & (INV_RING - 1)] = x;
+                X[j] = x;
+              }
+              nrm2 += x * x;
+              __syncwarp();
+            }
+          }
+#pragma unroll
+          for (int d = 0; d < INV_PF; ++d) {
+            Ac[d] = An[d];
+            Bc[d] = Bn[d];
+          }
+          rc = rn;
+          fc = fn;
+        }
+      }
+      __syncwarp();
+      unit = !(nrm2 > 0.0 && isfinite(nrm2));
+      sc = unit ? 0.0 : 1.0 / sqrt(nrm2);
     }
-    for (int r = lane; r < n; r += 32) z[r] = yv[r];
+    double* z = J.Z + (long long)t * J.ldz;
+    for (int r = lane; r < n; r += 32) z[r] = unit ? (r == t % n ? 1.0 : 0.0) : X[r] * sc;
+    __syncwarp();
   }
-  __syncthreads();
-  // Gram-Schmidt (twice) inside clusters, in eigenvalue order
+}
+
+// Orthonormalisation of the inverse-iteration vectors inside eigenvalue
+// clusters, in eigenvalue order (the result of dstein's modified
+// Gram-Schmidt, reorganised for bandwidth): each cluster is processed in
+// panels of GS_P vectors; a panel is first projected against all earlier
+// vectors of its cluster twice (block classical Gram-Schmidt, 32x32 tiles
+// of Z_prev^T Z_panel accumulated through shared memory, so every earlier
+// vector is read once per panel rather than once per vector), then its own
+// vectors are orthonormalised one by one (classical Gram-Schmidt twice).
+// 256 threads; smem: 2*64*33 + 32*33 + 64 doubles.
+constexpr int GS_P = 32;
+constexpr int GS_R = 64;  // rows per staged tile
+constexpr int GS_SMEM_DOUBLES = 2 * GS_R * 33 + GS_P * 33 + 64;
+
+__device__ void cluster_gs(double* Z, long long ldz, int n, int cs, int ce, double* sm) {
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
   const int nwarps = nt >> 5;
-  for (int t = 0; t < kk; ++t) {
-    const int cs = J.cstarts[t];
-    if (cs == t) continue;
-    double* zt = J.Z + (long long)t * J.ldz;
-    for (int rep = 0; rep < 2; ++rep) {
-      for (int c = cs + warp; c < t; c += nwarps) {
-        const double* zc = J.Z + (long long)c * J.ldz;
-        double s = 0.0;
-        for (int r = lane; r < n; r += 32) s += zc[r] * zt[r];
-        s = warp_sum(s);
-        if (lane == 0) dots[c - cs] = s;
+  double* At = sm;               // GS_R x 33: earlier vectors tile
+  double* Bt = At + GS_R * 33;   // GS_R x 33: panel tile
+  double* G = Bt + GS_R * 33;    // 32 x 33: G[c][p]
+  double* red = G + GS_P * 33;   // 64
+  for (int q = cs; q < ce; q += GS_P) {
+    const int np = min(GS_P, ce - q);
+    for (int rep = 0; rep < 2 && q > cs; ++rep) {
+      for (int c0 = cs; c0 < q; c0 += 32) {
+        const int nc = min(32, q - c0);
+        // G = Z[:, c0:c0+nc]^T Z[:, q:q+np]; thread owns p = lane, c = 4*warp + i
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int r0 = 0; r0 < n; r0 += GS_R) {
+          for (int e = tid; e < GS_R * 32; e += nt) {
+            const int rr = e % GS_R, cc = e / GS_R, r = r0 + rr;
+            At[rr * 33 + cc] = (r < n && cc < nc) ? Z[r + (long long)(c0 + cc) * ldz] : 0.0;
+            Bt[rr * 33 + cc] = (r < n && cc < np) ? Z[r + (long long)(q + cc) * ldz] : 0.0;
+          }
+          __syncthreads();
+#pragma unroll 8
+          for (int rr = 0; rr < GS_R; ++rr) {
+            const double bv = Bt[rr * 33 + lane];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) acc[i] += At[rr * 33 + 4 * warp + i] * bv;
+          }
+          __syncthreads();
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) G[(4 * warp + i) * 33 + lane] = acc[i];
+        __syncthreads();
+        // Z[:, q+p] -= Z[:, c0:c0+nc] G[:, p]; thread per row
+        for (int r = tid; r < n; r += nt) {
+          double zp[GS_P];
+#pragma unroll
+          for (int p = 0; p < GS_P; ++p) zp[p] = p < np ? Z[r + (long long)(q + p) * ldz] : 0.0;
+          for (int c = 0; c < nc; ++c) {
+            const double z = Z[r + (long long)(c0 + c) * ldz];
+#pragma unroll
+            for (int p = 0; p < GS_P; ++p) zp[p] -= z * G[c * 33 + p];
+          }
+#pragma unroll
+          for (int p = 0; p < GS_P; ++p)
+            if (p < np) Z[r + (long long)(q + p) * ldz] = zp[p];
+        }
+        __syncthreads();
       }
-      __syncthreads();
-      for (int r = tid; r < n; r += nt) {
-        double a = zt[r];
-        for (int c = cs; c < t; ++c) a -= dots[c - cs] * J.Z[r + (long long)c * J.ldz];
-        zt[r] = a;
+    }
+    // inside the panel: vector by vector
+    for (int t = q; t < q + np; ++t) {
+      double* zt = Z + (long long)t * ldz;
+      for (int rep = 0; rep < 2 && t > q; ++rep) {
+        for (int c = q + warp; c < t; c += nwarps) {
+          const double* zc = Z + (long long)c * ldz;
+          double s = 0.0;
+          for (int r = lane; r < n; r += 32) s += zc[r] * zt[r];
+          s = warp_sum(s);
+          if (lane == 0) G[c - q] = s;
+        }
+        __syncthreads();
+        for (int r = tid; r < n; r += nt) {
+          double a = zt[r];
+          for (int c = q; c < t; ++c) a -= G[c - q] * Z[r + (long long)c * ldz];
+          zt[r] = a;
+        }
+        __syncthreads();
       }
+      double part = 0.0;
+      for (int r = tid; r < n; r += nt) part += zt[r] * zt[r];
+      const double nrm2 = block_sum(part, red);
+      const double sc = nrm2 > 0.0 ? 1.0 / sqrt(nrm2) : 0.0;
+      for (int r = tid; r < n; r += nt) zt[r] *= sc;
       __syncthreads();
     }
-    double part = 0.0;
-    for (int r = tid; r < n; r += nt) part += zt[r] * zt[r];
-    const double nrm2 = block_sum(part, red);
-    const double sc = nrm2 > 0.0 ? 1.0 / sqrt(nrm2) : 0.0;
-    for (int r = tid; r < n; r += nt) zt[r] *= sc;
-    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(256) k_band_mgs(const EigDev* __restrict__ jobs) {
+  const EigDev J = jobs[blockIdx.x];
+  const int kk = J.kk;
+  __shared__ double sm[GS_SMEM_DOUBLES];
+  for (int cs = 0; cs < kk;) {
+    int ce = cs + 1;
+    while (ce < kk && J.cstarts[ce] == cs) ++ce;
+    if (ce - cs > 1) cluster_gs(J.Z, J.ldz, J.n, cs, ce, sm);
+    cs = ce;
   }
 }
 
@@ -1326,10 +1509,14 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
     d.cstarts = ctx.arena.alloc_n<int>(d.kk);
     d.vals_only = 1;
     HSVD_CUDA(cudaMemsetAsync(d.band, 0, (size_t)LDBB * n * sizeof(double), ctx.stream));
-    lu_slot_max = std::max(lu_slot_max, (size_t)n * (2 * B2 + 1 + B2 + 2));
+    lu_slot_max = std::max(lu_slot_max, (size_t)n * (2 * B2 + 1 + B2 + 3));
   }
   // band LU workspaces (INV_WARPS slots per matrix; slot size of the largest n)
-  double* lu = ctx.arena.alloc_n<double>(lu_slot_max * INV_WARPS * count);
+  // shifts spread over cpm CTAs per matrix (3 CTAs fit an SM), workspace
+  // capped at 8 GB
+  int cpm = std::max(1, std::min(ceil_div(3 * ctx.num_sms, count), ceil_div(kkmax, INV_WARPS)));
+  while (cpm > 1 && lu_slot_max * sizeof(double) * INV_WARPS * cpm * count > (size_t(8) << 30)) --cpm;
+  double* lu = ctx.arena.alloc_n<double>(lu_slot_max * INV_WARPS * cpm * count);
   for (int g = 0; g < count; ++g) {  // indexed by blockIdx.x in the kernel
     dev[g].lu = lu;
     dev[g].lu_slot = (long long)lu_slot_max;
@@ -1389,12 +1576,16 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
   }
   // eigenvectors of the band matrix
   {
-    const size_t smem = ((size_t)INV_WARPS * (B2 + 1) * (2 * B2 + 1) + kkmax + 64) * sizeof(double);
+    const size_t smem =
+        ((size_t)INV_WARPS * ((B2 + 1) * (2 * B2 + 1) + INV_RING) + 64) * sizeof(double);
     HSVD_CUDA(cudaFuncSetAttribute(k_band_invit, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));
     ctx.launch_begin();
-    k_band_invit<<<count, INV_WARPS * 32, smem, ctx.stream>>>(dd);
+    k_band_invit<<<dim3(cpm, count), INV_WARPS * 32, smem, ctx.stream>>>(dd);
     ctx.check_launch("k_band_invit");
+    ctx.launch_begin();
+    k_band_mgs<<<count, 256, 0, ctx.stream>>>(dd);
+    ctx.check_launch("k_band_mgs");
   }
   // back through the stage-1 reflectors
   back_transform(ctx, jobs, dev, dd, nmax, B2);
