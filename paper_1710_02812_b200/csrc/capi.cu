@@ -526,7 +526,13 @@ int hsvd_cu_rank_k_svd_sharded(hsvd_cu_ctx* ctx, const void* x, int dtype, int64
     begin(ctx);
     XView xv{x, dtype_of(dtype), ldx > 0 ? ldx : n, m_local, n};
     if (m_local > 0) xv = stage_x(ctx->c, x, dtype, m_local, n, ldx, where);
-    DFac f = rank_k_svd_sharded(ctx->c, *ctx->comm, xv, m_total, row0, to_cfg(cfg));
+    DFac f;
+    try {
+      f = rank_k_svd_sharded(ctx->c, *ctx->comm, xv, m_total, row0, to_cfg(cfg));
+    } catch (...) {
+      ctx->comm->abort();  // release the peers blocked on this rank
+      throw;
+    }
     *out = make_result(ctx, f, true, true);
     return HSVD_CU_OK;
   });

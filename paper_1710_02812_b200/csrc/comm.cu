@@ -24,6 +24,7 @@ struct NcclApi {
   ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
   ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
@@ -50,6 +51,7 @@ NcclApi& nccl() {
     LOAD(GetUniqueId);
     LOAD(CommInitRank);
     LOAD(CommDestroy);
+    LOAD(CommAbort);
     LOAD(Send);
     LOAD(Recv);
     LOAD(Broadcast);
@@ -79,6 +81,12 @@ class NcclComm : public Comm {
   }
   ~NcclComm() override {
     if (comm_) nccl().CommDestroy(comm_);
+  }
+  void abort() override {
+    if (comm_ && nccl().CommAbort) {
+      nccl().CommAbort(comm_);
+      comm_ = nullptr;
+    }
   }
   int rank() const override { return rank_; }
   int size() const override { return world_; }
@@ -139,17 +147,30 @@ struct ThreadGroup {
   std::vector<std::vector<double>> hostbuf;
   int bar_count = 0;
   long long bar_gen = 0;
+  bool aborted = false;  // a rank failed: every wait returns with an error
 
+  void check_abort() const {
+    if (aborted) throw Error(kNccl, "thread group: a peer rank failed");
+  }
   void barrier() {
     std::unique_lock<std::mutex> lk(mu);
+    check_abort();
     const long long gen = bar_gen;
     if (++bar_count == world) {
       bar_count = 0;
       ++bar_gen;
       cv.notify_all();
     } else {
-      cv.wait(lk, [&] { return bar_gen != gen; });
+      cv.wait(lk, [&] { return bar_gen != gen || aborted; });
+      check_abort();
     }
+  }
+  void abort() {
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      aborted = true;
+    }
+    cv.notify_all();
   }
 };
 
@@ -177,14 +198,16 @@ class ThreadComm : public Comm {
     HSVD_CUDA(cudaStreamSynchronize(c.stream));
     std::unique_lock<std::mutex> lk(g_->mu);
     auto& s = g_->slots[rank_ * g_->world + peer];
-    g_->cv.wait(lk, [&] { return !s.posted; });
+    g_->cv.wait(lk, [&] { return !s.posted || g_->aborted; });
+    g_->check_abort();
     s.ptr = buf;
     s.bytes = bytes;
     s.posted = true;
     s.consumed = false;
     g_->cv.notify_all();
-    g_->cv.wait(lk, [&] { return s.consumed; });
+    g_->cv.wait(lk, [&] { return s.consumed || g_->aborted; });
     s.posted = false;
+    g_->check_abort();
     g_->cv.notify_all();
     TRACE("[r%d] send -> %d done\n", rank_, peer);
   }
@@ -195,7 +218,8 @@ class ThreadComm : public Comm {
     {
       std::unique_lock<std::mutex> lk(g_->mu);
       auto& s = g_->slots[peer * g_->world + rank_];
-      g_->cv.wait(lk, [&] { return s.posted && !s.consumed; });
+      g_->cv.wait(lk, [&] { return (s.posted && !s.consumed) || g_->aborted; });
+      g_->check_abort();
       if (s.bytes != bytes) throw Error(kNccl, "thread comm: size mismatch");
       src = s.ptr;
     }
@@ -246,6 +270,7 @@ class ThreadComm : public Comm {
     HSVD_CUDA(cudaStreamSynchronize(c.stream));
     g_->barrier();
   }
+  void abort() override { g_->abort(); }
 
  private:
   std::shared_ptr<ThreadGroup> g_;

@@ -24,6 +24,9 @@ class Comm {
   // Brackets the point-to-point calls of one tree level (ncclGroupStart/End).
   virtual void group_start() {}
   virtual void group_end() {}
+  // Called by a rank that failed mid-collective: peers blocked on it return
+  // an error instead of waiting forever (ncclCommAbort / group abort).
+  virtual void abort() {}
 };
 
 // NCCL over NVLink/NVSwitch (libnccl.so.2 loaded at runtime).

@@ -9,7 +9,10 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
+#include <set>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "common.cuh"
@@ -134,6 +137,32 @@ class Staging {
   void* dev_ = nullptr;
   size_t size_ = 0, off_ = 0;
 };
+
+// Opt a kernel in to the device's full dynamic shared memory, once per
+// (device, kernel).  The attribute is process-global state shared by every
+// context; setting it to each launch's own size would race between host
+// threads driving different contexts (a smaller size set by one thread makes
+// another thread's larger launch fail).
+inline void smem_optin_impl(const void* func, size_t bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<int, const void*>> done;
+  int dev = 0;
+  HSVD_CUDA(cudaGetDevice(&dev));
+  int optin = 0;
+  HSVD_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  cudaFuncAttributes fa;
+  HSVD_CUDA(cudaFuncGetAttributes(&fa, func));
+  const int dyn_max = optin - static_cast<int>(fa.sharedSizeBytes);
+  if (bytes > (size_t)dyn_max)
+    throw Error(kInvalid, "kernel needs more shared memory than a CTA may use");
+  std::lock_guard<std::mutex> lk(mu);
+  if (!done.insert({dev, func}).second) return;
+  HSVD_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_max));
+}
+template <typename K>
+void smem_optin(K* kernel, size_t bytes) {
+  smem_optin_impl(reinterpret_cast<const void*>(kernel), bytes);
+}
 
 struct Ctx {
   int device = 0;

@@ -379,7 +379,7 @@ void finalize(Ctx& ctx, const std::vector<FinJob>& jobs) {
   k_colnorm_part<<<dim3(chmax, pmax, nj), 256, 0, ctx.stream>>>(dd);
   ctx.check_launch("k_colnorm_part");
   const size_t smem = 2 * (size_t)pmax * sizeof(double) + (size_t)pmax * sizeof(int) + 64;
-  HSVD_CUDA(cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  smem_optin(k_finalize, smem);
   ctx.launch_begin();
   k_finalize<<<nj, FIN_THREADS, smem, ctx.stream>>>(dd);
   ctx.check_launch("k_finalize");
@@ -388,7 +388,7 @@ void finalize(Ctx& ctx, const std::vector<FinJob>& jobs) {
   k_scale_gather<<<dim3(gx, pmax, nj), 256, 0, ctx.stream>>>(dd);
   ctx.check_launch("k_scale_gather");
   const size_t smem2 = ((size_t)pmax + 32) * sizeof(double) + (size_t)pmax * sizeof(int) + 64;
-  HSVD_CUDA(cudaFuncSetAttribute(k_complete, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+  smem_optin(k_complete, smem2);
   ctx.launch_begin();
   k_complete<<<nj, FIN_THREADS, smem2, ctx.stream>>>(dd);
   ctx.check_launch("k_complete");

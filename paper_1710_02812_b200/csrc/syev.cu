@@ -299,6 +299,9 @@ __global__ void __launch_bounds__(LAT, 1) k_latrd(const EigDev* __restrict__ job
   double* recv = red + 32;         // [2][CS][n] partial mat-vecs (double-buffered)
   __shared__ double s_alpha, s_diag;
   cg::cluster_group cluster = cg::this_cluster();
+  // every CTA of the cluster must be running before its shared memory is
+  // written by a peer (the early return above is uniform over the cluster)
+  if (CS > 1) cluster.sync();
 
   for (int t = 0; t < nbp; ++t) {
     const int j = j0 + t;
@@ -854,6 +857,104 @@ constexpr unsigned kSweepDone = 0x7fffffffu;
 constexpr int CHASE_WARPS = 8;
 static_assert(B2 == 32, "k_chase maps one band row per lane");
 
+// One bulge-chasing step of a warp: reflector from column c (rows r0..r0+L),
+// applied to the left block (columns c+1..c+nl), two-sided to the L x L
+// block R at r0 and from the right to the na rows below R.  Every element
+// is addressed from a per-lane base pointer plus a compile-time offset
+// (band column stride LDBB, diagonal stride LDBB-1); FULL (L == B2 and
+// nl == B2-1) drops the per-column bounds.  Returns false when the column
+// is already reduced (the sweep ends).
+template <bool FULL>
+__device__ __forceinline__ bool chase_step(double* bb, int c, int r0, int L, int nl, int na,
+                                           int lane, double* vs, double* ws) {
+  constexpr long long LD = LDBB;
+  const bool lx = lane < L;
+  double* px = bb + (r0 + lane - c) + (long long)c * LD;
+  double* pyl = bb + (r0 + lane - c - 1) + (long long)(c + 1) * LD;
+  double* pa1 = bb + lane + (long long)r0 * LD;                 // (r0+lane, r0+j), j <= lane
+  double* pa2 = bb + (long long)(r0 + lane) * LD - lane;        // (r0+j, r0+lane), j > lane
+  double* pya = bb + (L + lane) + (long long)r0 * LD;           // (r0+L+lane, r0+j)
+  const bool ly = lane < na;
+  // all loads of the step issued together (one memory round trip)
+  const double x = lx ? *px : 0.0;
+  double yl[B2 - 1], ar[B2], ya[B2];
+#pragma unroll
+  for (int l = 0; l < B2 - 1; ++l) yl[l] = (lx && (FULL || l < nl)) ? pyl[l * (LD - 1)] : 0.0;
+#pragma unroll
+  for (int j = 0; j < B2; ++j) {
+    const double* pa = lane >= j ? pa1 + j * (LD - 1) : pa2 + j;
+    ar[j] = (lx && (FULL || j < L)) ? *pa : 0.0;
+  }
+#pragma unroll
+  for (int j = 0; j < B2; ++j) ya[j] = (ly && (FULL || j < L)) ? pya[j * (LD - 1)] : 0.0;
+  const double xn2 = warp_sum(lane >= 1 ? x * x : 0.0);
+  const double alpha = __shfl_sync(0xffffffffu, x, 0);
+  if (xn2 == 0.0) return false;
+  const double nrm = sqrt(alpha * alpha + xn2);
+  const double beta = alpha >= 0.0 ? -nrm : nrm;
+  const double tau = (beta - alpha) / beta;
+  const double scal = 1.0 / (alpha - beta);
+  const double v = lane == 0 ? 1.0 : (lx ? x * scal : 0.0);
+  vs[lane] = v;
+  if (lx) *px = lane == 0 ? beta : 0.0;
+  // left block: d_l = sum_i v_i y_il by a transposing butterfly (lane l
+  // ends with d_l), then y_il -= tau v_i d_l
+  {
+    double t[B2];
+#pragma unroll
+    for (int l = 0; l < B2 - 1; ++l) t[l] = v * yl[l];
+    t[B2 - 1] = 0.0;
+#pragma unroll
+    for (int ofs = 16; ofs >= 1; ofs >>= 1) {
+      const bool up = (lane & ofs) != 0;
+#pragma unroll
+      for (int j = 0; j < ofs; ++j) {
+        const double send = up ? t[j] : t[j + ofs];
+        const double got = __shfl_xor_sync(0xffffffffu, send, ofs);
+        t[j] = (up ? t[j + ofs] : t[j]) + got;
+      }
+    }
+    const double dl = tau * t[0];
+#pragma unroll
+    for (int l = 0; l < B2 - 1; ++l) {
+      const double d = __shfl_sync(0xffffffffu, dl, l);
+      if (lx && (FULL || l < nl)) pyl[l * (LD - 1)] = yl[l] - d * v;
+    }
+  }
+  __syncwarp();
+  // R x R: two-sided (symmetric, lower storage); p = tau R v
+  double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
+#pragma unroll
+  for (int j = 0; j < B2; j += 4) {
+    p0 += ar[j] * vs[j];
+    p1 += ar[j + 1] * vs[j + 1];
+    p2 += ar[j + 2] * vs[j + 2];
+    p3 += ar[j + 3] * vs[j + 3];
+  }
+  const double pp = tau * ((p0 + p1) + (p2 + p3));
+  const double al = -0.5 * tau * warp_sum(pp * v);
+  const double w = pp + al * v;
+  ws[lane] = w;
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < B2; ++j)
+    if (lx && lane >= j && (FULL || j < L)) pa1[j * (LD - 1)] = ar[j] - (v * ws[j] + w * vs[j]);
+  // rows after R: right application (creates the next bulge)
+  double y0 = 0.0, y1 = 0.0, y2 = 0.0, y3 = 0.0;
+#pragma unroll
+  for (int j = 0; j < B2; j += 4) {
+    y0 += ya[j] * vs[j];
+    y1 += ya[j + 1] * vs[j + 1];
+    y2 += ya[j + 2] * vs[j + 2];
+    y3 += ya[j + 3] * vs[j + 3];
+  }
+  const double y = tau * ((y0 + y1) + (y2 + y3));
+#pragma unroll
+  for (int j = 0; j < B2; ++j)
+    if (ly && (FULL || j < L)) pya[j * (LD - 1)] = ya[j] - y * vs[j];
+  return true;
+}
+
 __global__ void __launch_bounds__(CHASE_WARPS * 32, 1) k_chase(const EigDev* __restrict__ jobs) {
   const EigDev J = jobs[blockIdx.x];
   const int n = J.n;
@@ -876,86 +977,21 @@ __global__ void __launch_bounds__(CHASE_WARPS * 32, 1) k_chase(const EigDev* __r
       if (s > 0) {  // wait for sweep s-1 to be 3 steps ahead (or done)
         const unsigned need = (unsigned)(k + 3);
         while (true) {
-          const unsigned long long v = vprog[pslot];
-          const int vs = (int)(v >> 32) - 1;
-          const unsigned st = (unsigned)(v & 0xffffffffu);
+          const unsigned long long pv = vprog[pslot];
+          const int vs = (int)(pv >> 32) - 1;
+          const unsigned st = (unsigned)(pv & 0xffffffffu);
           if (vs > s - 1 || (vs == s - 1 && (st >= need))) break;
-          __nanosleep(64);
+          __nanosleep(32);
         }
         __threadfence_block();
       }
       const int c = k == 0 ? s : s + 1 + (k - 1) * B2;
-      const int nl = r0 - c - 1;                 // left-block columns (0 or B2-1)
-      const int na = min(n, r0 + 2 * B2) - r1;   // rows after R
-      // all loads of the step issued together (one memory round trip)
-      const double x = lane < L ? band_at(bb, r0 + lane, c) : 0.0;
-      double yl[B2 - 1], ar[B2], ya[B2];
-#pragma unroll
-      for (int l = 0; l < B2 - 1; ++l)
-        yl[l] = (l < nl && lane < L) ? band_at(bb, r0 + lane, c + 1 + l) : 0.0;
-#pragma unroll
-      for (int j = 0; j < B2; ++j)
-        ar[j] = (j < L && lane < L)
-                    ? (lane >= j ? band_at(bb, r0 + lane, r0 + j) : band_at(bb, r0 + j, r0 + lane))
-                    : 0.0;
-#pragma unroll
-      for (int j = 0; j < B2; ++j) ya[j] = (j < L && lane < na) ? band_at(bb, r1 + lane, r0 + j) : 0.0;
-      const double xn2 = warp_sum(lane >= 1 ? x * x : 0.0);
-      const double alpha = __shfl_sync(0xffffffffu, x, 0);
-      if (xn2 == 0.0) break;  // no bulge left in this sweep
-      const double nrm = sqrt(alpha * alpha + xn2);
-      const double beta = alpha >= 0.0 ? -nrm : nrm;
-      const double tau = (beta - alpha) / beta;
-      const double scal = 1.0 / (alpha - beta);
-      const double v = lane == 0 ? 1.0 : (lane < L ? x * scal : 0.0);
-      vsh[warp][lane] = v;
-      if (lane < L) band_at(bb, r0 + lane, c) = lane == 0 ? beta : 0.0;
-      // left block: dots d_l = sum_i v_i y_il by a transposing butterfly
-      // (lane l ends with d_l), then y_il -= tau v_i d_l
-      if (nl > 0) {
-        double t[B2];
-#pragma unroll
-        for (int l = 0; l < B2 - 1; ++l) t[l] = v * yl[l];
-        t[B2 - 1] = 0.0;
-#pragma unroll
-        for (int ofs = 16; ofs >= 1; ofs >>= 1) {
-          const bool up = (lane & ofs) != 0;
-#pragma unroll
-          for (int j = 0; j < ofs; ++j) {
-            const double send = up ? t[j] : t[j + ofs];
-            const double got = __shfl_xor_sync(0xffffffffu, send, ofs);
-            t[j] = (up ? t[j + ofs] : t[j]) + got;
-          }
-        }
-        const double dl = tau * t[0];
-#pragma unroll
-        for (int l = 0; l < B2 - 1; ++l) {
-          const double d = __shfl_sync(0xffffffffu, dl, l);
-          if (l < nl && lane < L) band_at(bb, r0 + lane, c + 1 + l) = yl[l] - d * v;
-        }
-      }
-      __syncwarp();
-      // R x R: two-sided (symmetric, lower storage)
-      double p = 0.0;
-#pragma unroll
-      for (int j = 0; j < B2; ++j) p += ar[j] * vsh[warp][j];
-      p *= tau;
-      const double al = -0.5 * tau * warp_sum(p * v);
-      const double w = p + al * v;
-      wsh[warp][lane] = w;
-      __syncwarp();
-#pragma unroll
-      for (int j = 0; j < B2; ++j)
-        if (j < L && lane < L && lane >= j)
-          band_at(bb, r0 + lane, r0 + j) = ar[j] - (v * wsh[warp][j] + w * vsh[warp][j]);
-      // rows after R x R: right application (creates the next bulge)
-      double y = 0.0;
-#pragma unroll
-      for (int j = 0; j < B2; ++j) y += ya[j] * vsh[warp][j];
-      y *= tau;
-#pragma unroll
-      for (int j = 0; j < B2; ++j)
-        if (j < L && lane < na) band_at(bb, r1 + lane, r0 + j) = ya[j] - y * vsh[warp][j];
+      const int nl = r0 - c - 1;                // left-block columns (0 or B2-1)
+      const int na = min(n, r0 + 2 * B2) - r1;  // rows after R
+      const bool ok = (L == B2 && nl == B2 - 1)
+                          ? chase_step<true>(bb, c, r0, L, nl, na, lane, vsh[warp], wsh[warp])
+                          : chase_step<false>(bb, c, r0, L, nl, na, lane, vsh[warp], wsh[warp]);
+      if (!ok) break;  // no bulge left in this sweep
       __syncwarp();
       __threadfence_block();
       if (lane == 0) vprog[warp] = prog_encode(s, (unsigned)(k + 1));
@@ -1377,12 +1413,7 @@ constexpr size_t kLatrdSmemMax = 200 * 1024;
 
 template <int R>
 void launch_latrd_t(Ctx& ctx, int count, int cs, size_t smem, const EigDev* dd, int j0) {
-  static bool attr = false;
-  if (!attr) {
-    HSVD_CUDA(cudaFuncSetAttribute(k_latrd<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)kLatrdSmemMax));
-    attr = true;
-  }
+  smem_optin(k_latrd<R>, kLatrdSmemMax);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(count * cs);
   cfg.blockDim = dim3(LAT);
@@ -1446,7 +1477,7 @@ void back_transform(Ctx& ctx, const std::vector<EigJob>& jobs, const std::vector
   }
   gemm_grouped(ctx, DType::F64, DType::F64, true, false, true, ds);
   const size_t tsm = ((size_t)NBT * (NBT + 1) + NBT) * sizeof(double);
-  HSVD_CUDA(cudaFuncSetAttribute(k_build_t, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
+  smem_optin(k_build_t, tsm);
   ctx.launch_begin();
   k_build_t<<<dim3(nblk_max, count), NBT, tsm, ctx.stream>>>(dd, off);
   ctx.check_launch("k_build_t");
@@ -1569,7 +1600,7 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
   {
     const size_t smem = (3 * (size_t)nmax + 3 * (size_t)kkmax + 32) * sizeof(double) +
                         (size_t)kkmax * sizeof(int) + 64;
-    HSVD_CUDA(cudaFuncSetAttribute(k_steig, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    smem_optin(k_steig, smem);
     ctx.launch_begin();
     k_steig<<<count, EIG_THREADS, smem, ctx.stream>>>(dd);
     ctx.check_launch("k_steig");
@@ -1578,8 +1609,7 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
   {
     const size_t smem =
         ((size_t)INV_WARPS * ((B2 + 1) * (2 * B2 + 1) + INV_RING) + 64) * sizeof(double);
-    HSVD_CUDA(cudaFuncSetAttribute(k_band_invit, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem));
+    smem_optin(k_band_invit, smem);
     ctx.launch_begin();
     k_band_invit<<<dim3(cpm, count), INV_WARPS * 32, smem, ctx.stream>>>(dd);
     ctx.check_launch("k_band_invit");
@@ -1645,11 +1675,9 @@ void eig_topk(Ctx& ctx, const std::vector<EigJob>& jobs_in) {
     dd = upload_jobs(ctx, dev);
     const int R = ceil_div(nmax, LAT);
     // cluster size: spread each matrix's mat-vec over several SMs while the
-    // batch alone would leave SMs idle
-    // (capped at 4: 8-CTA clusters from several concurrent contexts on one
-    // GPU were observed to stall intermittently)
+    // batch alone would leave SMs idle (portable cluster size <= 8)
     int cs = 1;
-    while (cs < 4 && (long long)count * cs * 2 <= ctx.num_sms &&
+    while (cs < 8 && (long long)count * cs * 2 <= ctx.num_sms &&
            ((size_t)nmax * (1 + 4 * cs) + 4 * NB + 64) * sizeof(double) <= kLatrdSmemMax)
       cs *= 2;
     if (const char* env = std::getenv("HSVD_LATRD_CS")) cs = std::max(1, std::atoi(env));
@@ -1671,8 +1699,7 @@ void eig_topk(Ctx& ctx, const std::vector<EigJob>& jobs_in) {
     }
   } else {
     const size_t smem = (4 * (size_t)nmax + TRD_THREADS + 64) * sizeof(double);
-    HSVD_CUDA(cudaFuncSetAttribute(k_sytrd, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem));
+    smem_optin(k_sytrd, smem);
     ctx.launch_begin();
     k_sytrd<<<count, TRD_THREADS, smem, ctx.stream>>>(dd);
     ctx.check_launch("k_sytrd");
@@ -1681,8 +1708,7 @@ void eig_topk(Ctx& ctx, const std::vector<EigJob>& jobs_in) {
   {
     const size_t smem = (3 * (size_t)nmax + 3 * (size_t)kkmax + 32) * sizeof(double) +
                         (size_t)kkmax * sizeof(int) + 64;
-    HSVD_CUDA(cudaFuncSetAttribute(k_steig, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem));
+    smem_optin(k_steig, smem);
     ctx.launch_begin();
     k_steig<<<count, EIG_THREADS, smem, ctx.stream>>>(dd);
     ctx.check_launch("k_steig");

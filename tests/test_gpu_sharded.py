@@ -73,3 +73,35 @@ def test_nccl_world1_path():
     f = H.rank_k_svd_sharded(x, m, 0, cfg, ctx)
     assert np.abs(f.sigma - single.sigma).max() <= 1e-11 * single.sigma[0]
     assert O.largest_principal_angle(single.u, f.u) < 1e-9
+
+
+def test_failing_rank_releases_peers():
+    """A rank that fails inside the sharded pipeline aborts the group: its
+    peers return an error instead of blocking on it forever."""
+    import paper_1710_02812_b200 as H
+    rng = np.random.default_rng(5)
+    m, n = 512, 256
+    x = rng.standard_normal((m, n)).astype(np.float32)
+    cfg = H.MatConfig(gamma=1e-12, row_block_rows=128, col_block_cols=128, max_rank=16)
+    grp = H.ThreadGroup(2)
+    errs = [None, None]
+
+    def body(rank):
+        try:
+            ctx = H.Context(0)
+            ctx.join_group(grp, rank)
+            r0, ml = H.shard_rows(m, cfg.row_block_rows, rank, 2)
+            if rank == 1:
+                ml -= 1  # rows no longer match the shard plan -> this rank fails
+            H.rank_k_svd_sharded(x[r0:r0 + ml], m, r0, cfg, ctx)
+        except Exception as e:
+            errs[rank] = str(e)
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=120)
+    assert not any(t.is_alive() for t in th), "a rank is still blocked"
+    assert errs[1] is not None and "must hold rows" in errs[1]
+    assert errs[0] is not None and "peer rank failed" in errs[0]
