@@ -184,11 +184,58 @@ def fp64_peak_tflops(torch, dev):
     return 2.0 * n ** 3 / (best / 1000.0) / 1e12
 
 
-def tridiag_bytes(n):
-    """k_sytrd algorithmic bytes per matrix: the fused update+symv reads and
-    writes the trailing (n-j-2)^2 block once per column, plus one read pass."""
-    s = sum((n - j - 2) ** 2 for j in range(0, n - 2))
-    return 8.0 * ((n - 1) ** 2 + 2.0 * s)
+def kernel_families(prof):
+    """{kernel name: (launches, ms, flops)} summed over phases."""
+    fam = {}
+    for key, (cnt, ms, fl) in prof.items():
+        k = key.rsplit(":", 1)[-1]
+        c0, m0, f0 = fam.get(k, (0, 0.0, 0.0))
+        fam[k] = (c0 + cnt, m0 + ms, f0 + fl)
+    return fam
+
+
+def load_traffic(workload):
+    """Measured DRAM bytes per launch of a kernel family (ncu, committed
+    under profiles/), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f).get(workload, {})
+    except Exception:
+        return {}
+
+
+def roofline(prof, steps, w, hbm_peak, fp64_peak):
+    """Roofline of the kernel family with the largest share of the step.
+    k_gemm (the grouped DMMA GEMM: Grams, projections, the two-stage band
+    reduction and both back-transforms) is tensor-bound: achieved = its
+    algorithmic flops (counted per launch by the library) / its time.
+    k_latrd is HBM-bound: algorithmic bytes = the trailing block streamed
+    once per column."""
+    fam = kernel_families(prof)
+    name = max(fam, key=lambda k: fam[k][1])
+    cnt, ms, fl = fam[name]
+    traffic = load_traffic(w.name).get(name)
+    if name == "k_gemm" and fl > 0:
+        peak = fp64_peak()
+        achieved = fl / (ms / 1000.0) / 1e12
+        return {"kernel": "k_gemm (all launches)", "bound": "tensor", "achieved": achieved,
+                "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "traffic": traffic, "traffic_unit": "bytes per launch",
+                "peak_source": "fp64 cuBLAS DGEMM 8192^3 measured in this run",
+                "algorithmic_flops_per_launch": fl / cnt, "avg_launch_ms": ms / cnt,
+                "launches_per_step": cnt / steps, "share": ms / sum(v[1] for v in fam.values())}
+    if name == "k_latrd":
+        nleaves, q = w.P * w.Q, min(w.c, w.d)
+        byts_step = nleaves * 8.0 * sum((q - j - 1) ** 2 for j in range(q - 1))
+        achieved = byts_step / ((ms / steps) / 1000.0) / 1e9
+        return {"kernel": "k_latrd", "bound": "hbm", "achieved": achieved, "peak": hbm_peak,
+                "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)",
+                "algorithmic_bytes_per_launch": byts_step / (cnt / steps),
+                "avg_launch_ms": ms / cnt}
+    return {"kernel": name, "bound": None, "achieved": None, "peak": None, "unit": None,
+            "frac": None, "traffic": traffic,
+            "note": "latency-bound kernel (no HBM or tensor roofline applies)"}
 
 
 def run_ours(args, w):
@@ -295,44 +342,7 @@ def run_ours(args, w):
     except Exception:
         pass
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    top_name, top_launches, top_ms, top_share = shares[0]
-    roof = None
-    nleaves = w.P * w.Q
-    q = min(w.c, w.d)
-    if top_name.endswith("k_latrd"):
-        # Blocked tridiagonalisation: every column's mat-vec streams the
-        # (n-j-1)^2 fp64 trailing block once (the algorithm's bytes); one launch
-        # = one 32-column panel of all leaves, so bytes/launch / ms/launch =
-        # total bytes / total ms over the timed steps.
-        cnt, tot_ms = prof["leaf.eig:k_latrd"]
-        byts_step = nleaves * 8.0 * sum((q - j - 1) ** 2 for j in range(q - 1))
-        launches_step = cnt / args.steps
-        achieved = byts_step / ((tot_ms / args.steps) / 1000.0) / 1e9
-        # ncu --set full of panel 20 (profiles/r01_cfg2_full.md): dram bytes
-        # 58.0 GB vs 56.7 GB algorithmic -> x1.023 (no re-reads)
-        roof = {"kernel": "leaf.eig:k_latrd", "bound": "hbm", "achieved": achieved,
-                "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
-                "traffic": 1.023 * byts_step / launches_step,
-                "traffic_source": "ncu dram__bytes_read+write / algorithmic = 1.023 (r01)",
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)",
-                "algorithmic_bytes_per_launch": byts_step / launches_step,
-                "avg_launch_ms": tot_ms / cnt}
-    elif top_name.endswith("k_sytrd"):
-        leaf_ms = prof.get("leaf.eig:k_sytrd", (0, 0.0))[1] / args.steps
-        byts = nleaves * tridiag_bytes(q)
-        achieved = byts / (leaf_ms / 1000.0) / 1e9
-        roof = {"kernel": "leaf.eig:k_sytrd", "bound": "hbm", "achieved": achieved,
-                "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
-                "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)",
-                "algorithmic_bytes_per_launch": byts}
-    else:
-        fp64 = fp64_peak_tflops(torch, dev)
-        g_ms = prof.get("leaf.gram:k_gemm", (0, 0.0))[1] / args.steps
-        flops = nleaves * 2.0 * max(w.c, w.d) * q * q / 2.0  # syrk: lower half
-        achieved = flops / (g_ms / 1000.0) / 1e12 if g_ms > 0 else 0.0
-        roof = {"kernel": "leaf.gram:k_gemm", "bound": "tensor", "achieved": achieved,
-                "peak": fp64, "unit": "TFLOP/s", "frac": achieved / fp64, "traffic": None,
-                "peak_source": "fp64 cuBLAS DGEMM 8192^3 measured in this run"}
+    roof = roofline(prof, args.steps, w, hbm_peak, lambda: fp64_peak_tflops(torch, dev))
 
     cpu = None
     if not args.no_cpu_baseline and ws == 1:

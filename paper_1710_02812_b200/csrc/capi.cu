@@ -272,6 +272,7 @@ int64_t hsvd_cu_profile_report(hsvd_cu_ctx* ctx, char* buf, int64_t len) {
     HSVD_CUDA(cudaStreamSynchronize(c.stream));
     std::vector<std::string> order;
     std::vector<std::pair<long long, double>> agg;
+    std::vector<double> fl;
     for (auto& r : c.prof) {
       float ms = 0.f;
       HSVD_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
@@ -280,9 +281,11 @@ int64_t hsvd_cu_profile_report(hsvd_cu_ctx* ctx, char* buf, int64_t len) {
       if (i == order.size()) {
         order.push_back(r.name);
         agg.push_back({0, 0.0});
+        fl.push_back(0.0);
       }
       agg[i].first += 1;
       agg[i].second += ms;
+      fl[i] += r.flops;
     }
     if (buf && len > 0) {  // a sizing query (buf == NULL) keeps the records
       for (auto& r : c.prof) {
@@ -292,7 +295,8 @@ int64_t hsvd_cu_profile_report(hsvd_cu_ctx* ctx, char* buf, int64_t len) {
       c.prof.clear();
     }
     for (size_t i = 0; i < order.size(); ++i)
-      out += order[i] + "\t" + std::to_string(agg[i].first) + "\t" + std::to_string(agg[i].second) + "\n";
+      out += order[i] + "\t" + std::to_string(agg[i].first) + "\t" + std::to_string(agg[i].second) +
+             "\t" + std::to_string(fl[i]) + "\n";
     return HSVD_CU_OK;
   });
   if (rc != HSVD_CU_OK) return -1;

@@ -212,9 +212,12 @@ struct Ctx {
   struct ProfRec {
     std::string name;
     cudaEvent_t a, b;
+    double flops;  // algorithmic flops of the launch (GEMMs), else 0
   };
+  double pending_flops = 0.0;
   bool profiling = false;
   const char* phase = "";
+  const char* sub = nullptr;  // optional sub-phase inside a phase (profile key phase/sub)
   std::vector<ProfRec> prof;
   std::vector<cudaEvent_t> ev_free;
   cudaEvent_t pending = nullptr;
@@ -251,9 +254,11 @@ struct Ctx {
     if (profiling && pending) {
       cudaEvent_t b = get_event();
       HSVD_CUDA(cudaEventRecord(b, stream));
-      prof.push_back({std::string(phase) + ":" + what, pending, b});
+      prof.push_back({std::string(phase) + (sub ? std::string("/") + sub : std::string()) + ":" + what,
+                      pending, b, pending_flops});
       pending = nullptr;
     }
+    pending_flops = 0.0;
   }
 };
 
@@ -262,6 +267,13 @@ struct PhaseScope {
   const char* prev;
   PhaseScope(Ctx& ctx, const char* p) : c(ctx), prev(ctx.phase) { c.phase = p; }
   ~PhaseScope() { c.phase = prev; }
+};
+
+struct SubPhase {
+  Ctx& c;
+  const char* prev;
+  SubPhase(Ctx& ctx, const char* s) : c(ctx), prev(ctx.sub) { c.sub = s; }
+  ~SubPhase() { c.sub = prev; }
 };
 
 }  // namespace hsvdcu

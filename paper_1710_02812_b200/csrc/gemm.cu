@@ -231,6 +231,7 @@ void gemm_grouped(Ctx& ctx, DType ta, DType tb, bool trans_a, bool trans_b, bool
   live.reserve(descs.size());
   int maxM = 0, maxN = 0, maxK = 0;
   long long tiles = 0;
+  double flops = 0.0;  // algorithmic (SYRK: the lower triangle)
   for (const auto& d : descs) {
     if (d.M <= 0 || d.N <= 0) continue;
     if (d.K <= 0) {
@@ -244,6 +245,7 @@ void gemm_grouped(Ctx& ctx, DType ta, DType tb, bool trans_a, bool trans_b, bool
     long long t = (long long)ceil_div(d.M, BM) * ceil_div(d.N, BN);
     if (syrk) t = (t + ceil_div(d.M, BM)) / 2;
     tiles += t;
+    flops += syrk ? (double)d.M * (d.M + 1) * d.K : 2.0 * d.M * d.N * d.K;
   }
   if (live.empty()) return;
   const int count = static_cast<int>(live.size());
@@ -268,6 +270,7 @@ void gemm_grouped(Ctx& ctx, DType ta, DType tb, bool trans_a, bool trans_b, bool
     ws = ctx.arena.alloc_n<double>((size_t)slot * count * splits);
   }
   const int sy = syrk ? 1 : 0;
+  ctx.pending_flops = flops;
   if (ta == DType::F64 && tb == DType::F64)
     launch_typed<double, double>(ctx, trans_a, trans_b, grid, dd, sy, splits, ws, slot);
   else if (ta == DType::F32 && tb == DType::F64)

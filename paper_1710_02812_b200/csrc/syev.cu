@@ -1450,7 +1450,20 @@ void launch_latrd(Ctx& ctx, int R, int count, int cs, size_t smem, const EigDev*
   }
 }
 
-constexpr int kTwoStageMinN = 1 << 30;  // enabled by HSVD_TWO_STAGE_MIN_N until validated
+// Reduction choice.  The two-stage path moves the O(n^3) work onto DMMA
+// GEMMs but its band stages (panel QR, bulge chase, band inverse iteration)
+// run one CTA (or a few) per matrix, so it pays off for large n or for
+// batches that fill the GPU (measured on B200: single matrix, one-stage
+// wins at n = 1024 and 2048, two-stage at 4096; 64 matrices of n = 2048,
+// 2500 or 4096, two-stage wins).  HSVD_TWO_STAGE_MIN_N overrides with a
+// plain size threshold.
+constexpr int kTwoStageMinN = 1024;       // batched
+constexpr int kTwoStageMinBatch = 32;
+constexpr int kTwoStageAlwaysN = 3072;    // any batch size
+bool use_two_stage(int nmax, int count) {
+  if (const char* env = std::getenv("HSVD_TWO_STAGE_MIN_N")) return nmax >= std::atoi(env);
+  return nmax >= kTwoStageAlwaysN || (nmax >= kTwoStageMinN && count >= kTwoStageMinBatch);
+}
 
 // Z <- Q Z with Q = H_0 H_1 ... (reflector of column j: unit at row j + off,
 // stored in A column j), in compact-WY blocks of NBT reflectors.
@@ -1552,10 +1565,10 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
     dev[g].lu = lu;
     dev[g].lu_slot = (long long)lu_slot_max;
   }
-  const EigDev* dd =
-      upload_jobs(ctx, dev);
+  const EigDev* dd = upload_jobs(ctx, dev);
 
   // stage 1: dense -> band
+  SubPhase sp1(ctx, "band");
   std::vector<GemmDesc> g1, g2, g3, g4, g5, g6;
   for (int p = 0; p < npan; ++p) {
     const int j0 = p * B2, r0 = j0 + B2;
@@ -1580,20 +1593,28 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
       g6.push_back({e.VW + r0, e.WV + r0, A22, n, n, e.lda, m, m, 2 * B2, -1.0, 1.0});  // syr2k
     }
     if (g1.empty()) continue;
-    gemm_grouped(ctx, DType::F64, DType::F64, false, false, false, g1);
-    gemm_grouped(ctx, DType::F64, DType::F64, false, false, false, g2);
-    gemm_grouped(ctx, DType::F64, DType::F64, true, false, false, g3);
-    gemm_grouped(ctx, DType::F64, DType::F64, true, false, false, g4);
-    gemm_grouped(ctx, DType::F64, DType::F64, false, false, false, g5);
-    ctx.launch_begin();
-    k_copy_w<<<dim3(256, count), 256, 0, ctx.stream>>>(dd, j0);
-    ctx.check_launch("k_copy_w");
+    {
+      SubPhase sy(ctx, "band.y");
+      gemm_grouped(ctx, DType::F64, DType::F64, false, false, false, g1);
+    }
+    {
+      SubPhase sw(ctx, "band.w");
+      gemm_grouped(ctx, DType::F64, DType::F64, false, false, false, g2);
+      gemm_grouped(ctx, DType::F64, DType::F64, true, false, false, g3);
+      gemm_grouped(ctx, DType::F64, DType::F64, true, false, false, g4);
+      gemm_grouped(ctx, DType::F64, DType::F64, false, false, false, g5);
+      ctx.launch_begin();
+      k_copy_w<<<dim3(256, count), 256, 0, ctx.stream>>>(dd, j0);
+      ctx.check_launch("k_copy_w");
+    }
+    SubPhase s2k(ctx, "band.syr2k");
     gemm_grouped(ctx, DType::F64, DType::F64, false, true, true, g6);
   }
   for (int g = 0; g < count; ++g)
     HSVD_CUDA(cudaMemcpyAsync(dev[g].band0, dev[g].band, (size_t)LDBB * dev[g].n * sizeof(double),
                               cudaMemcpyDeviceToDevice, ctx.stream));
   // stage 2: band -> tridiagonal (values), eigenvalues by bisection
+  SubPhase sp2(ctx, "tri");
   ctx.launch_begin();
   k_chase<<<count, CHASE_WARPS * 32, 0, ctx.stream>>>(dd);
   ctx.check_launch("k_chase");
@@ -1618,6 +1639,7 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
     ctx.check_launch("k_band_mgs");
   }
   // back through the stage-1 reflectors
+  SubPhase sp3(ctx, "back");
   back_transform(ctx, jobs, dev, dd, nmax, B2);
 }
 
@@ -1654,12 +1676,9 @@ void eig_topk(Ctx& ctx, const std::vector<EigJob>& jobs_in) {
     nmax = std::max(nmax, j.n);
     kkmax = std::max(kkmax, j.kk);
   }
-  const EigDev* dd =
-      upload_jobs(ctx, dev);
+  const EigDev* dd = upload_jobs(ctx, dev);
 
-  int two_stage_min = kTwoStageMinN;
-  if (const char* env = std::getenv("HSVD_TWO_STAGE_MIN_N")) two_stage_min = std::atoi(env);
-  if (nmax >= two_stage_min) {
+  if (use_two_stage(nmax, count)) {
     two_stage(ctx, jobs, dev, nmax, kkmax);
     ctx.arena.release(mk);
     return;

@@ -328,7 +328,8 @@ class Context:
         _check(self.lib.hsvd_cu_profile(self.handle, 1 if enable else 0))
 
     def profile_report(self) -> dict:
-        """{'phase:kernel': (launches, total_ms)} since the last report."""
+        """{'phase[/sub]:kernel': (launches, total_ms, algorithmic_flops)} since
+        the last report (flops counted for the GEMM launches, else 0)."""
         need = self.lib.hsvd_cu_profile_report(self.handle, None, 0)
         if need < 0:
             _raise(ECUDA)
@@ -336,8 +337,8 @@ class Context:
         self.lib.hsvd_cu_profile_report(self.handle, buf, len(buf))
         out = {}
         for line in buf.value.decode().splitlines():
-            name, cnt, ms = line.split("\t")
-            out[name] = (int(cnt), float(ms))
+            name, cnt, ms, fl = line.split("\t")
+            out[name] = (int(cnt), float(ms), float(fl))
         return out
 
 

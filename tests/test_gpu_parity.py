@@ -79,8 +79,14 @@ def test_full_svd_blocked_eigensolver(shape, H):
     assert np.linalg.norm(rec - a) <= 1e-11 * np.linalg.norm(a)
 
 
+@pytest.mark.parametrize("eig", ["auto", "two_stage"])
 @pytest.mark.parametrize("name", sorted(CONFIG_CASES))
-def test_config_parity_with_oracle(name, H):
+def test_config_parity_with_oracle(name, eig, H, monkeypatch):
+    """Whole pipeline against the oracle; eig="two_stage" forces the
+    dense -> band -> tridiagonal eigensolver for every matrix of n >= 256
+    (the default picks it only for large batched leaves)."""
+    if eig == "two_stage":
+        monkeypatch.setenv("HSVD_TWO_STAGE_MIN_N", "256")
     m, n, r, spec, noise, dt, P, Q, k = CONFIG_CASES[name]
     x = _synthetic(m, n, r, spec, noise, dt, seed=171002812 + len(name))
     cfg = dict(gamma=1e-12, row_block_rows=m // P, col_block_cols=n // Q, max_rank=k)
