@@ -22,9 +22,15 @@ struct GemmDesc {
   double alpha, beta;
 };
 
+// flags for gemm_grouped
+enum : int {
+  kGemmLowerOnly = 1,  // with syrk: write the lower tile triangle only (no mirror)
+  kGemmSymA = 2,       // op(A) = A is symmetric and only its lower triangle is read
+};
+
 // syrk=true: op(A) op(B) is known symmetric (op(B) == op(A)^T); only the
-// lower tile triangle is computed and mirrored.
+// lower tile triangle is computed (and mirrored unless kGemmLowerOnly).
 void gemm_grouped(Ctx& ctx, DType ta, DType tb, bool trans_a, bool trans_b, bool syrk,
-                  const std::vector<GemmDesc>& descs);
+                  const std::vector<GemmDesc>& descs, int flags = 0);
 
 }  // namespace hsvdcu
