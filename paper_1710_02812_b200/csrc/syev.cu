@@ -725,35 +725,70 @@ __device__ __forceinline__ double& band_at(double* bb, int i, int j) {
 
 // Panel j0: copy the diagonal block to the band, Householder QR of the
 // panel below the band (R -> band, explicit V in place and in VW/WV), T.
-__global__ void __launch_bounds__(512) k_panel_qr(const EigDev* __restrict__ jobs, int j0) {
-  const EigDev J = jobs[blockIdx.x];
+__global__ void __launch_bounds__(512, 1) k_panel_qr(const EigDev* __restrict__ jobs, int j0,
+                                                     int CS) {
+  // One matrix per cluster of CS CTAs; CTA c keeps rows [c*mc, (c+1)*mc) of
+  // the m x B2 panel in shared memory (column-major, ld mc + 1) for the whole
+  // factorisation.  Per column: the norm and the B2-1 column dots are summed
+  // from per-CTA partials exchanged through distributed shared memory (every
+  // CTA writes its partials into every peer, one cluster barrier, then each
+  // sums them in rank order -- identical values in every CTA).
+  const EigDev J = jobs[blockIdx.x / CS];
+  const int crank = blockIdx.x % CS;
+  cg::cluster_group cluster = cg::this_cluster();
   const int n = J.n;
-  if (j0 >= n) return;
   const int tid = threadIdx.x, nt = blockDim.x;
   const int lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
   double* A = J.A;
   const long long lda = J.lda;
-  const int jb = min(B2, n - j0);
+  const int jb = max(0, min(B2, n - j0));
   const int r0 = j0 + B2;
-  const int m = n - r0;
-  __shared__ double beta_s[B2];
-  __shared__ double red[32];
-  __shared__ double S[B2][B2 + 1];
-  __shared__ double T[B2][B2 + 1];
-  __shared__ double tau_s[B2];
-  for (int e = tid; e < jb * jb; e += nt) {
-    const int t = e / jb, i = e % jb;
-    if (i >= t) band_at(J.band, j0 + i, j0 + t) = A[(j0 + i) + (long long)(j0 + t) * lda];
+  const int m = max(0, n - r0);
+  const int mc = (m + CS - 1) / CS;          // rows per CTA
+  const int lo = min(m, crank * mc), hi = min(m, lo + mc), ml = hi - lo;
+  const int ldp = mc + 1;
+  extern __shared__ double psm[];
+  double* Pl = psm;                          // [B2][ldp]
+  double* xbuf = Pl + (size_t)B2 * ldp;      // [CS][2]   norm partial, alpha
+  double* dbuf = xbuf + 2 * CS;              // [CS][B2]  column-dot partials
+  double* sbuf = dbuf + (size_t)CS * B2;     // [CS][B2*B2] V^T V partials (rank 0)
+  __shared__ double beta_s[B2], tau_s[B2], red[32];
+  __shared__ double S[B2][B2 + 1], T[B2][B2 + 1];
+  cluster.sync();  // peers' shared memory is live before any DSMEM write
+  if (j0 >= n) {
+    cluster.sync();
+    return;
   }
-  if (m <= 0) return;
+  if (crank == 0)
+    for (int e = tid; e < jb * jb; e += nt) {
+      const int t = e / jb, i = e % jb;
+      if (i >= t) band_at(J.band, j0 + i, j0 + t) = A[(j0 + i) + (long long)(j0 + t) * lda];
+    }
   const int nr = m >= 2 ? min(jb, m - 1) : 0;
   double* P = A + r0 + (long long)j0 * lda;
+  // panel rows -> shared memory
+  for (int e = tid; e < jb * ml; e += nt) {
+    const int t = e / ml, i = e % ml;
+    Pl[t * ldp + i] = P[lo + i + (long long)t * lda];
+  }
+  __syncthreads();
   for (int t = 0; t < nr; ++t) {
-    double* pt = P + (long long)t * lda;
+    double* pt = Pl + t * ldp;
+    // (a) norm of rows t+1.. and alpha = P[t][t]
     double part = 0.0;
-    for (int i = t + 1 + tid; i < m; i += nt) part += pt[i] * pt[i];
-    const double xn2 = block_sum(part, red);
-    const double alpha = pt[t];
+    for (int i = max(0, t + 1 - lo) + tid; i < ml; i += nt) part += pt[i] * pt[i];
+    part = block_sum(part, red);
+    const bool own_t = t >= lo && t < hi;
+    if (tid == 0)
+      for (int c = 0; c < CS; ++c) {
+        double* px = cluster.map_shared_rank(xbuf, c);
+        px[2 * crank] = part;
+        if (own_t) px[1] = pt[t - lo];  // slot 1 of rank 0's pair is unused
+      }
+    cluster.sync();
+    double xn2 = 0.0;
+    for (int c = 0; c < CS; ++c) xn2 += xbuf[2 * c];
+    const double alpha = xbuf[1];
     double tau = 0.0, beta = alpha, scal = 0.0;
     if (xn2 > 0.0) {
       const double nrm = sqrt(alpha * alpha + xn2);
@@ -761,75 +796,123 @@ __global__ void __launch_bounds__(512) k_panel_qr(const EigDev* __restrict__ job
       tau = (beta - alpha) / beta;
       scal = 1.0 / (alpha - beta);
     }
-    for (int i = t + 1 + tid; i < m; i += nt) pt[i] *= scal;
+    for (int i = max(0, t + 1 - lo) + tid; i < ml; i += nt) pt[i] *= scal;
     if (tid == 0) {
       beta_s[t] = beta;
       tau_s[t] = tau;
-      J.tau[j0 + t] = tau;
+      if (crank == 0) J.tau[j0 + t] = tau;
     }
     __syncthreads();
+    // (c) s_u = P[t][u] + sum_{i>t} v_i P[i][u] for u > t (partials)
+    for (int u = t + 1 + warp; u < jb; u += nwarps) {
+      const double* pu = Pl + u * ldp;
+      double sp = 0.0;
+      for (int i = max(0, t + 1 - lo) + lane; i < ml; i += 32) sp += pt[i] * pu[i];
+      sp = warp_sum(sp);
+      if (own_t) sp += pu[t - lo];
+      if (lane < CS) cluster.map_shared_rank(dbuf, lane)[crank * B2 + u] = sp;
+    }
+    cluster.sync();
+    // (d) P[i][u] -= tau s_u v_i
     if (tau != 0.0) {
       for (int u = t + 1 + warp; u < jb; u += nwarps) {
-        double* pu = P + (long long)u * lda;
-        double s = 0.0;
-        for (int i = t + 1 + lane; i < m; i += 32) s += pt[i] * pu[i];
-        s = warp_sum(s) + pu[t];
-        s *= tau;
-        if (lane == 0) pu[t] -= s;
-        for (int i = t + 1 + lane; i < m; i += 32) pu[i] -= s * pt[i];
+        double su = 0.0;
+        for (int c = 0; c < CS; ++c) su += dbuf[c * B2 + u];
+        su *= tau;
+        double* pu = Pl + u * ldp;
+        if (own_t && lane == 0) pu[t - lo] -= su;
+        for (int i = max(0, t + 1 - lo) + lane; i < ml; i += 32) pu[i] -= su * pt[i];
       }
     }
     __syncthreads();
   }
   if (tid < B2 && tid >= nr) {
     tau_s[tid] = 0.0;
-    if (tid < jb) J.tau[j0 + tid] = 0.0;
+    if (crank == 0 && tid < jb) J.tau[j0 + tid] = 0.0;
   }
   __syncthreads();
-  // R -> band (rows r0+i, columns j0+t, i <= t)
+  // R -> band (panel rows i <= t < B2, owned by the CTAs holding rows < B2)
   for (int e = tid; e < jb * jb; e += nt) {
     const int t = e / jb, i = e % jb;
-    if (i <= t && i < m)
-      band_at(J.band, r0 + i, j0 + t) = (i == t && t < nr) ? beta_s[t] : P[i + (long long)t * lda];
+    if (i <= t && i < m && i >= lo && i < hi)
+      band_at(J.band, r0 + i, j0 + t) = (i == t && t < nr) ? beta_s[t] : Pl[t * ldp + i - lo];
+  }
+  // explicit V (unit lower trapezoidal) in place, in the VW / WV panels and
+  // in shared memory (for V^T V)
+  __syncthreads();
+  for (int e = tid; e < jb * ml; e += nt) {
+    const int t = e / ml, i = e % ml, ig = lo + i;
+    const double v = t >= nr ? 0.0 : (ig < t ? 0.0 : (ig == t ? 1.0 : Pl[t * ldp + i]));
+    Pl[t * ldp + i] = v;
+    P[ig + (long long)t * lda] = v;
+    J.VW[(r0 + ig) + (long long)t * n] = v;
+    J.WV[(r0 + ig) + (long long)(B2 + t) * n] = v;
   }
   __syncthreads();
-  // explicit V (unit lower trapezoidal) in place and in the VW / WV panels
-  for (int t = 0; t < jb; ++t) {
-    double* pt = P + (long long)t * lda;
-    for (int i = tid; i < m; i += nt) {
-      const double v = t >= nr ? 0.0 : (i < t ? 0.0 : (i == t ? 1.0 : pt[i]));
-      pt[i] = v;
-      J.VW[(r0 + i) + (long long)t * n] = v;
-      J.WV[(r0 + i) + (long long)(B2 + t) * n] = v;
-    }
-  }
-  __syncthreads();
-  // T (dlarft forward columnwise) from S = V^T V
+  // S = V^T V: partials of the local rows into rank 0
+  double* s0 = cluster.map_shared_rank(sbuf, 0) + (size_t)crank * B2 * B2;
   for (int pq = warp; pq < B2 * B2; pq += nwarps) {
-    const int p = pq / B2, q = pq % B2;
-    if (p > q) continue;
-    double s = 0.0;
+    const int pp = pq / B2, q = pq % B2;
+    if (pp > q) continue;
+    double sp = 0.0;
     if (q < nr) {
-      const double* vp = P + (long long)p * lda;
-      const double* vq = P + (long long)q * lda;
-      for (int i = q + lane; i < m; i += 32) s += vp[i] * vq[i];
-      s = warp_sum(s);
+      const double* vp = Pl + pp * ldp;
+      const double* vq = Pl + q * ldp;
+      for (int i = max(0, q - lo) + lane; i < ml; i += 32) sp += vp[i] * vq[i];
+      sp = warp_sum(sp);
     }
-    if (lane == 0) S[p][q] = s;
+    if (lane == 0) s0[pq] = sp;
+  }
+  cluster.sync();  // last DSMEM access: peers may exit after this
+  if (crank != 0) return;
+  for (int pq = tid; pq < B2 * B2; pq += nt) {
+    const int pp = pq / B2, q = pq % B2;
+    double sv = 0.0;
+    if (pp <= q)
+      for (int c = 0; c < CS; ++c) sv += sbuf[(size_t)c * B2 * B2 + pq];
+    S[pp][q] = sv;
   }
   for (int e = tid; e < B2 * (B2 + 1); e += nt) (&T[0][0])[e] = 0.0;
   __syncthreads();
   for (int t = 0; t < B2; ++t) {
     if (tid < t) {
-      double s = 0.0;
-      for (int l = tid; l < t; ++l) s += T[tid][l] * S[l][t];
-      T[tid][t] = -tau_s[t] * s;
+      double sv = 0.0;
+      for (int l = tid; l < t; ++l) sv += T[tid][l] * S[l][t];
+      T[tid][t] = -tau_s[t] * sv;
     }
     if (tid == 0) T[t][t] = tau_s[t];
     __syncthreads();
   }
   double* out = J.Tp + (long long)(j0 / B2) * B2 * B2;
   for (int e = tid; e < B2 * B2; e += nt) out[e] = T[e % B2][e / B2];
+}
+
+constexpr size_t kPanelSmemMax = 200 * 1024;
+size_t panel_smem(int mc, int cs) {
+  return ((size_t)B2 * (mc + 1) + 2 * cs + (size_t)cs * B2 + (size_t)cs * B2 * B2) * sizeof(double);
+}
+
+void launch_panel_qr(Ctx& ctx, int count, int mmax, const EigDev* dd, int j0) {
+  int cs = 1;
+  while (cs < 8 && panel_smem((mmax + cs - 1) / cs, cs) > kPanelSmemMax) cs *= 2;
+  const size_t smem = panel_smem((mmax + cs - 1) / cs, cs);
+  if (smem > kPanelSmemMax) throw Error(kInvalid, "k_panel_qr: n too large");
+  smem_optin(k_panel_qr, smem);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(count * cs);
+  cfg.blockDim = dim3(512);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = ctx.stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  ctx.launch_begin();
+  HSVD_CUDA(cudaLaunchKernelEx(&cfg, k_panel_qr, dd, j0, cs));
+  ctx.check_launch("k_panel_qr");
 }
 
 // WV[:, 0:B2] = W (= VW[:, B2:2B2]) for the rows below the panel
@@ -981,7 +1064,7 @@ __global__ void __launch_bounds__(CHASE_WARPS * 32, 1) k_chase(const EigDev* __r
           const int vs = (int)(pv >> 32) - 1;
           const unsigned st = (unsigned)(pv & 0xffffffffu);
           if (vs > s - 1 || (vs == s - 1 && (st >= need))) break;
-          __nanosleep(32);
+          __nanosleep(200);
         }
         __threadfence_block();
       }
@@ -1068,16 +1151,19 @@ __global__ void __launch_bounds__(INV_WARPS * 32, 3) k_band_invit(const EigDev* 
         if (c < n) win[(i % WR) * WC + (c % WC)] = band_full(b0, n, i, c) - (i == c ? sh : 0.0);
     __syncwarp();
     double preA[3], preB[3];
-    auto fetch_row = [&](double* pre, int rn, int jj) {
-#pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        const int cc = lane + 32 * q, col = jj + 1 + cc;
-        pre[q] = (rn < n && cc < WC && col < n) ? band_full(b0, n, rn, col) - (rn == col ? sh : 0.0)
-                                                : 0.0;
-      }
+    // band row rn = jj + B2 + 1 at columns jj+1+cc, cc = lane + 32q: q = 0
+    // the strictly lower part (diagonal B2-lane of column rn-B2+lane), q = 1
+    // diagonal and upper part (column rn of the band, mirrored), q = 2
+    // (lane 0) the last upper element
+    auto fetch_row = [&](double* pre, int rn) {
+      const bool in = rn < n;
+      const double* crn = b0 + (long long)rn * LDBB;
+      pre[0] = in ? b0[(B2 - lane) + (long long)(rn - B2 + lane) * LDBB] : 0.0;
+      pre[1] = (in && rn + lane < n) ? crn[lane] - (lane == 0 ? sh : 0.0) : 0.0;
+      pre[2] = (in && lane == 0 && rn + B2 < n) ? crn[B2] : 0.0;
     };
-    fetch_row(preA, B2 + 1, 0);
-    fetch_row(preB, B2 + 2, 1);
+    fetch_row(preA, B2 + 1);
+    fetch_row(preB, B2 + 2);
     for (int j = 0; j < n; ++j) {
       const int nw = min(WR, n - j);  // candidate rows j..j+nw-1
       const int cj = j % WC;
@@ -1113,13 +1199,28 @@ __global__ void __launch_bounds__(INV_WARPS * 32, 3) k_band_invit(const EigDev* 
       const double ru = 1.0 / u;
       const int ncol = min(2 * B2, n - 1 - j);
       // columns j+1..j+ncol sit in slots cj+1..WC-1 then 0..(cj+ncol-WC)
-      const int hi1 = min(WC - 1, cj + ncol), hi2 = cj + ncol - WC;
-      // lane i (1..nw-1) eliminates row j+i
+      // lane i (1..nw-1) eliminates row j+i over all 2*B2 window columns
+      // after j (columns past n hold zeros in both rows), eight at a time
+      // with the loads batched ahead of the stores
       if (lane >= 1 && lane < nw) {
         const int si = ((j + lane) % WR) * WC;
         const double l = win[si + cj] * ru;
-        for (int c = cj + 1; c <= hi1; ++c) win[si + c] -= l * win[sj + c];
-        for (int c = 0; c <= hi2; ++c) win[si + c] -= l * win[sj + c];
+        double* ri = win + si;
+        const double* rp = win + sj;
+#pragma unroll
+        for (int c0 = 1; c0 <= 2 * B2; c0 += 8) {
+          int cc[8];
+          double x[8], y[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int c = cj + c0 + q;
+            cc[q] = c >= WC ? c - WC : c;
+            x[q] = ri[cc[q]];
+            y[q] = rp[cc[q]];
+          }
+#pragma unroll
+          for (int q = 0; q < 8; ++q) ri[cc[q]] = x[q] - l * y[q];
+        }
         Lm[(size_t)j * B2 + (lane - 1)] = l;
       }
       if (nw == WR) {  // row j+B2: its columns split over the lanes
@@ -1163,7 +1264,7 @@ __global__ void __launch_bounds__(INV_WARPS * 32, 3) k_band_invit(const EigDev* 
       }
 #pragma unroll
       for (int q = 0; q < 3; ++q) preA[q] = preB[q];
-      fetch_row(preB, j + B2 + 3, j + 2);
+      fetch_row(preB, j + B2 + 3);
       __syncwarp();
     }
     __syncwarp();
@@ -1572,9 +1673,7 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
   std::vector<GemmDesc> g1, g2, g3, g4, g5, g6;
   for (int p = 0; p < npan; ++p) {
     const int j0 = p * B2, r0 = j0 + B2;
-    ctx.launch_begin();
-    k_panel_qr<<<count, 512, 0, ctx.stream>>>(dd, j0);
-    ctx.check_launch("k_panel_qr");
+    launch_panel_qr(ctx, count, std::max(0, nmax - r0), dd, j0);
     g1.clear(); g2.clear(); g3.clear(); g4.clear(); g5.clear(); g6.clear();
     for (int g = 0; g < count; ++g) {
       const EigDev& e = dev[g];
