@@ -38,6 +38,7 @@ constexpr int EIG_THREADS = 256;
 constexpr int NB = 32;       // reflectors per compact-WY block
 constexpr int B2 = 32;       // bandwidth of the two-stage reduction
 constexpr int LDBB = 2 * B2 + 1;  // band storage: diagonals 0..2*B2 (chase fill)
+constexpr int kBandGroupDefault = 4;  // panels per delayed trailing update (two-stage stage 1)
 constexpr int INV_WARPS = 4;      // warps (= LU workspace slots) per band inverse iteration CTA
 
 struct EigDev {
@@ -66,6 +67,7 @@ struct EigDev {
   double* Y;         // n x B2
   double* P1;        // B2 x B2
   double* Mb;        // B2 x B2
+  double* Z1;        // (2*B2*group) x B2: pending-update products
   double* lu;        // per-warp band LU workspace (cpm * INV_WARPS slots per matrix)
   long long lu_slot;  // doubles per slot
 };
@@ -726,7 +728,7 @@ __device__ __forceinline__ double& band_at(double* bb, int i, int j) {
 // Panel j0: copy the diagonal block to the band, Householder QR of the
 // panel below the band (R -> band, explicit V in place and in VW/WV), T.
 __global__ void __launch_bounds__(512, 1) k_panel_qr(const EigDev* __restrict__ jobs, int j0,
-                                                     int CS) {
+                                                     int CS, int vcol) {
   // One matrix per cluster of CS CTAs; CTA c keeps rows [c*mc, (c+1)*mc) of
   // the m x B2 panel in shared memory (column-major, ld mc + 1) for the whole
   // factorisation.  Per column: the norm and the B2-1 column dots are summed
@@ -845,8 +847,8 @@ __global__ void __launch_bounds__(512, 1) k_panel_qr(const EigDev* __restrict__ 
     const double v = t >= nr ? 0.0 : (ig < t ? 0.0 : (ig == t ? 1.0 : Pl[t * ldp + i]));
     Pl[t * ldp + i] = v;
     P[ig + (long long)t * lda] = v;
-    J.VW[(r0 + ig) + (long long)t * n] = v;
-    J.WV[(r0 + ig) + (long long)(B2 + t) * n] = v;
+    J.VW[(r0 + ig) + (long long)(vcol + t) * n] = v;
+    J.WV[(r0 + ig) + (long long)(vcol + B2 + t) * n] = v;
   }
   __syncthreads();
   // S = V^T V: partials of the local rows into rank 0
@@ -892,7 +894,7 @@ size_t panel_smem(int mc, int cs) {
   return ((size_t)B2 * (mc + 1) + 2 * cs + (size_t)cs * B2 + (size_t)cs * B2 * B2) * sizeof(double);
 }
 
-void launch_panel_qr(Ctx& ctx, int count, int mmax, const EigDev* dd, int j0) {
+void launch_panel_qr(Ctx& ctx, int count, int mmax, const EigDev* dd, int j0, int vcol) {
   int cs = 1;
   while (cs < 8 && panel_smem((mmax + cs - 1) / cs, cs) > kPanelSmemMax) cs *= 2;
   const size_t smem = panel_smem((mmax + cs - 1) / cs, cs);
@@ -911,20 +913,30 @@ void launch_panel_qr(Ctx& ctx, int count, int mmax, const EigDev* dd, int j0) {
   cfg.attrs = at;
   cfg.numAttrs = 1;
   ctx.launch_begin();
-  HSVD_CUDA(cudaLaunchKernelEx(&cfg, k_panel_qr, dd, j0, cs));
+  HSVD_CUDA(cudaLaunchKernelEx(&cfg, k_panel_qr, dd, j0, cs, vcol));
   ctx.check_launch("k_panel_qr");
 }
 
-// WV[:, 0:B2] = W (= VW[:, B2:2B2]) for the rows below the panel
-__global__ void k_copy_w(const EigDev* __restrict__ jobs, int j0) {
+// WV[:, vcol:vcol+B2] = W (= VW[:, vcol+B2:vcol+2B2]) for the rows below the panel
+// (panels with no trailing matrix, r0 > n-2: W := 0 on the rows r0..n-1, so
+// the pending pairs of the group stay finite and exact)
+__global__ void k_copy_w(const EigDev* __restrict__ jobs, int j0, int vcol) {
   const EigDev J = jobs[blockIdx.y];
   const int n = J.n, r0 = j0 + B2;
-  if (r0 > n - 2) return;
+  if (r0 > n - 2) {
+    if (blockIdx.x == 0)
+      for (int e = threadIdx.x; e < max(0, n - r0) * B2; e += blockDim.x) {
+        const int i = r0 + e % max(1, n - r0), t = e / max(1, n - r0);
+        J.WV[i + (long long)(vcol + t) * n] = 0.0;
+        J.VW[i + (long long)(vcol + B2 + t) * n] = 0.0;
+      }
+    return;
+  }
   const long long total = (long long)(n - r0) * B2;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
     const int i = r0 + (int)(e % (n - r0)), t = (int)(e / (n - r0));
-    J.WV[i + (long long)t * n] = J.VW[i + (long long)(B2 + t) * n];
+    J.WV[i + (long long)(vcol + t) * n] = J.VW[i + (long long)(vcol + B2 + t) * n];
   }
 }
 
@@ -947,7 +959,12 @@ static_assert(B2 == 32, "k_chase maps one band row per lane");
 // (band column stride LDBB, diagonal stride LDBB-1); FULL (L == B2 and
 // nl == B2-1) drops the per-column bounds.  Returns false when the column
 // is already reduced (the sweep ends).
-template <bool FULL>
+template <bool CG>
+__device__ __forceinline__ double band_ld(const double* p) {
+  return CG ? __ldcg(p) : *p;
+}
+
+template <bool FULL, bool CG>
 __device__ __forceinline__ bool chase_step(double* bb, int c, int r0, int L, int nl, int na,
                                            int lane, double* vs, double* ws) {
   constexpr long long LD = LDBB;
@@ -959,17 +976,17 @@ __device__ __forceinline__ bool chase_step(double* bb, int c, int r0, int L, int
   double* pya = bb + (L + lane) + (long long)r0 * LD;           // (r0+L+lane, r0+j)
   const bool ly = lane < na;
   // all loads of the step issued together (one memory round trip)
-  const double x = lx ? *px : 0.0;
+  const double x = lx ? band_ld<CG>(px) : 0.0;
   double yl[B2 - 1], ar[B2], ya[B2];
 #pragma unroll
-  for (int l = 0; l < B2 - 1; ++l) yl[l] = (lx && (FULL || l < nl)) ? pyl[l * (LD - 1)] : 0.0;
+  for (int l = 0; l < B2 - 1; ++l) yl[l] = (lx && (FULL || l < nl)) ? band_ld<CG>(pyl + l * (LD - 1)) : 0.0;
 #pragma unroll
   for (int j = 0; j < B2; ++j) {
     const double* pa = lane >= j ? pa1 + j * (LD - 1) : pa2 + j;
-    ar[j] = (lx && (FULL || j < L)) ? *pa : 0.0;
+    ar[j] = (lx && (FULL || j < L)) ? band_ld<CG>(pa) : 0.0;
   }
 #pragma unroll
-  for (int j = 0; j < B2; ++j) ya[j] = (ly && (FULL || j < L)) ? pya[j * (LD - 1)] : 0.0;
+  for (int j = 0; j < B2; ++j) ya[j] = (ly && (FULL || j < L)) ? band_ld<CG>(pya + j * (LD - 1)) : 0.0;
   const double xn2 = warp_sum(lane >= 1 ? x * x : 0.0);
   const double alpha = __shfl_sync(0xffffffffu, x, 0);
   if (xn2 == 0.0) return false;
@@ -1038,20 +1055,35 @@ __device__ __forceinline__ bool chase_step(double* bb, int c, int r0, int L, int
   return true;
 }
 
-__global__ void __launch_bounds__(CHASE_WARPS * 32, 1) k_chase(const EigDev* __restrict__ jobs) {
-  const EigDev J = jobs[blockIdx.x];
+// The sweeps of one matrix run on a cluster of CS CTAs (CS * CHASE_WARPS
+// warps; sweep s on global warp s mod (CS * CHASE_WARPS)).  Progress flags
+// live in each CTA's shared memory and are polled through DSMEM; with CS > 1
+// the band is read through L2 (__ldcg), since a peer SM may have rewritten a
+// line this SM's L1 still holds, and every step's stores are fenced at gpu
+// scope before its flag is published.
+template <bool CL>
+__global__ void __launch_bounds__(CHASE_WARPS * 32, 1) k_chase(const EigDev* __restrict__ jobs,
+                                                              int CS) {
+  const int crank = CL ? (int)(blockIdx.x % CS) : 0;
+  const EigDev J = jobs[CL ? blockIdx.x / CS : blockIdx.x];
   const int n = J.n;
   double* bb = J.band;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, W = blockDim.x >> 5;
-  __shared__ unsigned long long prog[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int W = CHASE_WARPS * (CL ? CS : 1);   // warps working on this matrix
+  const int gw = crank * CHASE_WARPS + warp;    // this warp's global index
+  __shared__ unsigned long long prog[CHASE_WARPS];
   __shared__ double vsh[CHASE_WARPS][B2];
   __shared__ double wsh[CHASE_WARPS][B2];
-  if (tid < W) prog[tid] = prog_encode(tid - W, kSweepDone);
-  __syncthreads();
-  volatile unsigned long long* vprog = prog;
+  if (tid < CHASE_WARPS) prog[tid] = prog_encode(crank * CHASE_WARPS + tid - W, kSweepDone);
+  cg::cluster_group cluster = cg::this_cluster();
+  if (CL) cluster.sync();
+  else __syncthreads();
+  const int pg = (gw - 1 + W) % W;  // warp running sweep s-1
+  volatile unsigned long long* pprog =
+      CL ? cluster.map_shared_rank(prog, pg / CHASE_WARPS) + pg % CHASE_WARPS : prog + pg;
+  volatile unsigned long long* myprog = prog + warp;
   const int nsweeps = n - 2;
-  for (int s = warp; s < nsweeps; s += W) {
-    const int pslot = (warp - 1 + W) % W;
+  for (int s = gw; s < nsweeps; s += W) {
     for (int k = 0;; ++k) {
       const int r0 = s + 1 + k * B2;
       if (r0 >= n) break;
@@ -1060,33 +1092,42 @@ __global__ void __launch_bounds__(CHASE_WARPS * 32, 1) k_chase(const EigDev* __r
       if (s > 0) {  // wait for sweep s-1 to be 3 steps ahead (or done)
         const unsigned need = (unsigned)(k + 3);
         while (true) {
-          const unsigned long long pv = vprog[pslot];
+          const unsigned long long pv = *pprog;
           const int vs = (int)(pv >> 32) - 1;
           const unsigned st = (unsigned)(pv & 0xffffffffu);
           if (vs > s - 1 || (vs == s - 1 && (st >= need))) break;
-          __nanosleep(200);
+          __nanosleep(100);
         }
-        __threadfence_block();
+        if (CL) __threadfence();
+        else __threadfence_block();
       }
       const int c = k == 0 ? s : s + 1 + (k - 1) * B2;
       const int nl = r0 - c - 1;                // left-block columns (0 or B2-1)
       const int na = min(n, r0 + 2 * B2) - r1;  // rows after R
       const bool ok = (L == B2 && nl == B2 - 1)
-                          ? chase_step<true>(bb, c, r0, L, nl, na, lane, vsh[warp], wsh[warp])
-                          : chase_step<false>(bb, c, r0, L, nl, na, lane, vsh[warp], wsh[warp]);
+                          ? chase_step<true, CL>(bb, c, r0, L, nl, na, lane, vsh[warp], wsh[warp])
+                          : chase_step<false, CL>(bb, c, r0, L, nl, na, lane, vsh[warp], wsh[warp]);
       if (!ok) break;  // no bulge left in this sweep
       __syncwarp();
-      __threadfence_block();
-      if (lane == 0) vprog[warp] = prog_encode(s, (unsigned)(k + 1));
+      if (CL) __threadfence();
+      else __threadfence_block();
+      if (lane == 0) *myprog = prog_encode(s, (unsigned)(k + 1));
     }
     __syncwarp();
-    __threadfence_block();
-    if (lane == 0) vprog[warp] = prog_encode(s, kSweepDone);
+    if (CL) __threadfence();
+    else __threadfence_block();
+    if (lane == 0) *myprog = prog_encode(s, kSweepDone);
   }
-  __syncthreads();
+  if (CL) {
+    __threadfence();
+    cluster.sync();  // every sweep done; no DSMEM access after this
+    if (crank != 0) return;
+  } else {
+    __syncthreads();
+  }
   for (int i = tid; i < n; i += blockDim.x) {
-    J.d[i] = band_at(bb, i, i);
-    if (i < n - 1) J.e[i] = band_at(bb, i + 1, i);
+    J.d[i] = band_ld<CL>(&band_at(bb, i, i));
+    if (i < n - 1) J.e[i] = band_ld<CL>(&band_at(bb, i + 1, i));
   }
 }
 
@@ -1638,6 +1679,8 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
                int kkmax) {
   const int count = static_cast<int>(dev.size());
   const int npan = ceil_div(nmax, B2);
+  int kBandGroup = kBandGroupDefault;
+  if (const char* env = std::getenv("HSVD_BAND_GROUP")) kBandGroup = std::max(1, std::atoi(env));
   size_t lu_slot_max = 0;
   for (int g = 0; g < count; ++g) {
     EigDev& d = dev[g];
@@ -1645,9 +1688,10 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
     d.band = ctx.arena.alloc_n<double>((size_t)LDBB * n);
     d.band0 = ctx.arena.alloc_n<double>((size_t)LDBB * n);
     d.Tp = ctx.arena.alloc_n<double>((size_t)ceil_div(n, B2) * B2 * B2);
-    d.VW = ctx.arena.alloc_n<double>((size_t)n * 2 * B2);
-    d.WV = ctx.arena.alloc_n<double>((size_t)n * 2 * B2);
+    d.VW = ctx.arena.alloc_n<double>((size_t)n * 2 * B2 * kBandGroup);
+    d.WV = ctx.arena.alloc_n<double>((size_t)n * 2 * B2 * kBandGroup);
     d.Y = ctx.arena.alloc_n<double>((size_t)n * B2);
+    d.Z1 = ctx.arena.alloc_n<double>((size_t)2 * B2 * kBandGroup * B2);
     d.P1 = ctx.arena.alloc_n<double>((size_t)B2 * B2);
     d.Mb = ctx.arena.alloc_n<double>((size_t)B2 * B2);
     d.shifts = ctx.arena.alloc_n<double>(d.kk);
@@ -1668,13 +1712,33 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
   }
   const EigDev* dd = upload_jobs(ctx, dev);
 
-  // stage 1: dense -> band
+  // stage 1: dense -> band.  The trailing update is delayed over groups of
+  // kBandGroup panels: inside a group the panels' [V|W] pairs accumulate in
+  // VW / WV (64 columns per panel), the next panel's columns and its
+  // Y = A22 V are corrected with the pending pairs (small GEMMs with K = 64g),
+  // and one SYR2K with K = 64 * kBandGroup updates the trailing matrix at the
+  // end of the group (a quarter of the passes over A22).
   SubPhase sp1(ctx, "band");
-  std::vector<GemmDesc> g1, g2, g3, g4, g5, g6;
+  std::vector<GemmDesc> gc, g1, gz, gy, g2, g3, g4, g5, g6;
   for (int p = 0; p < npan; ++p) {
     const int j0 = p * B2, r0 = j0 + B2;
-    launch_panel_qr(ctx, count, std::max(0, nmax - r0), dd, j0);
-    g1.clear(); g2.clear(); g3.clear(); g4.clear(); g5.clear(); g6.clear();
+    const int gi = p % kBandGroup;        // panel index inside its group
+    const int vcol = 2 * B2 * gi;         // its [V|W] columns in VW / WV
+    const bool last_in_group = gi == kBandGroup - 1 || p == npan - 1;
+    if (gi > 0) {  // columns j0..j0+B2 (rows j0..n) with the pending updates
+      SubPhase sc(ctx, "band.corr");
+      gc.clear();
+      for (int g = 0; g < count; ++g) {
+        const EigDev& e = dev[g];
+        if (j0 >= e.n) continue;
+        const int rows = e.n - j0, cols = std::min(B2, e.n - j0);
+        gc.push_back({e.VW + j0, e.WV + j0, e.A + j0 + (long long)j0 * e.lda, e.n, e.n, e.lda, rows,
+                      cols, vcol, -1.0, 1.0});
+      }
+      gemm_grouped(ctx, DType::F64, DType::F64, false, true, false, gc);
+    }
+    launch_panel_qr(ctx, count, std::max(0, nmax - r0), dd, j0, vcol);
+    g1.clear(); gz.clear(); gy.clear(); g2.clear(); g3.clear(); g4.clear(); g5.clear(); g6.clear();
     for (int g = 0; g < count; ++g) {
       const EigDev& e = dev[g];
       const int n = e.n;
@@ -1683,18 +1747,32 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
       double* A22 = e.A + r0 + (long long)r0 * e.lda;
       const double* V = e.A + r0 + (long long)j0 * e.lda;
       const double* Tp = e.Tp + (long long)p * B2 * B2;
-      double* X = e.VW + r0 + (long long)B2 * n;
+      double* X = e.VW + r0 + (long long)(vcol + B2) * n;
       g1.push_back({A22, V, e.Y + r0, e.lda, e.lda, n, m, B2, m, 1.0, 0.0});       // Y = A22 V
+      if (gi > 0) {
+        gz.push_back({e.WV + r0, V, e.Z1, n, e.lda, vcol, vcol, B2, m, 1.0, 0.0});  // Z1 = WV^T V
+        gy.push_back({e.VW + r0, e.Z1, e.Y + r0, n, vcol, n, m, B2, vcol, -1.0, 1.0});  // Y -= VW Z1
+      }
       g2.push_back({e.Y + r0, Tp, X, n, B2, n, m, B2, B2, 1.0, 0.0});               // X = Y T
       g3.push_back({V, X, e.P1, e.lda, n, B2, B2, B2, m, 1.0, 0.0});                // P1 = V^T X
       g4.push_back({Tp, e.P1, e.Mb, B2, B2, B2, B2, B2, B2, 1.0, 0.0});             // M = T^T P1
       g5.push_back({V, e.Mb, X, e.lda, B2, n, m, B2, B2, -0.5, 1.0});               // W = X - V M/2
-      g6.push_back({e.VW + r0, e.WV + r0, A22, n, n, e.lda, m, m, 2 * B2, -1.0, 1.0});  // syr2k
+      if (last_in_group)                                                             // syr2k
+        g6.push_back({e.VW + r0, e.WV + r0, A22, n, n, e.lda, m, m, vcol + 2 * B2, -1.0, 1.0});
     }
-    if (g1.empty()) continue;
+    if (g1.empty()) {
+      ctx.launch_begin();
+      k_copy_w<<<dim3(1, count), 256, 0, ctx.stream>>>(dd, j0, vcol);
+      ctx.check_launch("k_copy_w");
+      continue;
+    }
     {
       SubPhase sy(ctx, "band.y");
       gemm_grouped(ctx, DType::F64, DType::F64, false, false, false, g1);
+      if (!gz.empty()) {
+        gemm_grouped(ctx, DType::F64, DType::F64, true, false, false, gz);
+        gemm_grouped(ctx, DType::F64, DType::F64, false, false, false, gy);
+      }
     }
     {
       SubPhase sw(ctx, "band.w");
@@ -1703,11 +1781,13 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
       gemm_grouped(ctx, DType::F64, DType::F64, true, false, false, g4);
       gemm_grouped(ctx, DType::F64, DType::F64, false, false, false, g5);
       ctx.launch_begin();
-      k_copy_w<<<dim3(256, count), 256, 0, ctx.stream>>>(dd, j0);
+      k_copy_w<<<dim3(256, count), 256, 0, ctx.stream>>>(dd, j0, vcol);
       ctx.check_launch("k_copy_w");
     }
-    SubPhase s2k(ctx, "band.syr2k");
-    gemm_grouped(ctx, DType::F64, DType::F64, false, true, true, g6);
+    if (!g6.empty()) {
+      SubPhase s2k(ctx, "band.syr2k");
+      gemm_grouped(ctx, DType::F64, DType::F64, false, true, true, g6);
+    }
   }
   for (int g = 0; g < count; ++g)
     HSVD_CUDA(cudaMemcpyAsync(dev[g].band0, dev[g].band, (size_t)LDBB * dev[g].n * sizeof(double),
@@ -1715,7 +1795,27 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
   // stage 2: band -> tridiagonal (values), eigenvalues by bisection
   SubPhase sp2(ctx, "tri");
   ctx.launch_begin();
-  k_chase<<<count, CHASE_WARPS * 32, 0, ctx.stream>>>(dd);
+  // spread each matrix's sweeps over a cluster while SMs would idle
+  int ccs = 1;
+  while (ccs < 2 && count * ccs * 2 <= ctx.num_sms) ccs *= 2;  // 4 measured slower
+  if (const char* env = std::getenv("HSVD_CHASE_CS")) ccs = std::max(1, std::atoi(env));
+  if (ccs == 1) {
+    k_chase<false><<<count, CHASE_WARPS * 32, 0, ctx.stream>>>(dd, 1);
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(count * ccs);
+    cfg.blockDim = dim3(CHASE_WARPS * 32);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = ctx.stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = ccs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    HSVD_CUDA(cudaLaunchKernelEx(&cfg, k_chase<true>, dd, ccs));
+  }
   ctx.check_launch("k_chase");
   {
     const size_t smem = (3 * (size_t)nmax + 3 * (size_t)kkmax + 32) * sizeof(double) +
