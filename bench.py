@@ -214,7 +214,9 @@ def roofline(prof, steps, w, hbm_peak, fp64_peak):
     fam = kernel_families(prof)
     name = max(fam, key=lambda k: fam[k][1])
     cnt, ms, fl = fam[name]
-    traffic = load_traffic(w.name).get(name)
+    meas = load_traffic(w.name)
+    # a committed measurement applies only to the same launch mix
+    traffic = meas.get(name) if meas.get("launches_per_step") == cnt / steps else None
     if name == "k_gemm" and fl > 0:
         peak = fp64_peak()
         achieved = fl / (ms / 1000.0) / 1e12

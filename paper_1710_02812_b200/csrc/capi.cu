@@ -74,7 +74,12 @@ DType dtype_of(int dt) {
 }
 
 // Brings x to the device (contiguous, ld = n) unless it already is there.
-XView stage_x(Ctx& c, const void* x, int dtype, int64_t m, int64_t n, int64_t ldx, int where) {
+// Host input: copied into the arena.  With chunk_rows > 0 the copy runs on
+// the context's copy stream in row chunks of that height (one per row slice
+// of the plan), each marked by an event, so the leaf Grams of the first
+// slices overlap the transfer of the later ones (XView::ready).
+XView stage_x(Ctx& c, const void* x, int dtype, int64_t m, int64_t n, int64_t ldx, int where,
+              int64_t chunk_rows = 0) {
   if (!x) throw Error(kInvalid, "x is null");
   if (m <= 0 || n <= 0) throw Error(kInvalid, "matrix is empty");
   if (ldx < n) throw Error(kInvalid, "ldx < n");
@@ -83,10 +88,35 @@ XView stage_x(Ctx& c, const void* x, int dtype, int64_t m, int64_t n, int64_t ld
   if (where == HSVD_CU_DEVICE) return v;
   const size_t es = v.dt == DType::F32 ? 4 : 8;
   void* d = c.arena.alloc((size_t)m * n * es);
-  HSVD_CUDA(cudaMemcpy2DAsync(d, n * es, x, ldx * es, n * es, m, cudaMemcpyHostToDevice, c.stream));
   v.X = d;
   v.ld = n;
+  if (chunk_rows <= 0 || chunk_rows >= m) {
+    HSVD_CUDA(cudaMemcpy2DAsync(d, n * es, x, ldx * es, n * es, m, cudaMemcpyHostToDevice, c.stream));
+    return v;
+  }
+  // the arena block may still be in use by earlier work on the compute stream
+  cudaStream_t cs = c.get_copy_stream();
+  cudaEvent_t start = c.get_chunk_event(0);
+  HSVD_CUDA(cudaEventRecord(start, c.stream));
+  HSVD_CUDA(cudaStreamWaitEvent(cs, start, 0));
+  size_t k = 1;
+  for (int64_t r = 0; r < m; r += chunk_rows, ++k) {
+    const int64_t rows = std::min<int64_t>(chunk_rows, m - r);
+    HSVD_CUDA(cudaMemcpy2DAsync(static_cast<char*>(d) + (size_t)r * n * es, n * es,
+                                static_cast<const char*>(x) + (size_t)r * ldx * es, ldx * es,
+                                n * es, rows, cudaMemcpyHostToDevice, cs));
+    cudaEvent_t ev = c.get_chunk_event(k);
+    HSVD_CUDA(cudaEventRecord(ev, cs));
+    v.ready.push_back({r + rows, ev});
+  }
   return v;
+}
+
+// Copy-chunk height for the overlapped input transfer: the plan's row slice
+// (hierarchy.cpp:11-18 partition), when there are several.
+int64_t overlap_rows(const HsvdConfig& hc, int64_t m) {
+  const int64_t d = (hc.d < 1 || hc.d > m) ? m : hc.d;
+  return d < m ? d : 0;
 }
 
 // Row-major host/device fp64 (rows x cols, ld) -> column-major device.
@@ -363,8 +393,9 @@ int hsvd_cu_rank_k_svd(hsvd_cu_ctx* ctx, const void* x, int dtype, int64_t m, in
     if (!x || m <= 0 || n <= 0) throw Error(kInvalid, "hierarchical_svd: matrix is empty");
     check_cfg(cfg);
     begin(ctx);
-    XView xv = stage_x(ctx->c, x, dtype, m, n, ldx, where);
-    DFac right = hierarchical_svd(ctx->c, xv, to_cfg(cfg));
+    const HsvdConfig hc = to_cfg(cfg);
+    XView xv = stage_x(ctx->c, x, dtype, m, n, ldx, where, overlap_rows(hc, m));
+    DFac right = hierarchical_svd(ctx->c, xv, hc);
     DFac f = recover_left_vectors(ctx->c, xv, right.B, right.ld, right.rank);
     *out = make_result(ctx, f, true, true);
     return HSVD_CU_OK;

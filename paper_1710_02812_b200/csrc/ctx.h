@@ -198,7 +198,28 @@ struct Ctx {
     }
     return h_dbl;
   }
+  // side stream for host->device input copies that overlap the compute
+  // stream, and the events marking the copied row chunks
+  cudaStream_t copy_stream = nullptr;
+  std::vector<cudaEvent_t> chunk_ev;
+  cudaStream_t get_copy_stream() {
+    if (!copy_stream) HSVD_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+    return copy_stream;
+  }
+  cudaEvent_t get_chunk_event(size_t i) {
+    while (chunk_ev.size() <= i) {
+      cudaEvent_t e;
+      HSVD_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      chunk_ev.push_back(e);
+    }
+    return chunk_ev[i];
+  }
   ~Ctx() {
+    for (auto e : chunk_ev) cudaEventDestroy(e);
+    if (copy_stream) {
+      cudaStreamSynchronize(copy_stream);
+      cudaStreamDestroy(copy_stream);
+    }
     if (h_ints) cudaFreeHost(h_ints);
     if (h_dbl) cudaFreeHost(h_dbl);
     for (auto& r : prof) {

@@ -65,6 +65,15 @@ void fetch_ranks(Ctx& ctx, const int* d_ranks, int count, std::vector<int>& out)
   std::memcpy(out.data(), h, count * sizeof(int));
 }
 
+void x_wait_rows(Ctx& ctx, const XView& x, long long row_end) {
+  long long prev = 0;
+  for (const RowChunk& c : x.ready) {
+    if (row_end >= 0 && prev >= row_end) break;
+    HSVD_CUDA(cudaStreamWaitEvent(ctx.stream, c.ev, 0));
+    prev = c.row_end;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // block SVD (leaves): Gram of the smaller side + top-k eigenpairs + projection
 // ---------------------------------------------------------------------------
@@ -111,8 +120,33 @@ std::vector<DFac> block_svd_batch(Ctx& ctx, const XView& x, const std::vector<Bl
       proj_w.push_back({base, m.Z, m.P, x.ld, m.q, m.s, bl.c, m.kk, bl.d, 1.0, 0.0});
   }
   ctx.phase = "leaf.gram";
-  gemm_grouped(ctx, x.dt, x.dt, false, true, true, gram_t);
-  gemm_grouped(ctx, x.dt, x.dt, true, false, true, gram_w);
+  if (x.ready.empty()) {
+    gemm_grouped(ctx, x.dt, x.dt, false, true, true, gram_t);
+    gemm_grouped(ctx, x.dt, x.dt, true, false, true, gram_w);
+  } else {
+    // input still arriving: one Gram launch per row-chunk group of blocks,
+    // each after its rows' copy (the copies overlap the earlier Grams)
+    // (the copy stream is in order: chunk c done implies every earlier one)
+    std::vector<GemmDesc> gt, gw;
+    long long prev = 0;
+    for (const RowChunk& c : x.ready) {
+      gt.clear();
+      gw.clear();
+      size_t it = 0, iw = 0;
+      for (int b = 0; b < nb; ++b) {
+        const bool tall = t[b].tall;
+        const GemmDesc& gd = tall ? gram_t[it++] : gram_w[iw++];
+        const Block& bl = blocks[b];
+        if (bl.r0 + bl.d <= prev || bl.r0 + bl.d > c.row_end) continue;
+        (tall ? gt : gw).push_back(gd);
+      }
+      HSVD_CUDA(cudaStreamWaitEvent(ctx.stream, c.ev, 0));
+      gemm_grouped(ctx, x.dt, x.dt, false, true, true, gt);
+      gemm_grouped(ctx, x.dt, x.dt, true, false, true, gw);
+      prev = c.row_end;
+    }
+    x_wait_rows(ctx, x);  // everything after reads any row
+  }
   ctx.phase = "leaf.eig";
   eig_topk(ctx, ej);
   ctx.phase = "leaf.proj";

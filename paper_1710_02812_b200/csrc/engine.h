@@ -23,12 +23,24 @@ struct DFac {
 };
 
 // Row-major m x n matrix on the device (reference DenseMatrix layout).
+// Row chunk [.., row_end) of a staged input is resident once `ev` completes.
+struct RowChunk {
+  long long row_end;
+  cudaEvent_t ev;
+};
+
 struct XView {
   const void* X;
   DType dt;
   long long ld;
   long long m, n;
+  // non-empty when X is still being copied in on the context's copy stream:
+  // work on rows < row_end must wait for the chunk's event first
+  std::vector<RowChunk> ready = {};
 };
+
+// Orders ctx.stream after the copies of rows [0, row_end) (all rows: -1).
+void x_wait_rows(Ctx& ctx, const XView& x, long long row_end = -1);
 
 struct Block {
   long long r0;
