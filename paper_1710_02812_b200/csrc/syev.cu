@@ -38,6 +38,7 @@ constexpr int EIG_THREADS = 256;
 constexpr int NB = 32;       // reflectors per compact-WY block
 constexpr int B2 = 32;       // bandwidth of the two-stage reduction
 constexpr int LDBB = 2 * B2 + 1;  // band storage: diagonals 0..2*B2 (chase fill)
+constexpr int kBandInvitMinN = 3072;  // band inverse iteration above this n
 constexpr int kBandGroupDefault = 4;  // panels per delayed trailing update (two-stage stage 1)
 constexpr int INV_WARPS = 4;      // warps (= LU workspace slots) per band inverse iteration CTA
 
@@ -58,7 +59,8 @@ struct EigDev {
   double* VW;    // n x 2*NB panel [V | W] (blocked tridiagonalisation)
   double* WV;    // n x 2*NB panel [W | V]
   // two-stage path
-  int vals_only;     // k_steig: eigenvalues (+ shifts, clusters) only
+  int vals_only;     // k_steig: 1 eigenvalues (+ shifts, clusters) only; 2 vectors
+                     // without the in-iteration Gram-Schmidt (k_band_mgs follows)
   double* shifts;    // kk perturbed inverse-iteration shifts
   int* cstarts;      // kk cluster starts
   double* band;      // (2*B2+1) x n lower band, chased to tridiagonal
@@ -69,6 +71,8 @@ struct EigDev {
   double* Mb;        // B2 x B2
   double* Z1;        // (2*B2*group) x B2: pending-update products
   double* lu;        // per-warp band LU workspace (cpm * INV_WARPS slots per matrix)
+  double* refl;      // chase reflectors: (steps) x 33 (v[0..31], tau), sweep-major
+  double* q2ws;      // k_q2_apply scratch (row-major n x 16 per warp)
   long long lu_slot;  // doubles per slot
 };
 
@@ -589,7 +593,13 @@ __global__ void __launch_bounds__(EIG_THREADS) k_steig(const EigDev* __restrict_
   }
   __syncthreads();
 
-  if (J.vals_only) {  // two-stage path: vectors come from the band matrix
+  if (J.vals_only) {  // two-stage path: clusters for k_band_mgs / band inverse iteration
+    for (int t = tid; t < kk; t += nt) {
+      J.shifts[t] = shift[t];
+      J.cstarts[t] = cstart[t];
+    }
+  }
+  if (J.vals_only == 1) {  // vectors come from the band matrix
     for (int t = tid; t < kk; t += nt) {
       J.lam[t] = lam[t];
       J.shifts[t] = shift[t];
@@ -637,7 +647,7 @@ __global__ void __launch_bounds__(EIG_THREADS) k_steig(const EigDev* __restrict_
       if (sc == 0.0) z[t % n] = 1.0;
     }
     __syncthreads();
-    if (it == 0) continue;
+    if (it == 0 || J.vals_only == 2) continue;
     // Gram-Schmidt (twice) inside clusters, in eigenvalue order
     for (int t = 0; t < kk; ++t) {
       const int cs = cstart[t];
@@ -964,9 +974,21 @@ __device__ __forceinline__ double band_ld(const double* p) {
   return CG ? __ldcg(p) : *p;
 }
 
+// Steps of sweep s (k with r0 = s+1+32k <= n-2) and the steps of all sweeps
+// before it: the compact sweep-major index of the stored chase reflectors.
+__device__ __forceinline__ int sweep_steps(int n, int s) { return (n - 3 - s) / B2 + 1; }
+__device__ __forceinline__ long long floor_sum(long long A) {  // sum_{a=0}^{A} floor(a/B2)
+  if (A < 0) return 0;
+  const long long q = (A + 1) / B2, r = (A + 1) % B2;
+  return B2 * q * (q - 1) / 2 + r * q;
+}
+__device__ __forceinline__ long long steps_before(int n, int s) {
+  return s + floor_sum(n - 3) - floor_sum(n - 3 - s);
+}
+
 template <bool FULL, bool CG>
 __device__ __forceinline__ bool chase_step(double* bb, int c, int r0, int L, int nl, int na,
-                                           int lane, double* vs, double* ws) {
+                                           int lane, double* vs, double* ws, double* rout) {
   constexpr long long LD = LDBB;
   const bool lx = lane < L;
   double* px = bb + (r0 + lane - c) + (long long)c * LD;
@@ -996,6 +1018,10 @@ __device__ __forceinline__ bool chase_step(double* bb, int c, int r0, int L, int
   const double scal = 1.0 / (alpha - beta);
   const double v = lane == 0 ? 1.0 : (lx ? x * scal : 0.0);
   vs[lane] = v;
+  if (rout) {  // kept for the eigenvector back-transform (k_q2_apply)
+    rout[lane] = v;
+    if (lane == 0) rout[B2] = tau;
+  }
   if (lx) *px = lane == 0 ? beta : 0.0;
   // left block: d_l = sum_i v_i y_il by a transposing butterfly (lane l
   // ends with d_l), then y_il -= tau v_i d_l
@@ -1104,10 +1130,17 @@ __global__ void __launch_bounds__(CHASE_WARPS * 32, 1) k_chase(const EigDev* __r
       const int c = k == 0 ? s : s + 1 + (k - 1) * B2;
       const int nl = r0 - c - 1;                // left-block columns (0 or B2-1)
       const int na = min(n, r0 + 2 * B2) - r1;  // rows after R
-      const bool ok = (L == B2 && nl == B2 - 1)
-                          ? chase_step<true, CL>(bb, c, r0, L, nl, na, lane, vsh[warp], wsh[warp])
-                          : chase_step<false, CL>(bb, c, r0, L, nl, na, lane, vsh[warp], wsh[warp]);
-      if (!ok) break;  // no bulge left in this sweep
+      double* rout = J.refl ? J.refl + (steps_before(n, s) + k) * (B2 + 1) : nullptr;
+      const bool ok =
+          (L == B2 && nl == B2 - 1)
+              ? chase_step<true, CL>(bb, c, r0, L, nl, na, lane, vsh[warp], wsh[warp], rout)
+              : chase_step<false, CL>(bb, c, r0, L, nl, na, lane, vsh[warp], wsh[warp], rout);
+      if (!ok) {  // no bulge left in this sweep: its remaining reflectors are I
+        if (J.refl && lane == 0)
+          for (int k2 = k; k2 < sweep_steps(n, s); ++k2)
+            J.refl[(steps_before(n, s) + k2) * (B2 + 1) + B2] = 0.0;
+        break;
+      }
       __syncwarp();
       if (CL) __threadfence();
       else __threadfence_block();
@@ -1128,6 +1161,99 @@ __global__ void __launch_bounds__(CHASE_WARPS * 32, 1) k_chase(const EigDev* __r
   for (int i = tid; i < n; i += blockDim.x) {
     J.d[i] = band_ld<CL>(&band_at(bb, i, i));
     if (i < n - 1) J.e[i] = band_ld<CL>(&band_at(bb, i + 1, i));
+  }
+}
+
+// Eigenvectors of the band matrix from those of its tridiagonal: Z <- Q2 Z
+// with Q2 the product of the chase reflectors in chase order, applied in
+// reverse (LAPACK dsbtrd's Q, applied as dormtr would).  One CTA per 32
+// eigenvectors of a matrix on a row-major n x 32 scratch copy (lane =
+// column: every row access is one coalesced 256-byte line).  The reflectors
+// of one sweep touch disjoint 32-row blocks: the CTA's warps share a sweep's
+// blocks, each prefetching its next block's rows while it applies the
+// current one, and synchronise once per sweep; the sweep's reflectors are
+// staged into shared memory by cp.async one sweep ahead.
+constexpr int Q2_COLS = 32, Q2_WARPS = 8;
+
+__device__ __forceinline__ void q2_cp8(double* dst, const double* src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src));
+}
+
+__global__ void __launch_bounds__(Q2_WARPS * 32, 1) k_q2_apply(const EigDev* __restrict__ jobs) {
+  const EigDev J = jobs[blockIdx.y];
+  const int n = J.n, kk = J.kk;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nt = blockDim.x;
+  const int c0 = blockIdx.x * Q2_COLS;
+  if (c0 >= kk || n < 3) return;
+  const int nc = min(Q2_COLS, kk - c0);
+  double* S = J.q2ws + (size_t)blockIdx.x * n * Q2_COLS;  // this matrix's scratch
+  extern __shared__ double rbuf[];                         // [2][kmax][B2 + 1]
+  const int kmax = sweep_steps(n, 0);
+  for (int e = tid; e < n * Q2_COLS; e += nt) {
+    const int r = e % n, q = e / n;
+    S[(size_t)r * Q2_COLS + q] = q < nc ? J.Z[r + (long long)(c0 + q) * J.ldz] : 0.0;
+  }
+  const double* R = J.refl;
+  auto stage = [&](int s, int buf) {
+    const double* src = R + steps_before(n, s) * (B2 + 1);
+    double* dst = rbuf + (size_t)buf * kmax * (B2 + 1);
+    const int cnt = sweep_steps(n, s) * (B2 + 1);
+    for (int e = tid; e < cnt; e += nt) q2_cp8(dst + e, src + e);
+  };
+  stage(n - 3, 0);
+  asm volatile("cp.async.commit_group;\n");
+  __syncthreads();
+  int it = 0;
+  for (int s = n - 3; s >= 0; --s, ++it) {
+    const int buf = it & 1;
+    if (s > 0) stage(s - 1, buf ^ 1);
+    asm volatile("cp.async.commit_group;\n");
+    asm volatile("cp.async.wait_group 1;\n");
+    __syncthreads();
+    const double* rb = rbuf + (size_t)buf * kmax * (B2 + 1);
+    const int K = sweep_steps(n, s);
+    double zn[B2];
+    auto fetch = [&](int k) {
+      const int r0 = s + 1 + k * B2, L = min(B2, n - r0);
+      const double* zb = S + (size_t)r0 * Q2_COLS + lane;
+#pragma unroll
+      for (int i = 0; i < B2; ++i) zn[i] = i < L ? zb[i * Q2_COLS] : 0.0;
+    };
+    if (warp < K) fetch(warp);
+    for (int k = warp; k < K; k += Q2_WARPS) {
+      double z[B2];
+#pragma unroll
+      for (int i = 0; i < B2; ++i) z[i] = zn[i];
+      if (k + Q2_WARPS < K) fetch(k + Q2_WARPS);  // disjoint rows of the same sweep
+      const double* rv = rb + k * (B2 + 1);
+      const double tau = rv[B2];
+      if (tau == 0.0) continue;
+      const int r0 = s + 1 + k * B2, L = min(B2, n - r0);
+      double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+#pragma unroll
+      for (int i = 0; i < B2; i += 4) {
+        d0 += rv[i] * z[i];
+        d1 += rv[i + 1] * z[i + 1];
+        d2 += rv[i + 2] * z[i + 2];
+        d3 += rv[i + 3] * z[i + 3];
+      }
+      const double dot = tau * ((d0 + d1) + (d2 + d3));
+      // all shared-memory reads of v before the global stores (a store could
+      // alias shared memory as far as the compiler knows)
+#pragma unroll
+      for (int i = 0; i < B2; ++i) z[i] -= dot * rv[i];
+      double* zb = S + (size_t)r0 * Q2_COLS + lane;
+#pragma unroll
+      for (int i = 0; i < B2; ++i)
+        if (i < L) zb[i * Q2_COLS] = z[i];
+    }
+    __syncthreads();  // next sweep: rows overlap, and this buffer is restaged
+  }
+  asm volatile("cp.async.wait_group 0;\n");
+  for (int e = tid; e < n * Q2_COLS; e += nt) {
+    const int r = e % n, q = e / n;
+    if (q < nc) J.Z[r + (long long)(c0 + q) * J.ldz] = S[(size_t)r * Q2_COLS + q];
   }
 }
 
@@ -1680,6 +1806,12 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
   const int count = static_cast<int>(dev.size());
   const int npan = ceil_div(nmax, B2);
   int kBandGroup = kBandGroupDefault;
+  // eigenvectors: inverse iteration on the tridiagonal + the chase
+  // reflectors (k_q2_apply), or inverse iteration on the band matrix
+  // (k_band_invit).  Measured on B200 (64-matrix batches): the first wins at
+  // n = 2048 and 2500, the second at n = 4096.  HSVD_BAND_INVIT=0/1 forces.
+  bool band_invit = nmax > kBandInvitMinN;
+  if (const char* env = std::getenv("HSVD_BAND_INVIT")) band_invit = std::atoi(env) != 0;
   if (const char* env = std::getenv("HSVD_BAND_GROUP")) kBandGroup = std::max(1, std::atoi(env));
   size_t lu_slot_max = 0;
   for (int g = 0; g < count; ++g) {
@@ -1696,7 +1828,12 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
     d.Mb = ctx.arena.alloc_n<double>((size_t)B2 * B2);
     d.shifts = ctx.arena.alloc_n<double>(d.kk);
     d.cstarts = ctx.arena.alloc_n<int>(d.kk);
-    d.vals_only = 1;
+    d.vals_only = band_invit ? 1 : 2;
+    if (!band_invit) {
+      long long steps = 0;  // chase reflectors of all sweeps
+      for (int s2 = 0; s2 <= n - 3; ++s2) steps += (n - 3 - s2) / B2 + 1;
+      d.refl = ctx.arena.alloc_n<double>((size_t)std::max(1LL, steps) * (B2 + 1));
+    }
     HSVD_CUDA(cudaMemsetAsync(d.band, 0, (size_t)LDBB * n * sizeof(double), ctx.stream));
     lu_slot_max = std::max(lu_slot_max, (size_t)n * (2 * B2 + 1 + B2 + 3));
   }
@@ -1705,10 +1842,16 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
   // capped at 8 GB
   int cpm = std::max(1, std::min(ceil_div(3 * ctx.num_sms, count), ceil_div(kkmax, INV_WARPS)));
   while (cpm > 1 && lu_slot_max * sizeof(double) * INV_WARPS * cpm * count > (size_t(8) << 30)) --cpm;
-  double* lu = ctx.arena.alloc_n<double>(lu_slot_max * INV_WARPS * cpm * count);
-  for (int g = 0; g < count; ++g) {  // indexed by blockIdx.x in the kernel
-    dev[g].lu = lu;
-    dev[g].lu_slot = (long long)lu_slot_max;
+  const int q2x = ceil_div(kkmax, Q2_COLS);
+  if (band_invit) {
+    double* lu = ctx.arena.alloc_n<double>(lu_slot_max * INV_WARPS * cpm * count);
+    for (int g = 0; g < count; ++g) {  // indexed by blockIdx.x in the kernel
+      dev[g].lu = lu;
+      dev[g].lu_slot = (long long)lu_slot_max;
+    }
+  } else {
+    for (int g = 0; g < count; ++g)
+      dev[g].q2ws = ctx.arena.alloc_n<double>((size_t)q2x * dev[g].n * Q2_COLS);
   }
   const EigDev* dd = upload_jobs(ctx, dev);
 
@@ -1826,7 +1969,16 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
     ctx.check_launch("k_steig");
   }
   // eigenvectors of the band matrix
-  {
+  if (!band_invit) {
+    ctx.launch_begin();
+    k_band_mgs<<<count, 256, 0, ctx.stream>>>(dd);  // clusters of the tridiagonal's vectors
+    ctx.check_launch("k_band_mgs");
+    ctx.launch_begin();
+    const size_t q2smem = (size_t)2 * ((nmax - 3) / B2 + 1) * (B2 + 1) * sizeof(double);
+    smem_optin(k_q2_apply, q2smem);
+    k_q2_apply<<<dim3(q2x, count), Q2_WARPS * 32, q2smem, ctx.stream>>>(dd);
+    ctx.check_launch("k_q2_apply");
+  } else {
     const size_t smem =
         ((size_t)INV_WARPS * ((B2 + 1) * (2 * B2 + 1) + INV_RING) + 64) * sizeof(double);
     smem_optin(k_band_invit, smem);

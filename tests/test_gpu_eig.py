@@ -15,11 +15,14 @@ def _gram(n, seed, decay):
     return x.T @ x
 
 
-@pytest.mark.parametrize("path", ["one", "two"])
+@pytest.mark.parametrize("path", ["one", "two", "two_bandinvit"])
 @pytest.mark.parametrize("n,kk", [(40, 10), (97, 97), (300, 40), (700, 100), (1100, 64)])
 def test_syevx_topk(path, n, kk, monkeypatch):
+    """path: one-stage; two-stage with tridiagonal inverse iteration + chase
+    reflectors; two-stage with inverse iteration on the band matrix."""
     import paper_1710_02812_b200 as H
-    monkeypatch.setenv("HSVD_TWO_STAGE_MIN_N", "1" if path == "two" else str(1 << 30))
+    monkeypatch.setenv("HSVD_TWO_STAGE_MIN_N", "1" if path.startswith("two") else str(1 << 30))
+    monkeypatch.setenv("HSVD_BAND_INVIT", "1" if path == "two_bandinvit" else "0")
     a = _gram(n, n + kk, 6.0)
     lam, z = H.syevx_topk(a, kk)
     w, v = np.linalg.eigh(a)
