@@ -1108,6 +1108,18 @@ __global__ void __launch_bounds__(CHASE_WARPS * 32, 1) k_chase(const EigDev* __r
   volatile unsigned long long* pprog =
       CL ? cluster.map_shared_rank(prog, pg / CHASE_WARPS) + pg % CHASE_WARPS : prog + pg;
   volatile unsigned long long* myprog = prog + warp;
+  // release-store of this warp's progress (cluster scope: the consumer may
+  // run on the peer SM and reads the band through L2 after its acquire)
+  auto publish = [&](unsigned long long val) {
+    if (CL) {
+      if (lane == 0)
+        asm volatile("st.release.cluster.u64 [%0], %1;\n" ::"l"(myprog), "l"(val) : "memory");
+    } else {
+      __threadfence_block();
+      if (lane == 0) *myprog = val;
+    }
+  };
+  unsigned long long seen = 0;  // last acquired progress of sweep s-1's warp
   const int nsweeps = n - 2;
   for (int s = gw; s < nsweeps; s += W) {
     for (int k = 0;; ++k) {
@@ -1117,15 +1129,31 @@ __global__ void __launch_bounds__(CHASE_WARPS * 32, 1) k_chase(const EigDev* __r
       if (L < 2) break;
       if (s > 0) {  // wait for sweep s-1 to be 3 steps ahead (or done)
         const unsigned need = (unsigned)(k + 3);
-        while (true) {
-          const unsigned long long pv = *pprog;
+        auto ahead = [&](unsigned long long pv) {
           const int vs = (int)(pv >> 32) - 1;
           const unsigned st = (unsigned)(pv & 0xffffffffu);
-          if (vs > s - 1 || (vs == s - 1 && (st >= need))) break;
-          __nanosleep(100);
+          return vs > s - 1 || (vs == s - 1 && st >= need);
+        };
+        // progress only grows: a value already acquired that suffices needs
+        // no new (remote) poll
+        if (!ahead(seen)) {
+          while (true) {
+            unsigned long long pv;
+            if (CL)
+              asm volatile("ld.acquire.cluster.u64 %0, [%1];\n"
+                           : "=l"(pv)
+                           : "l"(pprog)
+                           : "memory");
+            else
+              pv = *pprog;
+            if (ahead(pv)) {
+              seen = pv;
+              break;
+            }
+            __nanosleep(100);
+          }
+          if (!CL) __threadfence_block();
         }
-        if (CL) __threadfence();
-        else __threadfence_block();
       }
       const int c = k == 0 ? s : s + 1 + (k - 1) * B2;
       const int nl = r0 - c - 1;                // left-block columns (0 or B2-1)
@@ -1141,15 +1169,11 @@ __global__ void __launch_bounds__(CHASE_WARPS * 32, 1) k_chase(const EigDev* __r
             J.refl[(steps_before(n, s) + k2) * (B2 + 1) + B2] = 0.0;
         break;
       }
-      __syncwarp();
-      if (CL) __threadfence();
-      else __threadfence_block();
-      if (lane == 0) *myprog = prog_encode(s, (unsigned)(k + 1));
+      __syncwarp();  // every lane's band stores before lane 0's release
+      publish(prog_encode(s, (unsigned)(k + 1)));
     }
     __syncwarp();
-    if (CL) __threadfence();
-    else __threadfence_block();
-    if (lane == 0) *myprog = prog_encode(s, kSweepDone);
+    publish(prog_encode(s, kSweepDone));
   }
   if (CL) {
     __threadfence();
