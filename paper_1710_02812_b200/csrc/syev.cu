@@ -34,7 +34,7 @@ namespace {
 
 constexpr int TRD_THREADS = 1024;
 constexpr int TRD_QMAX = 8;  // rows per thread when n > 1024 (n <= 8192)
-constexpr int EIG_THREADS = 256;
+constexpr int EIG_THREADS = 512;
 constexpr int NB = 32;       // reflectors per compact-WY block
 constexpr int B2 = 32;       // bandwidth of the two-stage reduction
 constexpr int LDBB = 2 * B2 + 1;  // band storage: diagonals 0..2*B2 (chase fill)
@@ -556,20 +556,72 @@ __global__ void __launch_bounds__(EIG_THREADS) k_steig(const EigDev* __restrict_
   }
   const double pivmin = DBL_MIN * fmax(1.0, e2m);
 
-  // bisection (dstebz): eigenvalue with ascending index n-1-t
-  for (int t = tid; t < kk; t += nt) {
-    const int idx = n - 1 - t;
-    double lo = gl - 4.0 * eps * tnorm - 2.0 * pivmin;
-    double hi = gu + 4.0 * eps * tnorm + 2.0 * pivmin;
-    for (int it = 0; it < 256; ++it) {
-      const double tol = 2.0 * eps * fmax(fabs(lo), fabs(hi)) + 4.0 * pivmin;
-      if (hi - lo <= tol) break;
-      const double mid = 0.5 * (lo + hi);
-      if (mid <= lo || mid >= hi) break;
-      if (sturm_count_less(dd, e2, n, mid, pivmin) > idx) hi = mid;
-      else lo = mid;
+  // eigenvalue with ascending index n-1-t (dstebz's tolerance): multisection
+  // with P = nt / kk threads per eigenvalue -- each round evaluates P
+  // interior points of the bracket and keeps the sub-interval holding the
+  // eigenvalue (P = 1 is bisection), so the sequential Sturm counts per
+  // eigenvalue drop from ~52 to ~52 / log2(P + 1)
+  {
+    const int P = max(1, nt / kk);
+    double* blo = dots;  // [kk] bracket (the dots scratch is free here)
+    double* bhi = shift;
+    int* cnt = reinterpret_cast<int*>(cstart);  // [kk * P] (cstart is set later)
+    for (int t = tid; t < kk; t += nt) {
+      blo[t] = gl - 4.0 * eps * tnorm - 2.0 * pivmin;
+      bhi[t] = gu + 4.0 * eps * tnorm + 2.0 * pivmin;
     }
-    lam[t] = 0.5 * (lo + hi);
+    __syncthreads();
+    if (P == 1) {
+      for (int t = tid; t < kk; t += nt) {
+        const int idx = n - 1 - t;
+        double lo = blo[t], hi = bhi[t];
+        for (int it = 0; it < 256; ++it) {
+          const double tol = 2.0 * eps * fmax(fabs(lo), fabs(hi)) + 4.0 * pivmin;
+          if (hi - lo <= tol) break;
+          const double mid = 0.5 * (lo + hi);
+          if (mid <= lo || mid >= hi) break;
+          if (sturm_count_less(dd, e2, n, mid, pivmin) > idx) hi = mid;
+          else lo = mid;
+        }
+        lam[t] = 0.5 * (lo + hi);
+      }
+    } else {
+      const int t = tid / P, g = tid % P;
+      const bool mine = t < kk;
+      for (int round = 0; round < 256; ++round) {
+        bool active = false;
+        double x = 0.0;
+        if (mine) {
+          const double lo = blo[t], hi = bhi[t];
+          const double tol = 2.0 * eps * fmax(fabs(lo), fabs(hi)) + 4.0 * pivmin;
+          x = lo + (hi - lo) * (double)(g + 1) / (double)(P + 1);
+          active = hi - lo > tol && x > lo && x < hi;
+          cnt[t * P + g] = active ? sturm_count_less(dd, e2, n, x, pivmin) : -1;
+        }
+        if (!__syncthreads_or(active)) break;
+        if (mine && g == 0) {
+          const int idx = n - 1 - t;
+          const double lo = blo[t], hi = bhi[t];
+          // points are increasing; inactive ones (rounded onto an end of
+          // the bracket, or a converged bracket) carry no information
+          double nlo = lo, nhi = hi;
+          for (int q = 0; q < P; ++q) {
+            const int c = cnt[t * P + q];
+            if (c < 0) continue;
+            const double xq = lo + (hi - lo) * (double)(q + 1) / (double)(P + 1);
+            if (c > idx) {
+              nhi = xq;
+              break;
+            }
+            nlo = xq;
+          }
+          blo[t] = nlo;
+          bhi[t] = nhi;
+        }
+        __syncthreads();
+      }
+      for (int tt = tid; tt < kk; tt += nt) lam[tt] = 0.5 * (blo[tt] + bhi[tt]);
+    }
   }
   __syncthreads();
 
@@ -1986,7 +2038,7 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
   ctx.check_launch("k_chase");
   {
     const size_t smem = (3 * (size_t)nmax + 3 * (size_t)kkmax + 32) * sizeof(double) +
-                        (size_t)kkmax * sizeof(int) + 64;
+                        (size_t)std::max(kkmax, EIG_THREADS) * sizeof(int) + 64;
     smem_optin(k_steig, smem);
     ctx.launch_begin();
     k_steig<<<count, EIG_THREADS, smem, ctx.stream>>>(dd);
@@ -2029,6 +2081,8 @@ void eig_topk(Ctx& ctx, const std::vector<EigJob>& jobs_in) {
   Arena::Mark mk = ctx.arena.mark();
   std::vector<EigDev> dev(count);
   int nmax = 0, kkmax = 0;
+  const bool inline_gs =
+      std::getenv("HSVD_STEIG_INLINE_GS") && std::atoi(std::getenv("HSVD_STEIG_INLINE_GS")) != 0;
   for (int g = 0; g < count; ++g) {
     const EigJob& j = jobs[g];
     if (j.kk > j.n) throw Error(kInvalid, "eig_topk: kk > n");
@@ -2045,6 +2099,12 @@ void eig_topk(Ctx& ctx, const std::vector<EigJob>& jobs_in) {
     d.Z = j.Z;
     d.ldz = j.ldz;
     d.piv = ctx.arena.alloc_n<double>((size_t)j.n * j.kk);
+    // inverse iteration without the in-iteration Gram-Schmidt; clusters are
+    // orthonormalised once afterwards by the blocked k_band_mgs
+    // (HSVD_STEIG_INLINE_GS=1: dstein's per-iteration MGS inside k_steig)
+    d.shifts = ctx.arena.alloc_n<double>(j.kk);
+    d.cstarts = ctx.arena.alloc_n<int>(j.kk);
+    d.vals_only = inline_gs ? 0 : 2;
     const int nblk = std::max(1, ceil_div(j.n - 1, NBT));
     d.T = ctx.arena.alloc_n<double>((size_t)nblk * NBT * NBT);
     d.S = ctx.arena.alloc_n<double>((size_t)nblk * NBT * NBT);
@@ -2101,11 +2161,16 @@ void eig_topk(Ctx& ctx, const std::vector<EigJob>& jobs_in) {
   // 2. tridiagonal eigenpairs
   {
     const size_t smem = (3 * (size_t)nmax + 3 * (size_t)kkmax + 32) * sizeof(double) +
-                        (size_t)kkmax * sizeof(int) + 64;
+                        (size_t)std::max(kkmax, EIG_THREADS) * sizeof(int) + 64;
     smem_optin(k_steig, smem);
     ctx.launch_begin();
     k_steig<<<count, EIG_THREADS, smem, ctx.stream>>>(dd);
     ctx.check_launch("k_steig");
+    if (!inline_gs) {
+      ctx.launch_begin();
+      k_band_mgs<<<count, 256, 0, ctx.stream>>>(dd);
+      ctx.check_launch("k_band_mgs");
+    }
   }
   // 3. back-transform Z <- Q Z (blocks applied last to first)
   back_transform(ctx, jobs, dev, dd, nmax, 1);
