@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(NT) k_gemm(const GemmDesc* __restrict__ descs,
 // dimension contiguous in shared memory, so the copies are coalesced and
 // conflict-free and the address arithmetic is one increment per element.
 // ---------------------------------------------------------------------------
-constexpr int STAGES = 4;
+constexpr int STAGES = 3;
 
 __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool ok) {
   const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
