@@ -9,6 +9,7 @@
 //   kernels.hpp:12-26     DecompositionError, full_svd
 //   svd_factor.hpp:14-49  SvdFactor, MatConfig, validate, retained_count,
 //                         truncate_factor, reconstruct
+//   refine.hpp:9-21       RefineResult, refine_factors
 // DenseMatrix is an Eigen-free row-major real64 matrix with the accessors the
 // callers of the path use (rows(), cols(), data(), operator()); Eigen is not
 // available to this build.  std::invalid_argument and
@@ -304,6 +305,31 @@ inline SvdFactor recover_left_vectors(const DenseMatrix& x, const DenseMatrix& v
                                              x.cols(), x.cols(), HSVD_CU_HOST, v_r.data(),
                                              v_r.cols(), v_r.cols(), HSVD_CU_HOST, &r));
   return detail::take(r);
+}
+
+// refine.hpp:9-21 (Alg. 2).
+struct RefineResult {
+  SvdFactor factor;  // full (U, Sigma, V)
+  int iterations = 0;
+  double final_error = 0.0;  // last inter-iteration Sigma change
+  bool converged = false;
+};
+
+inline RefineResult refine_factors(const DenseMatrix& x, const DenseMatrix& v_hat,
+                                   const Vector& sigma_hat, double epsilon, int max_iters) {
+  hsvd_cu_result* r = nullptr;
+  std::int32_t it = 0, conv = 0;
+  double err = 0.0;
+  detail::check(hsvd_cu_refine_factors(
+      detail::ctx(), x.data(), HSVD_CU_F64, x.rows(), x.cols(), x.cols(), HSVD_CU_HOST,
+      v_hat.data(), v_hat.rows(), v_hat.cols(), v_hat.cols(), HSVD_CU_HOST, sigma_hat.data(),
+      static_cast<std::int64_t>(sigma_hat.size()), epsilon, max_iters, &it, &err, &conv, &r));
+  RefineResult out;
+  out.factor = detail::take(r);
+  out.iterations = it;
+  out.final_error = err;
+  out.converged = conv != 0;
+  return out;
 }
 
 }  // namespace hsvd

@@ -15,6 +15,7 @@
  *   hsvd_cu_merge_pair           hsvd::merge_pair_qr /       merge.hpp:19-30, merge.cpp:42-117
  *                                hsvd::merge_pair_naive
  *   hsvd_cu_full_svd             hsvd::full_svd              kernels.hpp:26, kernels.cpp:21-48
+ *   hsvd_cu_refine_factors       hsvd::refine_factors        refine.hpp:18-21, refine.cpp:26-72
  *
  * Matrices crossing the boundary use the reference's DenseMatrix layout:
  * row-major, real64 (fp32 is accepted for the input matrix X), leading
@@ -106,6 +107,17 @@ int hsvd_cu_hierarchical_svd(hsvd_cu_ctx* ctx, const void* x, int dtype, int64_t
 int hsvd_cu_recover_left_vectors(hsvd_cu_ctx* ctx, const void* x, int dtype, int64_t m, int64_t n,
                                  int64_t ldx, int where, const double* v_r, int64_t r,
                                  int64_t ldv, int v_where, hsvd_cu_result** out);
+
+/* hsvd::refine_factors (refine.hpp:18-21, refine.cpp:26-72; Alg. 2): v_hat
+ * (v_rows x r row-major, v_rows must equal n), sigma_hat (sigma_len = r, host).
+ * Result: (U, sigma, V); iterations, final_error (last relative sigma change)
+ * and converged as out parameters (non-convergence is not an error). */
+int hsvd_cu_refine_factors(hsvd_cu_ctx* ctx, const void* x, int dtype, int64_t m, int64_t n,
+                           int64_t ldx, int where, const double* v_hat, int64_t v_rows,
+                           int64_t r, int64_t ldv, int v_where, const double* sigma_hat,
+                           int64_t sigma_len, double epsilon, int32_t max_iters,
+                           int32_t* iterations, double* final_error, int32_t* converged,
+                           hsvd_cu_result** out);
 
 /* hierarchical_svd + recover_left_vectors with V_r kept on the device. */
 int hsvd_cu_rank_k_svd(hsvd_cu_ctx* ctx, const void* x, int dtype, int64_t m, int64_t n,

@@ -445,6 +445,68 @@ def recover_left_vectors(x: np.ndarray, v_r: np.ndarray) -> SvdFactor:
 
 
 # --------------------------------------------------------------------------
+# Refinement (refine.cpp, Alg. 2 of the paper) -- SURVEY 8(f) next #1
+# --------------------------------------------------------------------------
+
+@dataclass
+class RefineResult:
+    """refine.hpp:9-14."""
+    factor: SvdFactor
+    iterations: int = 0
+    final_error: float = 0.0
+    converged: bool = False
+
+
+def _padded_diff_norm(a: np.ndarray, b: np.ndarray) -> float:
+    """refine.cpp:13-22: ||a - b||_2 with the shorter vector zero-padded."""
+    n = max(a.shape[0], b.shape[0])
+    aa = np.zeros(n)
+    bb = np.zeros(n)
+    aa[:a.shape[0]] = a
+    bb[:b.shape[0]] = b
+    return float(math.sqrt(float(((aa - bb) ** 2).sum())))
+
+
+def refine_factors(x: np.ndarray, v_hat: np.ndarray, sigma_hat: np.ndarray,
+                   epsilon: float, max_iters: int) -> RefineResult:
+    """refine.cpp:26-72: alternate thin SVDs of X V and U_outer^T X until the
+    relative change of the singular-value vector is <= epsilon or max_iters
+    is reached (non-convergence is reported, not raised)."""
+    x = np.asarray(x, dtype=np.float64)
+    v_hat = np.asarray(v_hat, dtype=np.float64)
+    sigma_hat = np.asarray(sigma_hat, dtype=np.float64)
+    if not epsilon > 0.0:
+        raise ValueError("refine_factors: epsilon must be > 0")
+    if max_iters < 1:
+        raise ValueError("refine_factors: max_iters must be >= 1")
+    if sigma_hat.shape[0] != v_hat.shape[1]:
+        raise ValueError("refine_factors: sigma_hat length must match v_hat columns")
+    if v_hat.shape[0] != x.shape[1]:
+        raise ValueError("refine_factors: v_hat must have x.cols() rows")
+    defect = np.abs(v_hat.T @ v_hat - np.eye(v_hat.shape[1])).max()
+    if defect > 1e-6:
+        raise ValueError("refine_factors: v_hat columns are not orthonormal")
+    sigma = sigma_hat.copy()
+    v = v_hat
+    res = RefineResult(factor=SvdFactor(None, sigma, None))
+    error = 0.0
+    while True:
+        res.iterations += 1
+        u_outer = full_svd(x @ v).u                   # refine.cpp:50-51
+        step = full_svd(u_outer.T @ x)                 # refine.cpp:53
+        denom = float(np.linalg.norm(sigma))
+        diff = _padded_diff_norm(sigma, step.sigma)
+        error = diff / denom if denom > 0.0 else (math.inf if diff > 0.0 else 0.0)
+        sigma, v, u_inner = step.sigma, step.v, step.u
+        if not (error > epsilon and res.iterations < max_iters):
+            break
+    res.factor = SvdFactor(u=u_outer @ u_inner, sigma=sigma, v=v)
+    res.final_error = error
+    res.converged = error <= epsilon
+    return res
+
+
+# --------------------------------------------------------------------------
 # Generator (generate.cpp) -- spectrum + assembly from supplied Gaussians
 # --------------------------------------------------------------------------
 

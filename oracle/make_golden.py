@@ -32,7 +32,7 @@ def specs():
     out = []
     # generator cases: (m, n, seed)
     for m, n, seed in [(64, 32, 2024), (64, 32, 7), (256, 64, 620), (16, 8, 77),
-                       (40, 20, 9)]:
+                       (40, 20, 9), (512, 128, 820)]:
         out.append((f"lr_{m}x{n}_s{seed}", "lowrank", m, n, seed))
     # random_matrix cases used by test_hierarchy / test_kernels / test_merge
     mats = [(48, 32, 630), (40, 64, 456), (40, 16, 10000), (60, 30, 640),
@@ -67,6 +67,11 @@ def specs():
                  (18, 5, 6000 + t), (16, 3, 7000 + t), (16, 5, 8000 + t)]
     mats += [(12, 3, 9100), (12, 3, 9200), (12, 4, 9300), (12, 4, 9400),
              (5, 4, 9500), (5, 4, 9600), (10, 1, 9700), (10, 3, 9800)]
+    # test_refine.cpp
+    mats += [(24, 12, 800), (30, 15, 810), (5, 5, 811), (40, 18, 830), (50, 25, 840),
+             (30, 20, 860), (20, 10, 870), (10, 6, 880), (6, 2, 881)]
+    for t in range(50):
+        mats.append((24 + 4 * (t % 5), 12 + 2 * (t % 4), 850 + t))
     seen = set()
     for r, c, s in mats:
         key = f"m_{r}x{c}_s{s}"

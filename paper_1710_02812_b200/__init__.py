@@ -11,5 +11,5 @@ from .hsvd import (  # noqa: F401
     load_library, merge_pair_naive, merge_pair_qr, normalize_signs, partition,
     rank_k_svd, rank_k_svd_device, reconstruct, recover_left_vectors, retained_count, svd_of_col_slices,
     tree_merge, truncate_factor, validate, LIB_PATH, EXPORTED, ThreadGroup, nccl_unique_id,
-    shard_rows, rank_k_svd_sharded, syevx_topk,
+    shard_rows, rank_k_svd_sharded, syevx_topk, refine_factors, RefineResult,
 )

@@ -385,6 +385,36 @@ int hsvd_cu_recover_left_vectors(hsvd_cu_ctx* ctx, const void* x, int dtype, int
   });
 }
 
+int hsvd_cu_refine_factors(hsvd_cu_ctx* ctx, const void* x, int dtype, int64_t m, int64_t n,
+                           int64_t ldx, int where, const double* v_hat, int64_t v_rows,
+                           int64_t r, int64_t ldv, int v_where, const double* sigma_hat,
+                           int64_t sigma_len, double epsilon, int32_t max_iters,
+                           int32_t* iterations, double* final_error, int32_t* converged,
+                           hsvd_cu_result** out) {
+  return guarded([&] {
+    if (!out) throw Error(kInvalid, "out is null");
+    *out = nullptr;
+    // refine.cpp:29-36 (argument checks in the reference's order)
+    if (!(epsilon > 0.0)) throw Error(kInvalid, "refine_factors: epsilon must be > 0");
+    if (max_iters < 1) throw Error(kInvalid, "refine_factors: max_iters must be >= 1");
+    if (sigma_len != r || (r > 0 && !sigma_hat))
+      throw Error(kInvalid, "refine_factors: sigma_hat length must match v_hat columns");
+    if (v_rows != n || !v_hat || r < 1)
+      throw Error(kInvalid, "refine_factors: v_hat must have x.cols() rows");
+    begin(ctx);
+    XView xv = stage_x(ctx->c, x, dtype, m, n, ldx, where);
+    double* vd = stage_rowmajor(ctx->c, v_hat, n, r, ldv > 0 ? ldv : r, v_where);
+    std::vector<double> sh(sigma_hat, sigma_hat + r);
+    RefineStats st;
+    DFac f = refine_factors(ctx->c, xv, vd, n, (int)r, sh, epsilon, max_iters, &st);
+    if (iterations) *iterations = st.iterations;
+    if (final_error) *final_error = st.final_error;
+    if (converged) *converged = st.converged ? 1 : 0;
+    *out = make_result(ctx, f, true, true);
+    return HSVD_CU_OK;
+  });
+}
+
 int hsvd_cu_rank_k_svd(hsvd_cu_ctx* ctx, const void* x, int dtype, int64_t m, int64_t n,
                        int64_t ldx, int where, const hsvd_cu_config* cfg, hsvd_cu_result** out) {
   return guarded([&] {

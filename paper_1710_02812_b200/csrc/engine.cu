@@ -3,7 +3,9 @@
 // and merge.cpp; every dense step is one batched launch across all blocks /
 // pairs / row slices of a tree level.
 #include <algorithm>
+#include <cmath>
 #include <cstring>
+#include <limits>
 #include <string>
 
 #include "engine.h"
@@ -487,6 +489,119 @@ DFac recover_left_vectors(Ctx& ctx, const XView& x, const double* v_r, long long
   f.ld2 = n;
   f.dim2 = n;
   return f;
+}
+
+// refine.cpp:26-72 (Alg. 2): alternate thin SVDs of X V (left basis kept,
+// via recover_left_vectors) and of U_outer^T X (Gram of the r-side, eigen-
+// pairs, V = (X^T U_outer) Z / sigma, U_inner = Z), tracking the relative
+// change of sigma; the sigma vectors are read back each iteration (a few
+// hundred bytes) for the convergence test.
+DFac refine_factors(Ctx& ctx, const XView& x, const double* v_hat, long long ldv, int r,
+                    const std::vector<double>& sigma_hat, double epsilon, int max_iters,
+                    RefineStats* stats) {
+  const int m = static_cast<int>(x.m), n = static_cast<int>(x.n);
+  if (!(epsilon > 0.0)) throw Error(kInvalid, "refine_factors: epsilon must be > 0");
+  if (max_iters < 1) throw Error(kInvalid, "refine_factors: max_iters must be >= 1");
+  if ((int)sigma_hat.size() != r)
+    throw Error(kInvalid, "refine_factors: sigma_hat length must match v_hat columns");
+  {  // refine.cpp:37-42
+    double* H = ctx.arena.alloc_n<double>((size_t)r * r);
+    double* dd = ctx.arena.alloc_n<double>(1);
+    ctx.phase = "refine.check";
+    gemm_grouped(ctx, DType::F64, DType::F64, true, false, true,
+                 {{v_hat, v_hat, H, ldv, ldv, r, r, r, n, 1.0, 0.0}});
+    ortho_defect(ctx, H, r, r, dd);
+    double* hd = ctx.pinned_dbl(1);
+    HSVD_CUDA(cudaMemcpyAsync(hd, dd, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+    HSVD_CUDA(cudaStreamSynchronize(ctx.stream));
+    if (!(hd[0] <= 1e-6)) throw Error(kInvalid, "refine_factors: v_hat columns are not orthonormal");
+  }
+  std::vector<double> sigma = sigma_hat;
+  const double* V = v_hat;
+  long long ldV = ldv;
+  int rV = r;
+  DFac out;
+  double* Uo = nullptr;
+  double* Uin = nullptr;
+  int p = 0, kk = 0;
+  double error = 0.0;
+  int it = 0;
+  do {
+    ++it;
+    DFac L = recover_left_vectors(ctx, x, V, ldV, rV);  // left basis of X V
+    Uo = L.B;
+    p = L.rank;
+    kk = std::min(p, n);
+    double* Bt = ctx.arena.alloc_n<double>((size_t)n * p);
+    double* H = ctx.arena.alloc_n<double>((size_t)p * p);
+    double* lam = ctx.arena.alloc_n<double>(kk);
+    double* Z = ctx.arena.alloc_n<double>((size_t)p * kk);
+    double* P = ctx.arena.alloc_n<double>((size_t)n * kk);
+    double* Vn = ctx.arena.alloc_n<double>((size_t)n * kk);
+    double* sig = ctx.arena.alloc_n<double>(kk);
+    int* perm = ctx.arena.alloc_n<int>(kk);
+    double* Zp = ctx.arena.alloc_n<double>((size_t)p * kk);
+    int* d_rd = ctx.arena.alloc_n<int>(2);
+    ctx.phase = "refine.proj";  // B^T = X^T U_outer (n x p): Xt is n x m, ld x.ld
+    gemm_grouped(ctx, x.dt, DType::F64, false, false, false,
+                 {{x.X, Uo, Bt, x.ld, L.ld, n, n, p, m, 1.0, 0.0}});
+    ctx.phase = "refine.gram";
+    gemm_grouped(ctx, DType::F64, DType::F64, true, false, true,
+                 {{Bt, Bt, H, n, n, p, p, p, n, 1.0, 0.0}});
+    ctx.phase = "refine.eig";
+    eig_topk(ctx, {{H, p, p, kk, lam, Z, p}});
+    ctx.phase = "refine.back";
+    gemm_grouped(ctx, DType::F64, DType::F64, false, false, false,
+                 {{Bt, Z, P, n, p, n, n, kk, p, 1.0, 0.0}});
+    ctx.phase = "refine.fin";
+    finalize(ctx, {{P, n, n, kk, 0.0, 0, Vn, n, sig, perm, d_rd, d_rd + 1, 1}});
+    gather_cols(ctx, {{Zp, p, Z, p, p, kk, perm}});
+    std::vector<int> rd;
+    fetch_ranks(ctx, d_rd, 2, rd);
+    const int rk = std::max(1, std::min(kk, rd[0]));
+    std::vector<double> sn(rk);
+    double* hs = ctx.pinned_dbl(rk);
+    HSVD_CUDA(cudaMemcpyAsync(hs, sig, rk * sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+    HSVD_CUDA(cudaStreamSynchronize(ctx.stream));
+    std::memcpy(sn.data(), hs, rk * sizeof(double));
+    // refine.cpp:13-22, 55-57: padded difference relative to the old sigma
+    const size_t len = std::max(sigma.size(), sn.size());
+    double diff2 = 0.0, den2 = 0.0;
+    for (size_t i = 0; i < len; ++i) {
+      const double a = i < sigma.size() ? sigma[i] : 0.0, b = i < sn.size() ? sn[i] : 0.0;
+      diff2 += (a - b) * (a - b);
+    }
+    for (double a : sigma) den2 += a * a;
+    const double diff = std::sqrt(diff2), denom = std::sqrt(den2);
+    error = denom > 0.0 ? diff / denom
+                        : (diff > 0.0 ? std::numeric_limits<double>::infinity() : 0.0);
+    sigma = sn;
+    kk = rk;
+    V = reorthonormalize(ctx, Vn, n, n, kk);
+    ldV = n;
+    rV = kk;
+    Uin = Zp;
+    out.sigma = sig;
+    out.degenerate = rd[1] == 1;
+  } while (error > epsilon && it < max_iters);
+  // U = U_outer U_inner (m x kk)
+  double* U = ctx.arena.alloc_n<double>((size_t)m * kk);
+  ctx.phase = "refine.u";
+  gemm_grouped(ctx, DType::F64, DType::F64, false, false, false,
+               {{Uo, Uin, U, m, p, m, m, kk, p, 1.0, 0.0}});
+  out.B = U;
+  out.ld = m;
+  out.dim = m;
+  out.rank = kk;
+  out.B2 = const_cast<double*>(V);
+  out.ld2 = n;
+  out.dim2 = n;
+  if (stats) {
+    stats->iterations = it;
+    stats->final_error = error;
+    stats->converged = error <= epsilon;
+  }
+  return out;
 }
 
 }  // namespace hsvdcu

@@ -101,6 +101,16 @@ DFac svd_of_col_slices(Ctx& ctx, const XView& x, long long c, double gamma, int 
 // hierarchy.cpp:96-112 -> U (m x r) in B, V (n x r) in B2.
 DFac recover_left_vectors(Ctx& ctx, const XView& x, const double* v_r, long long ldv, int r);
 
+// refine.hpp:9-21 / refine.cpp:26-72 -> U in B (m x r), V in B2 (n x r).
+struct RefineStats {
+  int iterations = 0;
+  double final_error = 0.0;
+  bool converged = false;
+};
+DFac refine_factors(Ctx& ctx, const XView& x, const double* v_hat, long long ldv, int r,
+                    const std::vector<double>& sigma_hat, double epsilon, int max_iters,
+                    RefineStats* stats);
+
 // Reads back ranks / degenerate flags written by finalize (synchronises).
 void fetch_ranks(Ctx& ctx, const int* d_ranks, int count, std::vector<int>& out);
 

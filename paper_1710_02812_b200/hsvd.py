@@ -74,7 +74,7 @@ EXPORTED = [
     "hsvd_cu_result_device", "hsvd_cu_result_free",
     "hsvd_cu_nccl_unique_id", "hsvd_cu_ctx_init_nccl", "hsvd_cu_thread_group_create",
     "hsvd_cu_thread_group_free", "hsvd_cu_ctx_join_group", "hsvd_cu_shard_rows",
-    "hsvd_cu_rank_k_svd_sharded", "hsvd_cu_syevx_topk",
+    "hsvd_cu_rank_k_svd_sharded", "hsvd_cu_syevx_topk", "hsvd_cu_refine_factors",
 ]
 
 
@@ -110,6 +110,9 @@ def load_library(path: str = LIB_PATH):
         lib.hsvd_cu_hierarchical_svd.argtypes = xargs + [C.POINTER(_Config), pp]
         lib.hsvd_cu_rank_k_svd.argtypes = xargs + [C.POINTER(_Config), pp]
         lib.hsvd_cu_recover_left_vectors.argtypes = xargs + [P, I64, I64, I32, pp]
+        lib.hsvd_cu_refine_factors.argtypes = xargs + [P, I64, I64, I64, I32, P, I64, D, I32,
+                                                       C.POINTER(I32), C.POINTER(D),
+                                                       C.POINTER(I32), pp]
         lib.hsvd_cu_svd_of_col_slices.argtypes = xargs + [I64, D, I64, pp]
         lib.hsvd_cu_full_svd.argtypes = [P, P, I64, I64, I64, pp]
         lib.hsvd_cu_merge_pair.argtypes = [P, I32, C.POINTER(_FactorIn), C.POINTER(_FactorIn),
@@ -526,6 +529,37 @@ def recover_left_vectors(x, v_r, ctx: Optional[Context] = None) -> SvdFactor:
     _check(c.lib.hsvd_cu_recover_left_vectors(c.handle, p, dt, m, n, ld, where, vr.ctypes.data,
                                               vr.shape[1], vr.shape[1], HOST, C.byref(h)))
     return _result(c, h)
+
+
+@dataclass
+class RefineResult:
+    """hsvd::RefineResult (refine.hpp:9-14)."""
+    factor: SvdFactor
+    iterations: int = 0
+    final_error: float = 0.0
+    converged: bool = False
+
+
+def refine_factors(x, v_hat, sigma_hat, epsilon: float, max_iters: int,
+                   ctx: Optional[Context] = None) -> RefineResult:
+    """hsvd::refine_factors (refine.cpp:26-72, Alg. 2): alternate thin SVDs of
+    X V and U_outer^T X on the device until the relative sigma change is
+    <= epsilon or max_iters is reached; non-convergence is reported."""
+    c = _ctx(ctx)
+    p, dt, m, n, ld, where, _keep = _matrix_arg(x)
+    vh = np.ascontiguousarray(np.asarray(v_hat, dtype=np.float64))
+    sh = np.ascontiguousarray(np.asarray(sigma_hat, dtype=np.float64).reshape(-1))
+    if vh.ndim != 2:
+        raise ValueError("refine_factors: v_hat must have x.cols() rows")
+    it, err, conv = C.c_int(0), C.c_double(0.0), C.c_int(0)
+    h = C.c_void_p()
+    _check(c.lib.hsvd_cu_refine_factors(c.handle, p, dt, m, n, ld, where, vh.ctypes.data,
+                                        vh.shape[0], vh.shape[1], vh.shape[1], HOST,
+                                        sh.ctypes.data if sh.size else None, sh.shape[0],
+                                        float(epsilon), int(max_iters), C.byref(it),
+                                        C.byref(err), C.byref(conv), C.byref(h)))
+    return RefineResult(factor=_result(c, h), iterations=int(it.value),
+                        final_error=float(err.value), converged=bool(conv.value))
 
 
 def rank_k_svd(x, cfg: MatConfig, ctx: Optional[Context] = None, want_u: bool = True) -> SvdFactor:

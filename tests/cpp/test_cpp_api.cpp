@@ -63,6 +63,13 @@ int main() {
     for (Index j = 0; j < n; ++j) diff += (rec(i, j) - x(i, j)) * (rec(i, j) - x(i, j));
   CHECK(std::sqrt(diff) < 1e-10 * frobenius_norm(x));
 
+  // refinement (refine.hpp): exact subspace is a fixed point after one pass
+  const RefineResult rr = refine_factors(x, *right.v, right.sigma, 1e-6, 5);
+  CHECK(rr.converged && rr.iterations <= 2 && rr.factor.rank() == r);
+  for (Index t = 0; t < r; ++t) CHECK(std::abs(rr.factor.sigma[(size_t)t] - (5.0 - t)) < 1e-10);
+  CHECK(throws<std::invalid_argument>([&] { refine_factors(x, *right.v, right.sigma, 0.0, 5); }));
+  CHECK(throws<std::invalid_argument>([&] { refine_factors(x, *right.v, right.sigma, 1e-6, 0); }));
+
   // merges and the tree (merge.hpp / hierarchy.hpp)
   SvdFactor f1, f2;
   f1.u = DenseMatrix(4, 1);

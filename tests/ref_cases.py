@@ -523,6 +523,122 @@ def case_acceptance_merge_oracle(impl, golden, tol=None):
     assert worst <= 1e-9, worst
 
 
+# --------------------------------------------------------------------------
+# test_refine.cpp (refine_factors, Alg. 2 -- SURVEY 8(f) next #1)
+# --------------------------------------------------------------------------
+
+def case_refine_fixed_point(impl, golden, tol=None):
+    """test_refine.cpp:13-23."""
+    x = rm(golden, 24, 12, 800)
+    full = O.full_svd(x)
+    r = 4
+    res = impl.refine_factors(x, full.v[:, :r].copy(), full.sigma[:r].copy(), 1e-3, 10)
+    assert res.iterations == 1
+    assert res.converged
+    assert res.final_error <= 1e-12
+    assert np.abs(res.factor.sigma - full.sigma[:r]).max() < 1e-10 * full.sigma[0]
+
+
+def case_refine_rotated_subspace(impl, golden, tol=None):
+    """test_refine.cpp:25-36: the fixed point depends only on the span."""
+    x = rm(golden, 30, 15, 810)
+    full = O.full_svd(x)
+    r = 5
+    rotated = full.v[:, :r] @ ro(golden, r, r, 811)
+    res = impl.refine_factors(x, rotated, full.sigma[:r].copy(), 1e-10, 20)
+    assert res.converged
+    assert np.abs(res.factor.sigma - full.sigma[:r]).max() < 1e-10
+
+
+def case_refine_hierarchical_output(impl, golden, tol=None):
+    """test_refine.cpp:38-54."""
+    x, _ = lowrank(golden, 512, 128, 820, "exp", 25, ratio=0.7, floor=1e-6)
+    cfg = impl.MatConfig(gamma=1e-2, row_block_rows=128, col_block_cols=16)
+    right = impl.hierarchical_svd(x, cfg)
+    res = impl.refine_factors(x, right.v, right.sigma, 1e-3, 10)
+    assert res.converged
+    assert res.iterations <= 3
+
+
+def case_refine_sigma_bounded(impl, golden, tol=None):
+    """test_refine.cpp:56-67: refined sigma never exceeds the true ones."""
+    x = rm(golden, 40, 18, 830)
+    true_sigma = O.full_svd(x).sigma
+    right = impl.hierarchical_svd(x, impl.MatConfig(gamma=0.1, row_block_rows=10,
+                                                    col_block_cols=6))
+    res = impl.refine_factors(x, right.v, right.sigma, 1e-6, 10)
+    for i in range(res.factor.rank()):
+        assert res.factor.sigma[i] <= true_sigma[i] + 1e-10 * true_sigma[0]
+
+
+def case_refine_top_monotone(impl, golden, tol=None):
+    """test_refine.cpp:69-89: chained single iterations, sigma_1 grows."""
+    x = rm(golden, 50, 25, 840)
+    right = impl.hierarchical_svd(x, impl.MatConfig(gamma=0.2, row_block_rows=25,
+                                                    col_block_cols=5))
+    v, sigma = right.v, right.sigma
+    prev_top = sigma[0]
+    for _ in range(4):
+        res = impl.refine_factors(x, v, sigma, 1e-15, 1)
+        assert res.factor.sigma[0] >= prev_top - 1e-10 * prev_top
+        prev_top = res.factor.sigma[0]
+        v, sigma = res.factor.v, res.factor.sigma
+
+
+def case_refine_never_hurts(impl, golden, tol=None):
+    """test_refine.cpp:91-110 (50 trials)."""
+    checked = 0
+    for trial in range(50):
+        m, n = 24 + 4 * (trial % 5), 12 + 2 * (trial % 4)
+        x = rm(golden, m, n, 850 + trial)
+        cfg = impl.MatConfig(gamma=0.05 + 0.05 * (trial % 3), row_block_rows=m // 2,
+                             col_block_cols=n // 3)
+        right = impl.hierarchical_svd(x, cfg)
+        before = impl.recover_left_vectors(x, right.v)
+        res = impl.refine_factors(x, right.v, right.sigma, 1e-6, 10)
+        k = min(before.rank(), res.factor.rank())
+        full = O.full_svd(x)
+        err_before = O.rank_k_error(full, O.SvdFactor(before.u, before.sigma, before.v), k)
+        err_after = O.rank_k_error(full, O.SvdFactor(res.factor.u, res.factor.sigma,
+                                                     res.factor.v), k)
+        assert err_after <= err_before + _t(tol, "refine_never_hurts", 1e-12), trial
+        checked += 1
+    assert checked == 50
+
+
+def case_refine_orthonormal(impl, golden, tol=None):
+    """test_refine.cpp:112-122."""
+    x = rm(golden, 30, 20, 860)
+    right = impl.hierarchical_svd(x, impl.MatConfig(gamma=0.1, row_block_rows=15,
+                                                    col_block_cols=5))
+    res = impl.refine_factors(x, right.v, right.sigma, 1e-4, 10)
+    assert O.orthonormality_defect(res.factor.u) < 1e-8
+    assert O.orthonormality_defect(res.factor.v) < 1e-8
+
+
+def case_refine_nonconvergence(impl, golden, tol=None):
+    """test_refine.cpp:124-136: reported, not thrown."""
+    x = rm(golden, 20, 10, 870)
+    right = impl.hierarchical_svd(x, impl.MatConfig(gamma=0.5, row_block_rows=5,
+                                                    col_block_cols=2))
+    res = impl.refine_factors(x, right.v, right.sigma, 1e-300, 1)
+    assert res.iterations == 1
+    assert not res.converged
+    assert res.final_error > 0.0
+
+
+def case_refine_validation(impl, golden, tol=None):
+    """test_refine.cpp:138-150."""
+    x = rm(golden, 10, 6, 880)
+    full = O.full_svd(x)
+    v2 = full.v[:, :2].copy()
+    assert raises(ValueError, impl.refine_factors, x, v2, full.sigma[:3].copy(), 1e-3, 10)
+    assert raises(ValueError, impl.refine_factors, x, v2, full.sigma[:2].copy(), 0.0, 10)
+    assert raises(ValueError, impl.refine_factors, x, v2, full.sigma[:2].copy(), 1e-3, 0)
+    assert raises(ValueError, impl.refine_factors, x, rm(golden, 6, 2, 881),
+                  full.sigma[:2].copy(), 1e-3, 10)
+
+
 ALL_CASES = [
     case_merge_self_sqrt2, case_merge_orthogonal_units, case_naive_concat_oracle,
     case_identical_basis, case_orthogonal_union, case_qr_equals_naive_100,
@@ -533,4 +649,7 @@ ALL_CASES = [
     case_hsvd_no_inflation, case_recover_left, case_full_width_row_slices,
     case_rank_k_error_regression, case_cli_gen_svd, case_full_svd_kernels,
     case_acceptance_exactness, case_acceptance_merge_oracle,
+    case_refine_fixed_point, case_refine_rotated_subspace, case_refine_hierarchical_output,
+    case_refine_sigma_bounded, case_refine_top_monotone, case_refine_never_hurts,
+    case_refine_orthonormal, case_refine_nonconvergence, case_refine_validation,
 ]

@@ -104,3 +104,25 @@ def test_config_parity_with_oracle(name, eig, H, monkeypatch):
     err_got = np.linalg.norm(x64 - (got.u * got.sigma) @ got.v.T) / np.linalg.norm(x64)
     assert abs(err_got - err_ref) <= 1e-2 * err_ref
     assert O.orthonormality_defect(got.u) < 1e-8 and O.orthonormality_defect(got.v) < 1e-8
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+def test_refine_parity_with_oracle(dt, H):
+    """refine_factors (Alg. 2, refine.cpp:26-72) on hierarchical output at a
+    few-thousand scale: same iteration count and convergence, sigma and both
+    subspaces against the oracle (north-star tolerances)."""
+    m, n, r = 3000, 1200, 40
+    x = _synthetic(m, n, r, lambda i: np.exp(-0.08 * i), 1e-4, dt, seed=17102)
+    cfg = dict(gamma=1e-3, row_block_rows=750, col_block_cols=300, max_rank=30)
+    # both start from the same (oracle) hierarchical output
+    ref_right = O.hierarchical_svd(x, O.MatConfig(**cfg), workers=8)
+    got = H.refine_factors(x, ref_right.v, ref_right.sigma, 1e-9, 6)
+    ref = O.refine_factors(x.astype(np.float64), ref_right.v, ref_right.sigma, 1e-9, 6)
+    assert got.iterations == ref.iterations and got.converged == ref.converged
+    assert got.factor.rank() == ref.factor.rank()
+    rel = np.abs(got.factor.sigma - ref.factor.sigma) / ref.factor.sigma
+    assert rel.max() <= 1e-8, rel.max()
+    assert O.largest_principal_angle(ref.factor.v, got.factor.v) <= 1e-6
+    assert O.largest_principal_angle(ref.factor.u, got.factor.u) <= 1e-6
+    assert O.orthonormality_defect(got.factor.u) < 1e-8
+    assert O.orthonormality_defect(got.factor.v) < 1e-8
