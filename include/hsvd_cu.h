@@ -119,6 +119,32 @@ int hsvd_cu_refine_factors(hsvd_cu_ctx* ctx, const void* x, int dtype, int64_t m
                            int32_t* iterations, double* final_error, int32_t* converged,
                            hsvd_cu_result** out);
 
+/* ---- device evaluation of reconstruction errors -- */
+/* A factor with both sides: u (m x rank), sigma (rank), v (n x rank); host
+ * row-major (where = HSVD_CU_HOST, lds in elements) or device column-major
+ * (where = HSVD_CU_DEVICE, as returned by hsvd_cu_result_device). */
+typedef struct {
+  const double* u;
+  int64_t ldu;
+  const double* sigma;
+  const double* v;
+  int64_t ldv;
+  int64_t m, n, rank;
+  int32_t where;
+} hsvd_cu_factor_uv;
+
+/* bench.cpp:30-42 factor_diff_norm: ||U_a S_a V_a^T - U_b S_b V_b^T||_F,
+ * fused tiles, the m x n difference never stored. */
+int hsvd_cu_factor_diff_norm(hsvd_cu_ctx* ctx, const hsvd_cu_factor_uv* a,
+                             const hsvd_cu_factor_uv* b, double* out);
+/* svd_factor.hpp:61 / svd_factor.cpp:66-80 rank_k_error(full_of_x, approx, k):
+ * ||X_k - Xhat_k||_F / ||X_k||_F (same argument checks as the reference). */
+int hsvd_cu_rank_k_error(hsvd_cu_ctx* ctx, const hsvd_cu_factor_uv* full_of_x,
+                         const hsvd_cu_factor_uv* approx, int64_t k, double* out);
+/* ||X - U S V^T||_F for x (m x n row-major, fp32/fp64, host or device). */
+int hsvd_cu_residual_norm(hsvd_cu_ctx* ctx, const void* x, int dtype, int64_t m, int64_t n,
+                          int64_t ldx, int where, const hsvd_cu_factor_uv* f, double* out);
+
 /* hierarchical_svd + recover_left_vectors with V_r kept on the device. */
 int hsvd_cu_rank_k_svd(hsvd_cu_ctx* ctx, const void* x, int dtype, int64_t m, int64_t n,
                        int64_t ldx, int where, const hsvd_cu_config* cfg, hsvd_cu_result** out);

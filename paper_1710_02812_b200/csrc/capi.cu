@@ -8,6 +8,7 @@
 #include "comm.h"
 #include "engine.h"
 #include "factor_ops.h"
+#include "metrics.h"
 #include "syev.h"
 
 using namespace hsvdcu;
@@ -411,6 +412,126 @@ int hsvd_cu_refine_factors(hsvd_cu_ctx* ctx, const void* x, int dtype, int64_t m
     if (final_error) *final_error = st.final_error;
     if (converged) *converged = st.converged ? 1 : 0;
     *out = make_result(ctx, f, true, true);
+    return HSVD_CU_OK;
+  });
+}
+
+// ---- reconstruction-error evaluation ---------------
+namespace {
+
+struct UVDev {  // column-major device copy of (U S, V) heads, or views
+  const double* u;
+  long long ldu;
+  const double* v;
+  long long ldv;
+  const double* sigma;
+};
+
+void check_uv(const hsvd_cu_factor_uv* f, const char* who) {
+  if (!f || !f->u || !f->v || !f->sigma)
+    throw Error(kInvalid, std::string(who) + ": factor must carry both u and v");
+  if (f->m < 1 || f->n < 1 || f->rank < 1) throw Error(kInvalid, std::string(who) + ": empty factor");
+}
+
+UVDev stage_uv(Ctx& c, const hsvd_cu_factor_uv* f, long long k) {
+  UVDev d;
+  if (f->where == HSVD_CU_DEVICE) {
+    d.u = f->u;
+    d.ldu = f->ldu > 0 ? f->ldu : f->m;
+    d.v = f->v;
+    d.ldv = f->ldv > 0 ? f->ldv : f->n;
+    d.sigma = f->sigma;
+    return d;
+  }
+  // host row-major -> device column-major (the first k columns)
+  d.u = stage_rowmajor(c, f->u, f->m, k, f->ldu > 0 ? f->ldu : f->rank, HSVD_CU_HOST);
+  d.ldu = f->m;
+  d.v = stage_rowmajor(c, f->v, f->n, k, f->ldv > 0 ? f->ldv : f->rank, HSVD_CU_HOST);
+  d.ldv = f->n;
+  double* s = c.arena.alloc_n<double>(k);
+  HSVD_CUDA(cudaMemcpyAsync(s, f->sigma, k * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+  d.sigma = s;
+  return d;
+}
+
+// ||sum_i s_i * U_i S_i V_i^T (+ X)||_F^2 for up to two factor heads
+double heads_sumsq(Ctx& c, int m, int n, const UVDev& a, int ka, double sa, const UVDev* b, int kb,
+                   double sb, const void* X, DType dt, long long ldx) {
+  const int K = ka + (b ? kb : 0);
+  double* A = c.arena.alloc_n<double>((size_t)m * K);
+  double* B = c.arena.alloc_n<double>((size_t)n * K);
+  scale_cols_copy(c, A, m, a.u, a.ldu, m, ka, a.sigma, sa);
+  scale_cols_copy(c, B, n, a.v, a.ldv, n, ka, nullptr, 1.0);
+  if (b) {
+    scale_cols_copy(c, A + (size_t)m * ka, m, b->u, b->ldu, m, kb, b->sigma, sb);
+    scale_cols_copy(c, B + (size_t)n * ka, n, b->v, b->ldv, n, kb, nullptr, 1.0);
+  }
+  return product_plus_sumsq(c, A, m, B, n, m, n, K, X, dt, ldx);
+}
+
+}  // namespace
+
+int hsvd_cu_factor_diff_norm(hsvd_cu_ctx* ctx, const hsvd_cu_factor_uv* a,
+                             const hsvd_cu_factor_uv* b, double* out) {
+  return guarded([&] {
+    if (!out) throw Error(kInvalid, "out is null");
+    check_uv(a, "factor_diff_norm");
+    check_uv(b, "factor_diff_norm");
+    if (a->m != b->m || a->n != b->n)
+      throw Error(kInvalid, "factor_diff_norm: factors must describe matrices of the same shape");
+    begin(ctx);
+    Ctx& c = ctx->c;
+    c.phase = "metric";
+    const UVDev da = stage_uv(c, a, a->rank), db = stage_uv(c, b, b->rank);
+    *out = std::sqrt(heads_sumsq(c, (int)a->m, (int)a->n, da, (int)a->rank, 1.0, &db,
+                                 (int)b->rank, -1.0, nullptr, DType::F64, 0));
+    return HSVD_CU_OK;
+  });
+}
+
+int hsvd_cu_rank_k_error(hsvd_cu_ctx* ctx, const hsvd_cu_factor_uv* full_of_x,
+                         const hsvd_cu_factor_uv* approx, int64_t k, double* out) {
+  return guarded([&] {
+    if (!out) throw Error(kInvalid, "out is null");
+    if (!approx || !approx->u || !approx->v)
+      throw Error(kInvalid, "rank_k_error: approx must carry both u and v");
+    if (k < 1 || k > approx->rank)
+      throw Error(kInvalid, "rank_k_error: k must be in [1, approx.rank()]");
+    check_uv(full_of_x, "rank_k_error");
+    if (full_of_x->m != approx->m || full_of_x->n != approx->n)
+      throw Error(kInvalid, "rank_k_error: factors must describe matrices of the same shape");
+    begin(ctx);
+    Ctx& c = ctx->c;
+    c.phase = "metric";
+    const long long kref = std::min<long long>(k, full_of_x->rank);  // svd_factor.cpp:72
+    const UVDev df = stage_uv(c, full_of_x, kref), da = stage_uv(c, approx, k);
+    const int m = (int)approx->m, n = (int)approx->n;
+    // ||X_k||_F of the reconstructed reference head (svd_factor.cpp:73-74)
+    const double denom =
+        std::sqrt(heads_sumsq(c, m, n, df, (int)kref, 1.0, nullptr, 0, 0.0, nullptr, DType::F64, 0));
+    if (denom == 0.0)
+      throw Error(kInvalid, "rank_k_error: reference rank-k approximation is zero");
+    const double num = std::sqrt(heads_sumsq(c, m, n, df, (int)kref, 1.0, &da, (int)k, -1.0,
+                                             nullptr, DType::F64, 0));
+    *out = num / denom;
+    return HSVD_CU_OK;
+  });
+}
+
+int hsvd_cu_residual_norm(hsvd_cu_ctx* ctx, const void* x, int dtype, int64_t m, int64_t n,
+                          int64_t ldx, int where, const hsvd_cu_factor_uv* f, double* out) {
+  return guarded([&] {
+    if (!out) throw Error(kInvalid, "out is null");
+    check_uv(f, "residual_norm");
+    if (f->m != m || f->n != n)
+      throw Error(kInvalid, "residual_norm: factor shape does not match x");
+    begin(ctx);
+    Ctx& c = ctx->c;
+    c.phase = "metric";
+    XView xv = stage_x(c, x, dtype, m, n, ldx, where);
+    const UVDev d = stage_uv(c, f, f->rank);
+    *out = std::sqrt(heads_sumsq(c, (int)m, (int)n, d, (int)f->rank, -1.0, nullptr, 0, 0.0, xv.X,
+                                 xv.dt, xv.ld));
     return HSVD_CU_OK;
   });
 }

@@ -58,6 +58,12 @@ class _FactorIn(C.Structure):
                 ("degenerate", C.c_int32)]
 
 
+class _FactorUV(C.Structure):
+    _fields_ = [("u", C.c_void_p), ("ldu", C.c_int64), ("sigma", C.c_void_p),
+                ("v", C.c_void_p), ("ldv", C.c_int64), ("m", C.c_int64), ("n", C.c_int64),
+                ("rank", C.c_int64), ("where", C.c_int32)]
+
+
 _lib = None
 _lib_lock = threading.Lock()
 
@@ -75,6 +81,7 @@ EXPORTED = [
     "hsvd_cu_nccl_unique_id", "hsvd_cu_ctx_init_nccl", "hsvd_cu_thread_group_create",
     "hsvd_cu_thread_group_free", "hsvd_cu_ctx_join_group", "hsvd_cu_shard_rows",
     "hsvd_cu_rank_k_svd_sharded", "hsvd_cu_syevx_topk", "hsvd_cu_refine_factors",
+    "hsvd_cu_factor_diff_norm", "hsvd_cu_rank_k_error", "hsvd_cu_residual_norm",
 ]
 
 
@@ -110,6 +117,10 @@ def load_library(path: str = LIB_PATH):
         lib.hsvd_cu_hierarchical_svd.argtypes = xargs + [C.POINTER(_Config), pp]
         lib.hsvd_cu_rank_k_svd.argtypes = xargs + [C.POINTER(_Config), pp]
         lib.hsvd_cu_recover_left_vectors.argtypes = xargs + [P, I64, I64, I32, pp]
+        uv = C.POINTER(_FactorUV)
+        lib.hsvd_cu_factor_diff_norm.argtypes = [P, uv, uv, C.POINTER(D)]
+        lib.hsvd_cu_rank_k_error.argtypes = [P, uv, uv, I64, C.POINTER(D)]
+        lib.hsvd_cu_residual_norm.argtypes = xargs + [uv, C.POINTER(D)]
         lib.hsvd_cu_refine_factors.argtypes = xargs + [P, I64, I64, I64, I32, P, I64, D, I32,
                                                        C.POINTER(I32), C.POINTER(D),
                                                        C.POINTER(I32), pp]
@@ -560,6 +571,58 @@ def refine_factors(x, v_hat, sigma_hat, epsilon: float, max_iters: int,
                                         C.byref(err), C.byref(conv), C.byref(h)))
     return RefineResult(factor=_result(c, h), iterations=int(it.value),
                         final_error=float(err.value), converged=bool(conv.value))
+
+
+# ---- device evaluation of reconstruction errors -----
+
+def _uv(f: SvdFactor, who: str):
+    """(struct, keep-alive arrays) for a host factor with both sides."""
+    if f.u is None or f.v is None:
+        raise ValueError(f"{who}: factor must carry both u and v")
+    u = np.ascontiguousarray(np.asarray(f.u, dtype=np.float64))
+    v = np.ascontiguousarray(np.asarray(f.v, dtype=np.float64))
+    s = np.ascontiguousarray(np.asarray(f.sigma, dtype=np.float64).reshape(-1))
+    st = _FactorUV(u.ctypes.data, u.shape[1], s.ctypes.data, v.ctypes.data, v.shape[1],
+                   u.shape[0], v.shape[0], s.shape[0], HOST)
+    return st, (u, v, s)
+
+
+def factor_diff_norm(a: SvdFactor, b: SvdFactor, ctx: Optional[Context] = None) -> float:
+    """bench.cpp:30-42: ||U_a S_a V_a^T - U_b S_b V_b^T||_F on the device (fused
+    tiles; the m x n difference is never stored)."""
+    c = _ctx(ctx)
+    sa, ka = _uv(a, "factor_diff_norm")
+    sb, kb = _uv(b, "factor_diff_norm")
+    out = C.c_double(0.0)
+    _check(c.lib.hsvd_cu_factor_diff_norm(c.handle, C.byref(sa), C.byref(sb), C.byref(out)))
+    return float(out.value)
+
+
+def rank_k_error(full_of_x_or_x, approx: SvdFactor, k: int,
+                 ctx: Optional[Context] = None) -> float:
+    """hsvd::rank_k_error (svd_factor.cpp:66-83): ||X_k - Xhat_k||_F / ||X_k||_F,
+    evaluated on the device.  The first argument is the full SVD of X or X
+    itself (then decomposed by full_svd first, as the reference does)."""
+    c = _ctx(ctx)
+    if approx.u is None or approx.v is None:
+        raise ValueError("rank_k_error: approx must carry both u and v")
+    full = full_of_x_or_x if isinstance(full_of_x_or_x, SvdFactor) else full_svd(full_of_x_or_x, c)
+    sf, kf = _uv(full, "rank_k_error")
+    sa, ka = _uv(approx, "rank_k_error")
+    out = C.c_double(0.0)
+    _check(c.lib.hsvd_cu_rank_k_error(c.handle, C.byref(sf), C.byref(sa), int(k), C.byref(out)))
+    return float(out.value)
+
+
+def residual_norm(x, f: SvdFactor, ctx: Optional[Context] = None) -> float:
+    """||X - U S V^T||_F on the device (x host/device, fp32/fp64)."""
+    c = _ctx(ctx)
+    p, dt, m, n, ld, where, _keep = _matrix_arg(x)
+    sf, kf = _uv(f, "residual_norm")
+    out = C.c_double(0.0)
+    _check(c.lib.hsvd_cu_residual_norm(c.handle, p, dt, m, n, ld, where, C.byref(sf),
+                                       C.byref(out)))
+    return float(out.value)
 
 
 def rank_k_svd(x, cfg: MatConfig, ctx: Optional[Context] = None, want_u: bool = True) -> SvdFactor:
