@@ -26,7 +26,8 @@
  * Every function returns HSVD_CU_OK or an error code; hsvd_cu_last_error()
  * returns the thread-local message (HSVD_CU_EINVAL <-> std::invalid_argument,
  * HSVD_CU_EDECOMP <-> hsvd::DecompositionError with rows/cols from
- * hsvd_cu_last_error_dims()).  There is no CPU fallback: without a CUDA
+ * hsvd_cu_last_error_dims(), HSVD_CU_EIO / HSVD_CU_EFORMAT <-> hsvd::IoError /
+ * hsvd::FormatError of the matrix loader).  There is no CPU fallback: without a CUDA
  * device every compute entry point fails with HSVD_CU_ECUDA.
  */
 #ifndef HSVD_CU_H_
@@ -47,7 +48,9 @@ enum {
   HSVD_CU_EDECOMP = 2,
   HSVD_CU_ECUDA = 3,
   HSVD_CU_ENCCL = 4,
-  HSVD_CU_ENOMEM = 5
+  HSVD_CU_ENOMEM = 5,
+  HSVD_CU_EIO = 6,     /* hsvd::IoError (matrix_io.hpp) */
+  HSVD_CU_EFORMAT = 7  /* hsvd::FormatError (matrix_io.hpp) */
 };
 enum { HSVD_CU_F32 = 0, HSVD_CU_F64 = 1 };
 enum { HSVD_CU_COLUMN_CONCAT = 0, HSVD_CU_ROW_CONCAT = 1 };
@@ -144,6 +147,18 @@ int hsvd_cu_rank_k_error(hsvd_cu_ctx* ctx, const hsvd_cu_factor_uv* full_of_x,
 /* ||X - U S V^T||_F for x (m x n row-major, fp32/fp64, host or device). */
 int hsvd_cu_residual_norm(hsvd_cu_ctx* ctx, const void* x, int dtype, int64_t m, int64_t n,
                           int64_t ldx, int where, const hsvd_cu_factor_uv* f, double* out);
+
+/* ---- HSVD1 input streamed to the device --------- */
+/* load_hsvd1 (matrix_io.cpp:14-15, 91-113): 22-byte header ("HSVD1\0", u64
+ * little-endian rows, u64 cols) and an fp64 row-major payload, streamed in
+ * chunks through pinned double buffers straight into device memory owned by
+ * the context (kept until the next load or the context's destruction, so it
+ * can be passed with HSVD_CU_DEVICE to the calls above).  Same checks and
+ * messages as the reference: EIO "cannot open", EFORMAT truncated header /
+ * bad magic / empty / implausible dimensions / truncated payload / NaN or
+ * Inf (the finiteness check runs on the device). */
+int hsvd_cu_load_hsvd1(hsvd_cu_ctx* ctx, const char* path, int64_t* rows, int64_t* cols,
+                       const double** dev_x);
 
 /* hierarchical_svd + recover_left_vectors with V_r kept on the device. */
 int hsvd_cu_rank_k_svd(hsvd_cu_ctx* ctx, const void* x, int dtype, int64_t m, int64_t n,

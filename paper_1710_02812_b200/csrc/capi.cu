@@ -1,6 +1,10 @@
 // C ABI (include/hsvd_cu.h) over the device engine.
+#include <algorithm>
 #include <cmath>
+#include <cstdint>
+#include <cstdio>
 #include <cstring>
+#include <memory>
 #include <new>
 #include <string>
 
@@ -17,6 +21,12 @@ struct hsvd_cu_ctx {
   Ctx c;
   long long generation = 0;
   std::unique_ptr<Comm> comm;
+  // matrix loaded by hsvd_cu_load_hsvd1 (outside the per-call arena)
+  double* loaded = nullptr;
+  size_t loaded_cap = 0;
+  ~hsvd_cu_ctx() {
+    if (loaded) cudaFree(loaded);
+  }
 };
 
 struct hsvd_cu_group {
@@ -532,6 +542,105 @@ int hsvd_cu_residual_norm(hsvd_cu_ctx* ctx, const void* x, int dtype, int64_t m,
     const UVDev d = stage_uv(c, f, f->rank);
     *out = std::sqrt(heads_sumsq(c, (int)m, (int)n, d, (int)f->rank, -1.0, nullptr, 0, 0.0, xv.X,
                                  xv.dt, xv.ld));
+    return HSVD_CU_OK;
+  });
+}
+
+// ---- HSVD1 loader (matrix_io.cpp:91-113), streamed to the device ---------
+namespace {
+
+__global__ void k_all_finite(const double* __restrict__ x, long long count, int* __restrict__ bad) {
+  int b = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+       i += (long long)gridDim.x * blockDim.x)
+    b |= !isfinite(x[i]);
+  if (__syncthreads_or(b) && threadIdx.x == 0) atomicOr(bad, 1);
+}
+
+}  // namespace
+
+int hsvd_cu_load_hsvd1(hsvd_cu_ctx* ctx, const char* path, int64_t* rows, int64_t* cols,
+                       const double** dev_x) {
+  return guarded([&] {
+    if (!ctx || !path || !rows || !cols || !dev_x) throw Error(kInvalid, "null argument");
+    const std::string p(path);
+    std::FILE* f = std::fopen(path, "rb");
+    if (!f) throw Error(kIo, p + ": cannot open for reading");
+    std::unique_ptr<std::FILE, int (*)(std::FILE*)> guard(f, &std::fclose);
+    unsigned char header[22];
+    if (std::fread(header, 1, sizeof(header), f) != sizeof(header))
+      throw Error(kFormat, p + ": truncated header");
+    static const char kMagic[6] = {'H', 'S', 'V', 'D', '1', '\0'};
+    if (std::memcmp(header, kMagic, sizeof(kMagic)) != 0)
+      throw Error(kFormat, p + ": bad magic, not an HSVD1 file");
+    auto u64 = [&](int off) {
+      std::uint64_t v = 0;
+      for (int i = 0; i < 8; ++i) v |= static_cast<std::uint64_t>(header[off + i]) << (8 * i);
+      return v;
+    };
+    const std::uint64_t r = u64(6), c = u64(14);
+    if (r == 0 || c == 0) throw Error(kFormat, p + ": empty matrix");
+    constexpr std::uint64_t kMaxElems = std::uint64_t(1) << 34;
+    if (r > kMaxElems || c > kMaxElems || r * c > kMaxElems)
+      throw Error(kFormat, p + ": implausible dimensions");
+    Ctx& cx = ctx->c;
+    HSVD_CUDA(cudaSetDevice(cx.device));
+    const size_t count = (size_t)(r * c), bytes = count * sizeof(double);
+    if (ctx->loaded_cap < bytes) {
+      if (ctx->loaded) HSVD_CUDA(cudaFree(ctx->loaded));
+      ctx->loaded = nullptr;
+      ctx->loaded_cap = 0;
+      if (cudaMalloc(&ctx->loaded, bytes) != cudaSuccess) {
+        (void)cudaGetLastError();
+        throw Error(kNoMemory, p + ": device allocation for the matrix failed");
+      }
+      ctx->loaded_cap = bytes;
+    }
+    // two pinned chunks: the file read of one overlaps the copy of the other
+    constexpr size_t kChunk = size_t(64) << 20;
+    void* pin[2] = {nullptr, nullptr};
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    auto cleanup = [&] {
+      for (int i = 0; i < 2; ++i) {
+        if (ev[i]) cudaEventDestroy(ev[i]);
+        if (pin[i]) cudaFreeHost(pin[i]);
+      }
+    };
+    try {
+      for (int i = 0; i < 2; ++i) {
+        HSVD_CUDA(cudaMallocHost(&pin[i], kChunk));
+        HSVD_CUDA(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+      }
+      char* dst = reinterpret_cast<char*>(ctx->loaded);
+      size_t done = 0;
+      int b = 0;
+      while (done < bytes) {
+        const size_t len = std::min(kChunk, bytes - done);
+        HSVD_CUDA(cudaEventSynchronize(ev[b]));  // this buffer's previous copy is done
+        if (std::fread(pin[b], 1, len, f) != len) throw Error(kFormat, p + ": truncated payload");
+        HSVD_CUDA(cudaMemcpyAsync(dst + done, pin[b], len, cudaMemcpyHostToDevice, cx.stream));
+        HSVD_CUDA(cudaEventRecord(ev[b], cx.stream));
+        done += len;
+        b ^= 1;
+      }
+      int* bad = nullptr;
+      HSVD_CUDA(cudaMalloc(&bad, sizeof(int)));
+      HSVD_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), cx.stream));
+      k_all_finite<<<4 * cx.num_sms, 256, 0, cx.stream>>>(ctx->loaded, (long long)count, bad);
+      int hb = 0;
+      HSVD_CUDA(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, cx.stream));
+      HSVD_CUDA(cudaStreamSynchronize(cx.stream));
+      cudaFree(bad);
+      if (hb) throw Error(kFormat, p + ": matrix contains NaN or Inf");
+    } catch (...) {
+      cudaStreamSynchronize(cx.stream);
+      cleanup();
+      throw;
+    }
+    cleanup();
+    *rows = (int64_t)r;
+    *cols = (int64_t)c;
+    *dev_x = ctx->loaded;
     return HSVD_CU_OK;
   });
 }

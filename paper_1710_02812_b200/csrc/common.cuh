@@ -17,6 +17,8 @@ enum Status : int {
   kCuda = 3,
   kNccl = 4,
   kNoMemory = 5,
+  kIo = 6,      // hsvd::IoError in the reference (matrix_io.hpp)
+  kFormat = 7,  // hsvd::FormatError in the reference (matrix_io.hpp)
 };
 
 struct Error : std::runtime_error {

@@ -25,7 +25,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libhsvd_b200.so")
 
-OK, EINVAL, EDECOMP, ECUDA, ENCCL, ENOMEM = range(6)
+OK, EINVAL, EDECOMP, ECUDA, ENCCL, ENOMEM, EIO, EFORMAT = range(8)
 F32, F64 = 0, 1
 HOST, DEVICE = 0, 1
 COLUMN_CONCAT = "ColumnConcat"
@@ -44,6 +44,14 @@ class DecompositionError(RuntimeError):
 
 class HsvdCudaError(RuntimeError):
     """CUDA / NCCL / allocation failure inside the library."""
+
+
+class IoError(RuntimeError):
+    """hsvd::IoError (matrix_io.hpp): a matrix file cannot be opened."""
+
+
+class FormatError(RuntimeError):
+    """hsvd::FormatError (matrix_io.hpp): malformed matrix file."""
 
 
 class _Config(C.Structure):
@@ -82,6 +90,7 @@ EXPORTED = [
     "hsvd_cu_thread_group_free", "hsvd_cu_ctx_join_group", "hsvd_cu_shard_rows",
     "hsvd_cu_rank_k_svd_sharded", "hsvd_cu_syevx_topk", "hsvd_cu_refine_factors",
     "hsvd_cu_factor_diff_norm", "hsvd_cu_rank_k_error", "hsvd_cu_residual_norm",
+    "hsvd_cu_load_hsvd1",
 ]
 
 
@@ -117,6 +126,7 @@ def load_library(path: str = LIB_PATH):
         lib.hsvd_cu_hierarchical_svd.argtypes = xargs + [C.POINTER(_Config), pp]
         lib.hsvd_cu_rank_k_svd.argtypes = xargs + [C.POINTER(_Config), pp]
         lib.hsvd_cu_recover_left_vectors.argtypes = xargs + [P, I64, I64, I32, pp]
+        lib.hsvd_cu_load_hsvd1.argtypes = [P, C.c_char_p, C.POINTER(I64), C.POINTER(I64), pp]
         uv = C.POINTER(_FactorUV)
         lib.hsvd_cu_factor_diff_norm.argtypes = [P, uv, uv, C.POINTER(D)]
         lib.hsvd_cu_rank_k_error.argtypes = [P, uv, uv, I64, C.POINTER(D)]
@@ -161,6 +171,10 @@ def _raise(code: int):
         r, c = C.c_int64(), C.c_int64()
         lib.hsvd_cu_last_error_dims(C.byref(r), C.byref(c))
         raise DecompositionError(msg, r.value, c.value)
+    if code == EIO:
+        raise IoError(msg)
+    if code == EFORMAT:
+        raise FormatError(msg)
     raise HsvdCudaError(f"[{code}] {msg}")
 
 
@@ -445,7 +459,10 @@ def default_context() -> Context:
 # --------------------------------------------------------------------------
 
 def _matrix_arg(x):
-    """(pointer, dtype code, m, n, ld, where, keepalive) for numpy / torch."""
+    """(pointer, dtype code, m, n, ld, where, keepalive) for numpy / torch /
+    a DeviceMatrix from load_hsvd1."""
+    if isinstance(x, DeviceMatrix):
+        return (x.ptr, F64, x.shape[0], x.shape[1], x.shape[1], DEVICE, x)
     mod = type(x).__module__
     if mod.startswith("torch"):
         if x.dim() != 2:
@@ -571,6 +588,38 @@ def refine_factors(x, v_hat, sigma_hat, epsilon: float, max_iters: int,
                                         C.byref(err), C.byref(conv), C.byref(h)))
     return RefineResult(factor=_result(c, h), iterations=int(it.value),
                         final_error=float(err.value), converged=bool(conv.value))
+
+
+# ---- HSVD1 input streamed to the device -------------
+
+class DeviceMatrix:
+    """A matrix resident in device memory owned by a context (the last
+    load_hsvd1); accepted wherever a matrix is (passed as HSVD_CU_DEVICE)."""
+
+    def __init__(self, ctx: "Context", ptr: int, rows: int, cols: int):
+        self.ctx, self.ptr, self.shape = ctx, ptr, (rows, cols)
+
+
+def load_hsvd1(path: str, ctx: Optional[Context] = None) -> DeviceMatrix:
+    """matrix_io.cpp:91-113 load_hsvd1, streamed straight to the device (IoError /
+    FormatError with the reference's messages)."""
+    c = _ctx(ctx)
+    r, k = C.c_int64(), C.c_int64()
+    ptr = C.c_void_p()
+    _check(c.lib.hsvd_cu_load_hsvd1(c.handle, os.fsencode(path), C.byref(r), C.byref(k),
+                                    C.byref(ptr)))
+    return DeviceMatrix(c, ptr.value, int(r.value), int(k.value))
+
+
+def save_hsvd1(x, path: str) -> None:
+    """matrix_io.cpp:115-127 save_hsvd1 (host writer, for tests and the CLI)."""
+    a = np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+    if a.ndim == 1:
+        a = a.reshape(-1, 1)
+    with open(path, "wb") as f:
+        f.write(b"HSVD1\0" + int(a.shape[0]).to_bytes(8, "little") +
+                int(a.shape[1]).to_bytes(8, "little"))
+        f.write(a.tobytes())
 
 
 # ---- device evaluation of reconstruction errors (SURVEY 8(f) next #2) -----
