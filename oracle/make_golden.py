@@ -32,7 +32,10 @@ def specs():
     out = []
     # generator cases: (m, n, seed)
     for m, n, seed in [(64, 32, 2024), (64, 32, 7), (256, 64, 620), (16, 8, 77),
-                       (40, 20, 9), (512, 128, 820)]:
+                       (40, 20, 9), (512, 128, 820),
+                       # test_bench.cpp sharp_decay_matrix fixtures
+                       (64, 32, 4000), (96, 48, 4100), (32, 16, 4200), (16, 8, 4300),
+                       (48, 24, 4400), (32, 16, 4500), (16, 8, 4600), (16, 8, 4700)]:
         out.append((f"lr_{m}x{n}_s{seed}", "lowrank", m, n, seed))
     # random_matrix cases used by test_hierarchy / test_kernels / test_merge
     mats = [(48, 32, 630), (40, 64, 456), (40, 16, 10000), (60, 30, 640),
