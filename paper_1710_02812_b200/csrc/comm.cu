@@ -40,11 +40,16 @@ NcclApi& nccl() {
   static NcclApi api;
   static std::once_flag once;
   std::call_once(once, [] {
-    const char* env = std::getenv("HSVD_NCCL_LIB");
-    const char* names[] = {env ? env : "libnccl.so.2", "libnccl.so.2", "libnccl.so"};
+    // 1. HSVD_NCCL_LIB; 2. an NCCL the process already has (torch's); 3. the
+    // default search.  Whatever is loaded first owns the soname libnccl.so.2
+    // for the process, so the Python layer points HSVD_NCCL_LIB at the NCCL
+    // torch is built against (an older system NCCL would break torch's import).
+    if (const char* env = std::getenv("HSVD_NCCL_LIB")) api.h = dlopen(env, RTLD_NOW | RTLD_LOCAL);
+    if (!api.h) api.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
     for (const char* nm : names) {
-      api.h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
       if (api.h) break;
+      api.h = dlopen(nm, RTLD_NOW | RTLD_LOCAL);
     }
     if (!api.h) return;
 #define LOAD(f) api.f = reinterpret_cast<decltype(api.f)>(dlsym(api.h, "nccl" #f))

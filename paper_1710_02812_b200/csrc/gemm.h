@@ -25,7 +25,6 @@ struct GemmDesc {
 // flags for gemm_grouped
 enum : int {
   kGemmLowerOnly = 1,  // with syrk: write the lower tile triangle only (no mirror)
-  kGemmSymA = 2,       // op(A) = A is symmetric and only its lower triangle is read
 };
 
 // syrk=true: op(A) op(B) is known symmetric (op(B) == op(A)^T); only the

@@ -94,8 +94,27 @@ EXPORTED = [
 ]
 
 
+def _prefer_bundled_nccl():
+    """Points HSVD_NCCL_LIB at the NCCL wheel torch is linked against (the
+    library dlopens NCCL lazily; loading an older system libnccl.so.2 first
+    would claim the soname and break a later `import torch`)."""
+    if os.environ.get("HSVD_NCCL_LIB"):
+        return
+    try:
+        import importlib.util
+        spec = importlib.util.find_spec("nvidia")
+        for base in (spec.submodule_search_locations or []) if spec else []:
+            cand = os.path.join(base, "nccl", "lib", "libnccl.so.2")
+            if os.path.exists(cand):
+                os.environ["HSVD_NCCL_LIB"] = cand
+                return
+    except Exception:  # pragma: no cover -- optional
+        pass
+
+
 def load_library(path: str = LIB_PATH):
     """Loads libhsvd_b200.so (raises if it has not been built)."""
+    _prefer_bundled_nccl()
     global _lib
     with _lib_lock:
         if _lib is not None:
