@@ -1242,21 +1242,21 @@ __global__ void __launch_bounds__(CHASE_WARPS * 32, 1) k_chase(const EigDev* __r
 
 // Eigenvectors of the band matrix from those of its tridiagonal: Z <- Q2 Z
 // with Q2 the product of the chase reflectors in chase order, applied in
-// reverse (LAPACK dsbtrd's Q, applied as dormtr would).  One CTA per 32
-// eigenvectors of a matrix on a row-major n x 32 scratch copy (lane =
-// column: every row access is one coalesced 256-byte line).  The reflectors
+// reverse (LAPACK dsbtrd's Q, applied as dormtr would).  One CTA per 16
+// eigenvectors of a matrix on a row-major n x 16 scratch copy (lane =
+// column x row parity: every warp access is two adjacent 128-byte rows).  The reflectors
 // of one sweep touch disjoint 32-row blocks: the CTA's warps share a sweep's
 // blocks, each prefetching its next block's rows while it applies the
 // current one, and synchronise once per sweep; the sweep's reflectors are
 // staged into shared memory by cp.async one sweep ahead.
-constexpr int Q2_COLS = 32, Q2_WARPS = 8;
+constexpr int Q2_COLS = 16, Q2_WARPS = 8, Q2_ROWS = B2 / 2;  // rows per lane
 
 __device__ __forceinline__ void q2_cp8(double* dst, const double* src) {
   const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src));
 }
 
-__global__ void __launch_bounds__(Q2_WARPS * 32, 1) k_q2_apply(const EigDev* __restrict__ jobs) {
+__global__ void __launch_bounds__(Q2_WARPS * 32, 2) k_q2_apply(const EigDev* __restrict__ jobs) {
   const EigDev J = jobs[blockIdx.y];
   const int n = J.n, kk = J.kk;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nt = blockDim.x;
@@ -1289,40 +1289,43 @@ __global__ void __launch_bounds__(Q2_WARPS * 32, 1) k_q2_apply(const EigDev* __r
     __syncthreads();
     const double* rb = rbuf + (size_t)buf * kmax * (B2 + 1);
     const int K = sweep_steps(n, s);
-    double zn[B2];
+    // lane = column (lane & 15) x row parity (lane >> 4): a warp instruction
+    // reads two adjacent 128-byte rows
+    const int q = lane & (Q2_COLS - 1), h = lane >> 4;
+    double zn[Q2_ROWS];
     auto fetch = [&](int k) {
       const int r0 = s + 1 + k * B2, L = min(B2, n - r0);
-      const double* zb = S + (size_t)r0 * Q2_COLS + lane;
+      const double* zb = S + (size_t)(r0 + h) * Q2_COLS + q;
 #pragma unroll
-      for (int i = 0; i < B2; ++i) zn[i] = i < L ? zb[i * Q2_COLS] : 0.0;
+      for (int j = 0; j < Q2_ROWS; ++j) zn[j] = 2 * j + h < L ? zb[2 * j * Q2_COLS] : 0.0;
     };
     if (warp < K) fetch(warp);
     for (int k = warp; k < K; k += Q2_WARPS) {
-      double z[B2];
+      double z[Q2_ROWS];
 #pragma unroll
-      for (int i = 0; i < B2; ++i) z[i] = zn[i];
+      for (int j = 0; j < Q2_ROWS; ++j) z[j] = zn[j];
       if (k + Q2_WARPS < K) fetch(k + Q2_WARPS);  // disjoint rows of the same sweep
       const double* rv = rb + k * (B2 + 1);
       const double tau = rv[B2];
       if (tau == 0.0) continue;
       const int r0 = s + 1 + k * B2, L = min(B2, n - r0);
-      double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+      double d0 = 0.0, d1 = 0.0;
 #pragma unroll
-      for (int i = 0; i < B2; i += 4) {
-        d0 += rv[i] * z[i];
-        d1 += rv[i + 1] * z[i + 1];
-        d2 += rv[i + 2] * z[i + 2];
-        d3 += rv[i + 3] * z[i + 3];
+      for (int j = 0; j < Q2_ROWS; j += 2) {
+        d0 += rv[2 * j + h] * z[j];
+        d1 += rv[2 * j + 2 + h] * z[j + 1];
       }
-      const double dot = tau * ((d0 + d1) + (d2 + d3));
+      double dot = d0 + d1;
+      dot += __shfl_xor_sync(0xffffffffu, dot, 16);  // the other row parity
+      dot *= tau;
       // all shared-memory reads of v before the global stores (a store could
       // alias shared memory as far as the compiler knows)
 #pragma unroll
-      for (int i = 0; i < B2; ++i) z[i] -= dot * rv[i];
-      double* zb = S + (size_t)r0 * Q2_COLS + lane;
+      for (int j = 0; j < Q2_ROWS; ++j) z[j] -= dot * rv[2 * j + h];
+      double* zb = S + (size_t)(r0 + h) * Q2_COLS + q;
 #pragma unroll
-      for (int i = 0; i < B2; ++i)
-        if (i < L) zb[i * Q2_COLS] = z[i];
+      for (int j = 0; j < Q2_ROWS; ++j)
+        if (2 * j + h < L) zb[2 * j * Q2_COLS] = z[j];
     }
     __syncthreads();  // next sweep: rows overlap, and this buffer is restaged
   }
