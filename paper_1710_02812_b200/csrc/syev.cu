@@ -1242,98 +1242,100 @@ __global__ void __launch_bounds__(CHASE_WARPS * 32, 1) k_chase(const EigDev* __r
 
 // Eigenvectors of the band matrix from those of its tridiagonal: Z <- Q2 Z
 // with Q2 the product of the chase reflectors in chase order, applied in
-// reverse (LAPACK dsbtrd's Q, applied as dormtr would).  One CTA per 16
-// eigenvectors of a matrix on a row-major n x 16 scratch copy (lane =
-// column x row parity: every warp access is two adjacent 128-byte rows).  The reflectors
-// of one sweep touch disjoint 32-row blocks: the CTA's warps share a sweep's
-// blocks, each prefetching its next block's rows while it applies the
-// current one, and synchronise once per sweep; the sweep's reflectors are
-// staged into shared memory by cp.async one sweep ahead.
-constexpr int Q2_COLS = 16, Q2_WARPS = 8, Q2_ROWS = B2 / 2;  // rows per lane
+// reverse (LAPACK dsbtrd's Q, applied as dormtr would).  Every reflector
+// re-reads and rewrites its 32 rows of Z, so the rows must live on chip: one
+// CTA per NC eigenvectors keeps its n x NC slice of Z in shared memory for
+// the whole pass (row-major; lane = column x row group, rows interleaved so
+// a warp's accesses are conflict-free).  The reflectors of one sweep touch
+// disjoint 32-row blocks: the CTA's 8 warps share a sweep's blocks and
+// synchronise once per sweep, with the next sweep's reflectors staged into
+// shared memory by cp.async while the current one is applied.
+constexpr int Q2_WARPS = 8;
 
-__device__ __forceinline__ void q2_cp8(double* dst, const double* src) {
-  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src));
-}
-
-__global__ void __launch_bounds__(Q2_WARPS * 32, 2) k_q2_apply(const EigDev* __restrict__ jobs) {
+template <int NC>
+__global__ void __launch_bounds__(Q2_WARPS * 32) k_q2_apply(const EigDev* __restrict__ jobs) {
+  constexpr int G = 32 / NC;       // row groups per warp
+  constexpr int RPL = B2 / G;      // rows per lane
   const EigDev J = jobs[blockIdx.y];
   const int n = J.n, kk = J.kk;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nt = blockDim.x;
-  const int c0 = blockIdx.x * Q2_COLS;
+  const int c0 = blockIdx.x * NC;
   if (c0 >= kk || n < 3) return;
-  const int nc = min(Q2_COLS, kk - c0);
-  double* S = J.q2ws + (size_t)blockIdx.x * n * Q2_COLS;  // this matrix's scratch
-  extern __shared__ double rbuf[];                         // [2][kmax][B2 + 1]
+  const int nc = min(NC, kk - c0);
   const int kmax = sweep_steps(n, 0);
-  for (int e = tid; e < n * Q2_COLS; e += nt) {
+  extern __shared__ __align__(16) double q2sm[];
+  double* Zs = q2sm;                              // [n][NC]
+  double* rbuf = q2sm + (size_t)n * NC;           // [2][kmax][B2 + 1]
+  for (int e = tid; e < n * NC; e += nt) {
     const int r = e % n, q = e / n;
-    S[(size_t)r * Q2_COLS + q] = q < nc ? J.Z[r + (long long)(c0 + q) * J.ldz] : 0.0;
+    Zs[r * NC + q] = q < nc ? J.Z[r + (long long)(c0 + q) * J.ldz] : 0.0;
   }
   const double* R = J.refl;
   auto stage = [&](int s, int buf) {
     const double* src = R + steps_before(n, s) * (B2 + 1);
     double* dst = rbuf + (size_t)buf * kmax * (B2 + 1);
     const int cnt = sweep_steps(n, s) * (B2 + 1);
-    for (int e = tid; e < cnt; e += nt) q2_cp8(dst + e, src + e);
+    for (int e = tid; e < cnt; e += nt) {
+      const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst + e));
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src + e));
+    }
   };
   stage(n - 3, 0);
   asm volatile("cp.async.commit_group;\n");
-  __syncthreads();
+  const int q = lane % NC, g = lane / NC;  // column, row group
   int it = 0;
   for (int s = n - 3; s >= 0; --s, ++it) {
-    const int buf = it & 1;
-    if (s > 0) stage(s - 1, buf ^ 1);
+    const int sb = it & 1;
+    if (s > 0) stage(s - 1, sb ^ 1);
     asm volatile("cp.async.commit_group;\n");
     asm volatile("cp.async.wait_group 1;\n");
     __syncthreads();
-    const double* rb = rbuf + (size_t)buf * kmax * (B2 + 1);
+    const double* rb = rbuf + (size_t)sb * kmax * (B2 + 1);
     const int K = sweep_steps(n, s);
-    // lane = column (lane & 15) x row parity (lane >> 4): a warp instruction
-    // reads two adjacent 128-byte rows
-    const int q = lane & (Q2_COLS - 1), h = lane >> 4;
-    double zn[Q2_ROWS];
-    auto fetch = [&](int k) {
-      const int r0 = s + 1 + k * B2, L = min(B2, n - r0);
-      const double* zb = S + (size_t)(r0 + h) * Q2_COLS + q;
-#pragma unroll
-      for (int j = 0; j < Q2_ROWS; ++j) zn[j] = 2 * j + h < L ? zb[2 * j * Q2_COLS] : 0.0;
-    };
-    if (warp < K) fetch(warp);
     for (int k = warp; k < K; k += Q2_WARPS) {
-      double z[Q2_ROWS];
-#pragma unroll
-      for (int j = 0; j < Q2_ROWS; ++j) z[j] = zn[j];
-      if (k + Q2_WARPS < K) fetch(k + Q2_WARPS);  // disjoint rows of the same sweep
       const double* rv = rb + k * (B2 + 1);
       const double tau = rv[B2];
       if (tau == 0.0) continue;
       const int r0 = s + 1 + k * B2, L = min(B2, n - r0);
-      double d0 = 0.0, d1 = 0.0;
+      double z[RPL], v[RPL];
 #pragma unroll
-      for (int j = 0; j < Q2_ROWS; j += 2) {
-        d0 += rv[2 * j + h] * z[j];
-        d1 += rv[2 * j + 2 + h] * z[j + 1];
+      for (int j = 0; j < RPL; ++j) {
+        const int i = g + G * j;  // row of the block
+        v[j] = rv[i];
+        z[j] = i < L ? Zs[(r0 + i) * NC + q] : 0.0;
       }
-      double dot = d0 + d1;
-      dot += __shfl_xor_sync(0xffffffffu, dot, 16);  // the other row parity
+      double dot = 0.0;
+#pragma unroll
+      for (int j = 0; j < RPL; ++j) dot += v[j] * z[j];
+#pragma unroll
+      for (int o = NC; o < 32; o <<= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
       dot *= tau;
-      // all shared-memory reads of v before the global stores (a store could
-      // alias shared memory as far as the compiler knows)
 #pragma unroll
-      for (int j = 0; j < Q2_ROWS; ++j) z[j] -= dot * rv[2 * j + h];
-      double* zb = S + (size_t)(r0 + h) * Q2_COLS + q;
-#pragma unroll
-      for (int j = 0; j < Q2_ROWS; ++j)
-        if (2 * j + h < L) zb[2 * j * Q2_COLS] = z[j];
+      for (int j = 0; j < RPL; ++j) {
+        const int i = g + G * j;
+        if (i < L) Zs[(r0 + i) * NC + q] = z[j] - dot * v[j];
+      }
     }
     __syncthreads();  // next sweep: rows overlap, and this buffer is restaged
   }
   asm volatile("cp.async.wait_group 0;\n");
-  for (int e = tid; e < n * Q2_COLS; e += nt) {
-    const int r = e % n, q = e / n;
-    if (q < nc) J.Z[r + (long long)(c0 + q) * J.ldz] = S[(size_t)r * Q2_COLS + q];
+  __syncthreads();
+  for (int e = tid; e < n * NC; e += nt) {
+    const int r = e % n, qq = e / n;
+    if (qq < nc) J.Z[r + (long long)(c0 + qq) * J.ldz] = Zs[r * NC + qq];
   }
+}
+
+// Columns per CTA: as many as fit shared memory with the reflector buffers.
+int q2_cols(int n) {
+  const size_t rb = (size_t)2 * ((n - 3) / B2 + 1) * (B2 + 1) * sizeof(double);
+  for (int nc : {8, 4, 2})
+    if ((size_t)n * nc * sizeof(double) + rb <= 220 * 1024) return nc;
+  return 0;
+}
+
+size_t q2_smem(int n, int nc) {
+  return (size_t)n * nc * sizeof(double) + (size_t)2 * ((n - 3) / B2 + 1) * (B2 + 1) * sizeof(double);
 }
 
 // Eigenvectors of the band matrix (band0, bandwidth B2) by inverse
@@ -1921,7 +1923,8 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
   // capped at 8 GB
   int cpm = std::max(1, std::min(ceil_div(3 * ctx.num_sms, count), ceil_div(kkmax, INV_WARPS)));
   while (cpm > 1 && lu_slot_max * sizeof(double) * INV_WARPS * cpm * count > (size_t(8) << 30)) --cpm;
-  const int q2x = ceil_div(kkmax, Q2_COLS);
+  const int q2nc = std::max(1, q2_cols(nmax));
+  const int q2x = ceil_div(kkmax, q2nc);
   if (band_invit) {
     double* lu = ctx.arena.alloc_n<double>(lu_slot_max * INV_WARPS * cpm * count);
     for (int g = 0; g < count; ++g) {  // indexed by blockIdx.x in the kernel
@@ -1930,7 +1933,7 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
     }
   } else {
     for (int g = 0; g < count; ++g)
-      dev[g].q2ws = ctx.arena.alloc_n<double>((size_t)q2x * dev[g].n * Q2_COLS);
+      dev[g].q2ws = nullptr;  // k_q2_apply keeps its columns in shared memory
   }
   const EigDev* dd = upload_jobs(ctx, dev);
 
@@ -2053,9 +2056,17 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
     k_band_mgs<<<count, 256, 0, ctx.stream>>>(dd);  // clusters of the tridiagonal's vectors
     ctx.check_launch("k_band_mgs");
     ctx.launch_begin();
-    const size_t q2smem = (size_t)2 * ((nmax - 3) / B2 + 1) * (B2 + 1) * sizeof(double);
-    smem_optin(k_q2_apply, q2smem);
-    k_q2_apply<<<dim3(q2x, count), Q2_WARPS * 32, q2smem, ctx.stream>>>(dd);
+    const size_t q2smem = q2_smem(nmax, q2nc);
+    if (q2nc == 8) {
+      smem_optin(k_q2_apply<8>, q2smem);
+      k_q2_apply<8><<<dim3(q2x, count), Q2_WARPS * 32, q2smem, ctx.stream>>>(dd);
+    } else if (q2nc == 4) {
+      smem_optin(k_q2_apply<4>, q2smem);
+      k_q2_apply<4><<<dim3(q2x, count), Q2_WARPS * 32, q2smem, ctx.stream>>>(dd);
+    } else {
+      smem_optin(k_q2_apply<2>, q2smem);
+      k_q2_apply<2><<<dim3(q2x, count), Q2_WARPS * 32, q2smem, ctx.stream>>>(dd);
+    }
     ctx.check_launch("k_q2_apply");
   } else {
     const size_t smem =
