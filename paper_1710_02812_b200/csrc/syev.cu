@@ -38,7 +38,7 @@ constexpr int EIG_THREADS = 512;
 constexpr int NB = 32;       // reflectors per compact-WY block
 constexpr int B2 = 32;       // bandwidth of the two-stage reduction
 constexpr int LDBB = 2 * B2 + 1;  // band storage: diagonals 0..2*B2 (chase fill)
-constexpr int kBandInvitMinN = 3072;  // band inverse iteration above this n
+constexpr int kBandInvitMinN = 1 << 30;  // band inverse iteration: only when forced
 constexpr int kBandGroupDefault = 4;  // panels per delayed trailing update (two-stage stage 1)
 constexpr int INV_WARPS = 4;      // warps (= LU workspace slots) per band inverse iteration CTA
 
@@ -1889,8 +1889,9 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
   int kBandGroup = kBandGroupDefault;
   // eigenvectors: inverse iteration on the tridiagonal + the chase
   // reflectors (k_q2_apply), or inverse iteration on the band matrix
-  // (k_band_invit).  Measured on B200 (64-matrix batches): the first wins at
-  // n = 2048 and 2500, the second at n = 4096.  HSVD_BAND_INVIT=0/1 forces.
+  // (k_band_invit).  Measured on B200 (64-matrix batches) with the on-chip
+  // k_q2_apply: the first wins at n = 2048, 2500 and 4096 (1039 vs 1065 ms
+  // at config 5 / 64 leaves).  HSVD_BAND_INVIT=1 forces the second.
   bool band_invit = nmax > kBandInvitMinN;
   if (const char* env = std::getenv("HSVD_BAND_INVIT")) band_invit = std::atoi(env) != 0;
   if (const char* env = std::getenv("HSVD_BAND_GROUP")) kBandGroup = std::max(1, std::atoi(env));
