@@ -72,7 +72,6 @@ struct EigDev {
   double* Z1;        // (2*B2*group) x B2: pending-update products
   double* lu;        // per-warp band LU workspace (cpm * INV_WARPS slots per matrix)
   double* refl;      // chase reflectors: (steps) x 33 (v[0..31], tau), sweep-major
-  double* q2ws;      // k_q2_apply scratch (row-major n x 16 per warp)
   long long lu_slot;  // doubles per slot
 };
 
@@ -1932,9 +1931,6 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
       dev[g].lu = lu;
       dev[g].lu_slot = (long long)lu_slot_max;
     }
-  } else {
-    for (int g = 0; g < count; ++g)
-      dev[g].q2ws = nullptr;  // k_q2_apply keeps its columns in shared memory
   }
   const EigDev* dd = upload_jobs(ctx, dev);
 
