@@ -94,6 +94,15 @@ def cpu_slice_sample(w, threads):
     return sec, xs.nbytes, desc
 
 
+def arm_config(w, ws):
+    """The workload description both arms print."""
+    return {"workload": w.name, "m": w.m, "n": w.n, "input_dtype": w.dtype,
+            "grid": f"{w.P}x{w.Q}", "k": w.k, "gamma": GAMMA,
+            "l2": "input exceeds the 126 MB L2; no flush between steps",
+            "parallelism": (f"rows sharded by row slice over {ws} GPUs (NCCL)"
+                            if ws > 1 else "single GPU")}
+
+
 def run_reference(args, w):
     ws, rank, _ = dist_env()
     if rank != 0:
@@ -113,7 +122,8 @@ def run_reference(args, w):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded BASELINE.json recipe)",
-        "config": {"workload": w.name, "sample": desc},
+        "config": dict(arm_config(w, 1), sample=desc,
+                       parallelism=f"CPU oracle port, {threads} host threads"),
         "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "port",
                          "sample": desc},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0,
@@ -361,11 +371,7 @@ def run_ours(args, w):
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded BASELINE.json recipe, generated on device)",
-        "config": {"workload": w.name, "m": w.m, "n": w.n, "input_dtype": w.dtype,
-                   "grid": f"{w.P}x{w.Q}", "k": w.k, "gamma": GAMMA, "rank_out": rank_k,
-                   "l2": "input exceeds the 126 MB L2; no flush between steps",
-                   "parallelism": (f"rows sharded by row slice over {ws} GPUs (NCCL)"
-                                   if ws > 1 else "single GPU")},
+        "config": dict(arm_config(w, ws), rank_out=rank_k),
         "e2e": e2e, "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu,
         "clocks": clk,
         "tflops_tc": w.flops_tc() / (ms / 1000.0) / 1e12,
