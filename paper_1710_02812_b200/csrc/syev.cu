@@ -66,6 +66,7 @@ struct EigDev {
   double* band;      // (2*B2+1) x n lower band, chased to tridiagonal
   double* band0;     // copy of the band after stage 1 (inverse iteration)
   double* Tp;        // npanels x B2 x B2 panel T factors
+  double* psum;      // 8 x B2 x B2 per-CTA partials of V^T V (k_panel_qr)
   double* Y;         // n x B2
   double* P1;        // B2 x B2
   double* Mb;        // B2 x B2
@@ -814,7 +815,6 @@ __global__ void __launch_bounds__(512, 1) k_panel_qr(const EigDev* __restrict__ 
   double* Pl = psm;                          // [B2][ldp]
   double* xbuf = Pl + (size_t)B2 * ldp;      // [CS][2]   norm partial, alpha
   double* dbuf = xbuf + 2 * CS;              // [CS][B2]  column-dot partials
-  double* sbuf = dbuf + (size_t)CS * B2;     // [CS][B2*B2] V^T V partials (rank 0)
   __shared__ double beta_s[B2], tau_s[B2], red[32];
   __shared__ double S[B2][B2 + 1], T[B2][B2 + 1];
   cluster.sync();  // peers' shared memory is live before any DSMEM write
@@ -913,7 +913,10 @@ __global__ void __launch_bounds__(512, 1) k_panel_qr(const EigDev* __restrict__ 
   }
   __syncthreads();
   // S = V^T V: partials of the local rows into rank 0
-  double* s0 = cluster.map_shared_rank(sbuf, 0) + (size_t)crank * B2 * B2;
+  // (partials through global memory: CS x B2^2 doubles would not fit next to
+  // the panel at the largest n; rank 0 sums them in rank order after the
+  // cluster barrier, reading through L2)
+  double* s0 = J.psum + (size_t)crank * B2 * B2;
   for (int pq = warp; pq < B2 * B2; pq += nwarps) {
     const int pp = pq / B2, q = pq % B2;
     if (pp > q) continue;
@@ -932,7 +935,7 @@ __global__ void __launch_bounds__(512, 1) k_panel_qr(const EigDev* __restrict__ 
     const int pp = pq / B2, q = pq % B2;
     double sv = 0.0;
     if (pp <= q)
-      for (int c = 0; c < CS; ++c) sv += sbuf[(size_t)c * B2 * B2 + pq];
+      for (int c = 0; c < CS; ++c) sv += __ldcg(J.psum + (size_t)c * B2 * B2 + pq);
     S[pp][q] = sv;
   }
   for (int e = tid; e < B2 * (B2 + 1); e += nt) (&T[0][0])[e] = 0.0;
@@ -952,7 +955,7 @@ __global__ void __launch_bounds__(512, 1) k_panel_qr(const EigDev* __restrict__ 
 
 constexpr size_t kPanelSmemMax = 200 * 1024;
 size_t panel_smem(int mc, int cs) {
-  return ((size_t)B2 * (mc + 1) + 2 * cs + (size_t)cs * B2 + (size_t)cs * B2 * B2) * sizeof(double);
+  return ((size_t)B2 * (mc + 1) + 2 * cs + (size_t)cs * B2) * sizeof(double);
 }
 
 void launch_panel_qr(Ctx& ctx, int count, int mmax, const EigDev* dd, int j0, int vcol) {
@@ -1901,6 +1904,7 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
     d.band = ctx.arena.alloc_n<double>((size_t)LDBB * n);
     d.band0 = ctx.arena.alloc_n<double>((size_t)LDBB * n);
     d.Tp = ctx.arena.alloc_n<double>((size_t)ceil_div(n, B2) * B2 * B2);
+    d.psum = ctx.arena.alloc_n<double>((size_t)8 * B2 * B2);
     d.VW = ctx.arena.alloc_n<double>((size_t)n * 2 * B2 * kBandGroup);
     d.WV = ctx.arena.alloc_n<double>((size_t)n * 2 * B2 * kBandGroup);
     d.Y = ctx.arena.alloc_n<double>((size_t)n * B2);

@@ -31,3 +31,22 @@ def test_syevx_topk(path, n, kk, monkeypatch):
     res = np.abs(a @ z - z * lam).max()
     assert res <= 1e-11 * w[0], res
     assert np.abs(z.T @ z - np.eye(kk)).max() < 1e-10
+
+
+@pytest.mark.parametrize("path", ["one", "two"])
+def test_syevx_topk_max_size(path, monkeypatch):
+    """The largest matrix the eigensolver takes (n = 6144: cluster panel QR at
+    8 CTAs, Q2 back-transform at 2 columns per CTA, k_steig near its shared
+    memory limit)."""
+    import paper_1710_02812_b200 as H
+    monkeypatch.setenv("HSVD_TWO_STAGE_MIN_N", "1" if path == "two" else str(1 << 30))
+    n, kk = 6144, 48
+    rng = np.random.default_rng(6144)
+    q = np.linalg.qr(rng.standard_normal((n, 96)))[0]
+    lam_true = np.concatenate([np.exp(-0.1 * np.arange(96)) * 100.0])
+    a = (q * lam_true) @ q.T + 1e-6 * np.eye(n)
+    lam, z = H.syevx_topk(a, kk)
+    assert np.abs(lam - (lam_true[:kk] + 1e-6)).max() <= 1e-10 * lam_true[0]
+    res = np.abs(a @ z - z * lam).max()
+    assert res <= 1e-10 * lam_true[0], res
+    assert np.abs(z.T @ z - np.eye(kk)).max() < 1e-10
