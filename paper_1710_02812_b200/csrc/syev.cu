@@ -1040,9 +1040,15 @@ __device__ __forceinline__ long long steps_before(int n, int s) {
   return s + floor_sum(n - 3) - floor_sum(n - 3 - s);
 }
 
+// carry: x and the left block of this step are the rows-after block the
+// same warp updated in its previous step (its column 0 and columns 1..31),
+// still in registers (x, yl); last: no further step in this sweep, so the
+// updated rows-after block is stored instead of being carried.
 template <bool FULL, bool CG>
 __device__ __forceinline__ bool chase_step(double* bb, int c, int r0, int L, int nl, int na,
-                                           int lane, double* vs, double* ws, double* rout) {
+                                           int lane, double* vs, double* ws, double* rout,
+                                           bool carry, bool last, double& x,
+                                           double (&yl)[B2 - 1]) {
   constexpr long long LD = LDBB;
   const bool lx = lane < L;
   double* px = bb + (r0 + lane - c) + (long long)c * LD;
@@ -1051,11 +1057,15 @@ __device__ __forceinline__ bool chase_step(double* bb, int c, int r0, int L, int
   double* pa2 = bb + (long long)(r0 + lane) * LD - lane;        // (r0+j, r0+lane), j > lane
   double* pya = bb + (L + lane) + (long long)r0 * LD;           // (r0+L+lane, r0+j)
   const bool ly = lane < na;
-  // all loads of the step issued together (one memory round trip)
-  const double x = lx ? band_ld<CG>(px) : 0.0;
-  double yl[B2 - 1], ar[B2], ya[B2];
+  // all loads of the step issued together (one memory round trip); a
+  // carried bulge needs none for x and the left block
+  double ar[B2], ya[B2];
+  if (!carry) {
+    x = lx ? band_ld<CG>(px) : 0.0;
 #pragma unroll
-  for (int l = 0; l < B2 - 1; ++l) yl[l] = (lx && (FULL || l < nl)) ? band_ld<CG>(pyl + l * (LD - 1)) : 0.0;
+    for (int l = 0; l < B2 - 1; ++l)
+      yl[l] = (lx && (FULL || l < nl)) ? band_ld<CG>(pyl + l * (LD - 1)) : 0.0;
+  }
 #pragma unroll
   for (int j = 0; j < B2; ++j) {
     const double* pa = lane >= j ? pa1 + j * (LD - 1) : pa2 + j;
@@ -1065,7 +1075,15 @@ __device__ __forceinline__ bool chase_step(double* bb, int c, int r0, int L, int
   for (int j = 0; j < B2; ++j) ya[j] = (ly && (FULL || j < L)) ? band_ld<CG>(pya + j * (LD - 1)) : 0.0;
   const double xn2 = warp_sum(lane >= 1 ? x * x : 0.0);
   const double alpha = __shfl_sync(0xffffffffu, x, 0);
-  if (xn2 == 0.0) return false;
+  if (xn2 == 0.0) {  // no bulge left: a carried block still has to reach memory
+    if (carry) {
+      if (lx) *px = x;
+#pragma unroll
+      for (int l = 0; l < B2 - 1; ++l)
+        if (lx && (FULL || l < nl)) pyl[l * (LD - 1)] = yl[l];
+    }
+    return false;
+  }
   const double nrm = sqrt(alpha * alpha + xn2);
   const double beta = alpha >= 0.0 ? -nrm : nrm;
   const double tau = (beta - alpha) / beta;
@@ -1129,9 +1147,15 @@ __device__ __forceinline__ bool chase_step(double* bb, int c, int r0, int L, int
     y3 += ya[j + 3] * vs[j + 3];
   }
   const double y = tau * ((y0 + y1) + (y2 + y3));
+  if (last) {
 #pragma unroll
-  for (int j = 0; j < B2; ++j)
-    if (ly && (FULL || j < L)) pya[j * (LD - 1)] = ya[j] - y * vs[j];
+    for (int j = 0; j < B2; ++j)
+      if (ly && (FULL || j < L)) pya[j * (LD - 1)] = ya[j] - y * vs[j];
+  } else {  // the next step's x and left block (stored by that step)
+    x = ya[0] - y * vs[0];
+#pragma unroll
+    for (int l = 0; l < B2 - 1; ++l) yl[l] = (FULL || l + 1 < L) ? ya[l + 1] - y * vs[l + 1] : 0.0;
+  }
   return true;
 }
 
@@ -1176,6 +1200,7 @@ __global__ void __launch_bounds__(CHASE_WARPS * 32, 1) k_chase(const EigDev* __r
   unsigned long long seen = 0;  // last acquired progress of sweep s-1's warp
   const int nsweeps = n - 2;
   for (int s = gw; s < nsweeps; s += W) {
+    double cx, cyl[B2 - 1];  // x and left block, carried between consecutive steps
     for (int k = 0;; ++k) {
       const int r0 = s + 1 + k * B2;
       if (r0 >= n) break;
@@ -1213,10 +1238,13 @@ __global__ void __launch_bounds__(CHASE_WARPS * 32, 1) k_chase(const EigDev* __r
       const int nl = r0 - c - 1;                // left-block columns (0 or B2-1)
       const int na = min(n, r0 + 2 * B2) - r1;  // rows after R
       double* rout = J.refl ? J.refl + (steps_before(n, s) + k) * (B2 + 1) : nullptr;
+      const bool last = r0 + B2 > n - 2;  // the loop's own continuation test
       const bool ok =
           (L == B2 && nl == B2 - 1)
-              ? chase_step<true, CL>(bb, c, r0, L, nl, na, lane, vsh[warp], wsh[warp], rout)
-              : chase_step<false, CL>(bb, c, r0, L, nl, na, lane, vsh[warp], wsh[warp], rout);
+              ? chase_step<true, CL>(bb, c, r0, L, nl, na, lane, vsh[warp], wsh[warp], rout,
+                                     k > 0, last, cx, cyl)
+              : chase_step<false, CL>(bb, c, r0, L, nl, na, lane, vsh[warp], wsh[warp], rout,
+                                      k > 0, last, cx, cyl);
       if (!ok) {  // no bulge left in this sweep: its remaining reflectors are I
         if (J.refl && lane == 0)
           for (int k2 = k; k2 < sweep_steps(n, s); ++k2)
