@@ -1930,7 +1930,7 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
     EigDev& d = dev[g];
     const int n = d.n;
     d.band = ctx.arena.alloc_n<double>((size_t)LDBB * n);
-    d.band0 = ctx.arena.alloc_n<double>((size_t)LDBB * n);
+    d.band0 = band_invit ? ctx.arena.alloc_n<double>((size_t)LDBB * n) : nullptr;
     d.Tp = ctx.arena.alloc_n<double>((size_t)ceil_div(n, B2) * B2 * B2);
     d.psum = ctx.arena.alloc_n<double>((size_t)8 * B2 * B2);
     d.VW = ctx.arena.alloc_n<double>((size_t)n * 2 * B2 * kBandGroup);
@@ -2043,9 +2043,10 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
       gemm_grouped(ctx, DType::F64, DType::F64, false, true, true, g6);
     }
   }
-  for (int g = 0; g < count; ++g)
-    HSVD_CUDA(cudaMemcpyAsync(dev[g].band0, dev[g].band, (size_t)LDBB * dev[g].n * sizeof(double),
-                              cudaMemcpyDeviceToDevice, ctx.stream));
+  if (band_invit)  // the band before the chase, for the band inverse iteration
+    for (int g = 0; g < count; ++g)
+      HSVD_CUDA(cudaMemcpyAsync(dev[g].band0, dev[g].band, (size_t)LDBB * dev[g].n * sizeof(double),
+                                cudaMemcpyDeviceToDevice, ctx.stream));
   // stage 2: band -> tridiagonal (values), eigenvalues by bisection
   SubPhase sp2(ctx, "tri");
   ctx.launch_begin();
