@@ -1091,8 +1091,8 @@ __device__ __forceinline__ bool chase_step(double* bb, int c, int r0, int L, int
   const double v = lane == 0 ? 1.0 : (lx ? x * scal : 0.0);
   vs[lane] = v;
   if (rout) {  // kept for the eigenvector back-transform (k_q2_apply)
-    rout[lane] = v;
-    if (lane == 0) rout[B2] = tau;
+    __stcs(rout + lane, v);  // streaming: read once by k_q2_apply, keep L2 for the band
+    if (lane == 0) __stcs(rout + B2, tau);
   }
   if (lx) *px = lane == 0 ? beta : 0.0;
   // left block: d_l = sum_i v_i y_il by a transposing butterfly (lane l
