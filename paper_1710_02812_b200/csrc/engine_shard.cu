@@ -65,8 +65,6 @@ DFac rank_k_svd_sharded(Ctx& ctx, Comm& comm, const XView& xl, long long m_total
   std::vector<Item> items(P);
   for (int s = 0; s < P; ++s) items[s].owner = owner_of(s, P, world);
   if (exp_m > 0) {
-    HsvdConfig local = cfg;
-    local.d = d_eff;
     auto rows = partition(xl.m, d_eff);
     auto cols = partition(xl.n, cfg.c);
     const int Pl = static_cast<int>(rows.size()), Q = static_cast<int>(cols.size());

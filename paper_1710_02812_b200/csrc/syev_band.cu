@@ -1,0 +1,1092 @@
+// Two-stage reduction of the batched eigensolver (large n): dense -> band
+// B2 by cluster panel QR + delayed DMMA trailing updates, band ->
+// tridiagonal by pipelined Householder bulge chasing, eigenvectors by
+// inverse iteration on the tridiagonal pushed through the chase reflectors
+// (k_q2_apply) or, when forced, by inverse iteration on the band itself;
+// then back through the stage-1 reflectors (syev.cu back_transform).
+#include "syev_impl.cuh"
+
+namespace hsvdcu {
+namespace syev_impl {
+
+namespace {
+
+// tools/proto/two_stage.py is the numpy model of every step; the pipelined
+// chase order was checked there to give the sequential result bit for bit.
+
+// Panel j0: copy the diagonal block to the band, Householder QR of the
+// panel below the band (R -> band, explicit V in place and in VW/WV), T.
+__global__ void __launch_bounds__(512, 1) k_panel_qr(const EigDev* __restrict__ jobs, int j0,
+                                                     int CS, int vcol) {
+  // One matrix per cluster of CS CTAs; CTA c keeps rows [c*mc, (c+1)*mc) of
+  // the m x B2 panel in shared memory (column-major, ld mc + 1) for the whole
+  // factorisation.  Per column: the norm and the B2-1 column dots are summed
+  // from per-CTA partials exchanged through distributed shared memory (every
+  // CTA writes its partials into every peer, one cluster barrier, then each
+  // sums them in rank order -- identical values in every CTA).
+  const EigDev J = jobs[blockIdx.x / CS];
+  const int crank = blockIdx.x % CS;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int n = J.n;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
+  double* A = J.A;
+  const long long lda = J.lda;
+  const int jb = max(0, min(B2, n - j0));
+  const int r0 = j0 + B2;
+  const int m = max(0, n - r0);
+  const int mc = (m + CS - 1) / CS;          // rows per CTA
+  const int lo = min(m, crank * mc), hi = min(m, lo + mc), ml = hi - lo;
+  const int ldp = mc + 1;
+  extern __shared__ double psm[];
+  double* Pl = psm;                          // [B2][ldp]
+  double* xbuf = Pl + (size_t)B2 * ldp;      // [CS][2]   norm partial, alpha
+  double* dbuf = xbuf + 2 * CS;              // [CS][B2]  column-dot partials
+  __shared__ double beta_s[B2], tau_s[B2], red[32];
+  __shared__ double S[B2][B2 + 1], T[B2][B2 + 1];
+  cluster.sync();  // peers' shared memory is live before any DSMEM write
+  if (j0 >= n) {
+    cluster.sync();
+    return;
+  }
+  if (crank == 0)
+    for (int e = tid; e < jb * jb; e += nt) {
+      const int t = e / jb, i = e % jb;
+      if (i >= t) band_at(J.band, j0 + i, j0 + t) = A[(j0 + i) + (long long)(j0 + t) * lda];
+    }
+  const int nr = m >= 2 ? min(jb, m - 1) : 0;
+  double* P = A + r0 + (long long)j0 * lda;
+  // panel rows -> shared memory
+  for (int e = tid; e < jb * ml; e += nt) {
+    const int t = e / ml, i = e % ml;
+    Pl[t * ldp + i] = P[lo + i + (long long)t * lda];
+  }
+  __syncthreads();
+  for (int t = 0; t < nr; ++t) {
+    double* pt = Pl + t * ldp;
+    // (a) norm of rows t+1.. and alpha = P[t][t]
+    double part = 0.0;
+    for (int i = max(0, t + 1 - lo) + tid; i < ml; i += nt) part += pt[i] * pt[i];
+    part = block_sum(part, red);
+    const bool own_t = t >= lo && t < hi;
+    if (tid == 0)
+      for (int c = 0; c < CS; ++c) {
+        double* px = cluster.map_shared_rank(xbuf, c);
+        px[2 * crank] = part;
+        if (own_t) px[1] = pt[t - lo];  // slot 1 of rank 0's pair is unused
+      }
+    cluster.sync();
+    double xn2 = 0.0;
+    for (int c = 0; c < CS; ++c) xn2 += xbuf[2 * c];
+    const double alpha = xbuf[1];
+    double tau = 0.0, beta = alpha, scal = 0.0;
+    if (xn2 > 0.0) {
+      const double nrm = sqrt(alpha * alpha + xn2);
+      beta = alpha >= 0.0 ? -nrm : nrm;
+      tau = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    for (int i = max(0, t + 1 - lo) + tid; i < ml; i += nt) pt[i] *= scal;
+    if (tid == 0) {
+      beta_s[t] = beta;
+      tau_s[t] = tau;
+      if (crank == 0) J.tau[j0 + t] = tau;
+    }
+    __syncthreads();
+    // (c) s_u = P[t][u] + sum_{i>t} v_i P[i][u] for u > t (partials)
+    for (int u = t + 1 + warp; u < jb; u += nwarps) {
+      const double* pu = Pl + u * ldp;
+      double sp = 0.0;
+      for (int i = max(0, t + 1 - lo) + lane; i < ml; i += 32) sp += pt[i] * pu[i];
+      sp = warp_sum(sp);
+      if (own_t) sp += pu[t - lo];
+      if (lane < CS) cluster.map_shared_rank(dbuf, lane)[crank * B2 + u] = sp;
+    }
+    cluster.sync();
+    // (d) P[i][u] -= tau s_u v_i
+    if (tau != 0.0) {
+      for (int u = t + 1 + warp; u < jb; u += nwarps) {
+        double su = 0.0;
+        for (int c = 0; c < CS; ++c) su += dbuf[c * B2 + u];
+        su *= tau;
+        double* pu = Pl + u * ldp;
+        if (own_t && lane == 0) pu[t - lo] -= su;
+        for (int i = max(0, t + 1 - lo) + lane; i < ml; i += 32) pu[i] -= su * pt[i];
+      }
+    }
+    __syncthreads();
+  }
+  if (tid < B2 && tid >= nr) {
+    tau_s[tid] = 0.0;
+    if (crank == 0 && tid < jb) J.tau[j0 + tid] = 0.0;
+  }
+  __syncthreads();
+  // R -> band (panel rows i <= t < B2, owned by the CTAs holding rows < B2)
+  for (int e = tid; e < jb * jb; e += nt) {
+    const int t = e / jb, i = e % jb;
+    if (i <= t && i < m && i >= lo && i < hi)
+      band_at(J.band, r0 + i, j0 + t) = (i == t && t < nr) ? beta_s[t] : Pl[t * ldp + i - lo];
+  }
+  // explicit V (unit lower trapezoidal) in place, in the VW / WV panels and
+  // in shared memory (for V^T V)
+  __syncthreads();
+  for (int e = tid; e < jb * ml; e += nt) {
+    const int t = e / ml, i = e % ml, ig = lo + i;
+    const double v = t >= nr ? 0.0 : (ig < t ? 0.0 : (ig == t ? 1.0 : Pl[t * ldp + i]));
+    Pl[t * ldp + i] = v;
+    P[ig + (long long)t * lda] = v;
+    J.VW[(r0 + ig) + (long long)(vcol + t) * n] = v;
+    J.WV[(r0 + ig) + (long long)(vcol + B2 + t) * n] = v;
+  }
+  __syncthreads();
+  // S = V^T V: partials of the local rows into rank 0
+  // (partials through global memory: CS x B2^2 doubles would not fit next to
+  // the panel at the largest n; rank 0 sums them in rank order after the
+  // cluster barrier, reading through L2)
+  double* s0 = J.psum + (size_t)crank * B2 * B2;
+  for (int pq = warp; pq < B2 * B2; pq += nwarps) {
+    const int pp = pq / B2, q = pq % B2;
+    if (pp > q) continue;
+    double sp = 0.0;
+    if (q < nr) {
+      const double* vp = Pl + pp * ldp;
+      const double* vq = Pl + q * ldp;
+      for (int i = max(0, q - lo) + lane; i < ml; i += 32) sp += vp[i] * vq[i];
+      sp = warp_sum(sp);
+    }
+    if (lane == 0) s0[pq] = sp;
+  }
+  cluster.sync();  // last DSMEM access: peers may exit after this
+  if (crank != 0) return;
+  for (int pq = tid; pq < B2 * B2; pq += nt) {
+    const int pp = pq / B2, q = pq % B2;
+    double sv = 0.0;
+    if (pp <= q)
+      for (int c = 0; c < CS; ++c) sv += __ldcg(J.psum + (size_t)c * B2 * B2 + pq);
+    S[pp][q] = sv;
+  }
+  for (int e = tid; e < B2 * (B2 + 1); e += nt) (&T[0][0])[e] = 0.0;
+  __syncthreads();
+  for (int t = 0; t < B2; ++t) {
+    if (tid < t) {
+      double sv = 0.0;
+      for (int l = tid; l < t; ++l) sv += T[tid][l] * S[l][t];
+      T[tid][t] = -tau_s[t] * sv;
+    }
+    if (tid == 0) T[t][t] = tau_s[t];
+    __syncthreads();
+  }
+  double* out = J.Tp + (long long)(j0 / B2) * B2 * B2;
+  for (int e = tid; e < B2 * B2; e += nt) out[e] = T[e % B2][e / B2];
+}
+
+constexpr size_t kPanelSmemMax = 200 * 1024;
+size_t panel_smem(int mc, int cs) {
+  return ((size_t)B2 * (mc + 1) + 2 * cs + (size_t)cs * B2) * sizeof(double);
+}
+
+void launch_panel_qr(Ctx& ctx, int count, int mmax, const EigDev* dd, int j0, int vcol) {
+  int cs = 1;
+  while (cs < 8 && panel_smem((mmax + cs - 1) / cs, cs) > kPanelSmemMax) cs *= 2;
+  const size_t smem = panel_smem((mmax + cs - 1) / cs, cs);
+  if (smem > kPanelSmemMax) throw Error(kInvalid, "k_panel_qr: n too large");
+  smem_optin(k_panel_qr, smem);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(count * cs);
+  cfg.blockDim = dim3(512);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = ctx.stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  ctx.launch_begin();
+  HSVD_CUDA(cudaLaunchKernelEx(&cfg, k_panel_qr, dd, j0, cs, vcol));
+  ctx.check_launch("k_panel_qr");
+}
+
+// WV[:, vcol:vcol+B2] = W (= VW[:, vcol+B2:vcol+2B2]) for the rows below the panel
+// (panels with no trailing matrix, r0 > n-2: W := 0 on the rows r0..n-1, so
+// the pending pairs of the group stay finite and exact)
+__global__ void k_copy_w(const EigDev* __restrict__ jobs, int j0, int vcol) {
+  const EigDev J = jobs[blockIdx.y];
+  const int n = J.n, r0 = j0 + B2;
+  if (r0 > n - 2) {
+    if (blockIdx.x == 0)
+      for (int e = threadIdx.x; e < max(0, n - r0) * B2; e += blockDim.x) {
+        const int i = r0 + e % max(1, n - r0), t = e / max(1, n - r0);
+        J.WV[i + (long long)(vcol + t) * n] = 0.0;
+        J.VW[i + (long long)(vcol + B2 + t) * n] = 0.0;
+      }
+    return;
+  }
+  const long long total = (long long)(n - r0) * B2;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int i = r0 + (int)(e % (n - r0)), t = (int)(e / (n - r0));
+    J.WV[i + (long long)(vcol + t) * n] = J.VW[i + (long long)(vcol + B2 + t) * n];
+  }
+}
+
+// Band -> tridiagonal by Householder bulge chasing (eigenvalues only).
+// One CTA per matrix; warp w runs sweeps w, w+W, ...; sweep s may do step
+// k only after sweep s-1 finished step k+3 (or the whole sweep), which
+// reproduces the sequential result exactly.
+__device__ __forceinline__ unsigned long long prog_encode(int s, unsigned steps) {
+  return ((unsigned long long)(unsigned)(s + 1) << 32) | steps;
+}
+constexpr unsigned kSweepDone = 0x7fffffffu;
+
+constexpr int CHASE_WARPS = 8;
+static_assert(B2 == 32, "k_chase maps one band row per lane");
+
+// One bulge-chasing step of a warp: reflector from column c (rows r0..r0+L),
+// applied to the left block (columns c+1..c+nl), two-sided to the L x L
+// block R at r0 and from the right to the na rows below R.  Every element
+// is addressed from a per-lane base pointer plus a compile-time offset
+// (band column stride LDBB, diagonal stride LDBB-1); FULL (L == B2 and
+// nl == B2-1) drops the per-column bounds.  Returns false when the column
+// is already reduced (the sweep ends).
+template <bool CG>
+__device__ __forceinline__ double band_ld(const double* p) {
+  return CG ? __ldcg(p) : *p;
+}
+
+// Steps of sweep s (k with r0 = s+1+32k <= n-2) and the steps of all sweeps
+// before it: the compact sweep-major index of the stored chase reflectors.
+__device__ __forceinline__ int sweep_steps(int n, int s) { return (n - 3 - s) / B2 + 1; }
+__device__ __forceinline__ long long floor_sum(long long A) {  // sum_{a=0}^{A} floor(a/B2)
+  if (A < 0) return 0;
+  const long long q = (A + 1) / B2, r = (A + 1) % B2;
+  return B2 * q * (q - 1) / 2 + r * q;
+}
+__device__ __forceinline__ long long steps_before(int n, int s) {
+  return s + floor_sum(n - 3) - floor_sum(n - 3 - s);
+}
+
+// carry: x and the left block of this step are the rows-after block the
+// same warp updated in its previous step (its column 0 and columns 1..31),
+// still in registers (x, yl); last: no further step in this sweep, so the
+// updated rows-after block is stored instead of being carried.
+template <bool FULL, bool CG>
+__device__ __forceinline__ bool chase_step(double* bb, int c, int r0, int L, int nl, int na,
+                                           int lane, double* vs, double* ws, double* rout,
+                                           bool carry, bool last, double& x,
+                                           double (&yl)[B2 - 1]) {
+  constexpr long long LD = LDBB;
+  const bool lx = lane < L;
+  double* px = bb + (r0 + lane - c) + (long long)c * LD;
+  double* pyl = bb + (r0 + lane - c - 1) + (long long)(c + 1) * LD;
+  double* pa1 = bb + lane + (long long)r0 * LD;                 // (r0+lane, r0+j), j <= lane
+  double* pa2 = bb + (long long)(r0 + lane) * LD - lane;        // (r0+j, r0+lane), j > lane
+  double* pya = bb + (L + lane) + (long long)r0 * LD;           // (r0+L+lane, r0+j)
+  const bool ly = lane < na;
+  // all loads of the step issued together (one memory round trip); a
+  // carried bulge needs none for x and the left block
+  double ar[B2], ya[B2];
+  if (!carry) {
+    x = lx ? band_ld<CG>(px) : 0.0;
+#pragma unroll
+    for (int l = 0; l < B2 - 1; ++l)
+      yl[l] = (lx && (FULL || l < nl)) ? band_ld<CG>(pyl + l * (LD - 1)) : 0.0;
+  }
+#pragma unroll
+  for (int j = 0; j < B2; ++j) {
+    const double* pa = lane >= j ? pa1 + j * (LD - 1) : pa2 + j;
+    ar[j] = (lx && (FULL || j < L)) ? band_ld<CG>(pa) : 0.0;
+  }
+#pragma unroll
+  for (int j = 0; j < B2; ++j) ya[j] = (ly && (FULL || j < L)) ? band_ld<CG>(pya + j * (LD - 1)) : 0.0;
+  const double xn2 = warp_sum(lane >= 1 ? x * x : 0.0);
+  const double alpha = __shfl_sync(0xffffffffu, x, 0);
+  if (xn2 == 0.0) {  // no bulge left: a carried block still has to reach memory
+    if (carry) {
+      if (lx) *px = x;
+#pragma unroll
+      for (int l = 0; l < B2 - 1; ++l)
+        if (lx && (FULL || l < nl)) pyl[l * (LD - 1)] = yl[l];
+    }
+    return false;
+  }
+  const double nrm = sqrt(alpha * alpha + xn2);
+  const double beta = alpha >= 0.0 ? -nrm : nrm;
+  const double tau = (beta - alpha) / beta;
+  const double scal = 1.0 / (alpha - beta);
+  const double v = lane == 0 ? 1.0 : (lx ? x * scal : 0.0);
+  vs[lane] = v;
+  if (rout) {  // kept for the eigenvector back-transform (k_q2_apply)
+    __stcs(rout + lane, v);  // streaming: read once by k_q2_apply, keep L2 for the band
+    if (lane == 0) __stcs(rout + B2, tau);
+  }
+  if (lx) *px = lane == 0 ? beta : 0.0;
+  // left block: d_l = sum_i v_i y_il by a transposing butterfly (lane l
+  // ends with d_l), then y_il -= tau v_i d_l
+  {
+    double t[B2];
+#pragma unroll
+    for (int l = 0; l < B2 - 1; ++l) t[l] = v * yl[l];
+    t[B2 - 1] = 0.0;
+#pragma unroll
+    for (int ofs = 16; ofs >= 1; ofs >>= 1) {
+      const bool up = (lane & ofs) != 0;
+#pragma unroll
+      for (int j = 0; j < ofs; ++j) {
+        const double send = up ? t[j] : t[j + ofs];
+        const double got = __shfl_xor_sync(0xffffffffu, send, ofs);
+        t[j] = (up ? t[j + ofs] : t[j]) + got;
+      }
+    }
+    const double dl = tau * t[0];
+#pragma unroll
+    for (int l = 0; l < B2 - 1; ++l) {
+      const double d = __shfl_sync(0xffffffffu, dl, l);
+      if (lx && (FULL || l < nl)) pyl[l * (LD - 1)] = yl[l] - d * v;
+    }
+  }
+  __syncwarp();
+  // R x R: two-sided (symmetric, lower storage); p = tau R v
+  double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
+#pragma unroll
+  for (int j = 0; j < B2; j += 4) {
+    p0 += ar[j] * vs[j];
+    p1 += ar[j + 1] * vs[j + 1];
+    p2 += ar[j + 2] * vs[j + 2];
+    p3 += ar[j + 3] * vs[j + 3];
+  }
+  const double pp = tau * ((p0 + p1) + (p2 + p3));
+  const double al = -0.5 * tau * warp_sum(pp * v);
+  const double w = pp + al * v;
+  ws[lane] = w;
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < B2; ++j)
+    if (lx && lane >= j && (FULL || j < L)) pa1[j * (LD - 1)] = ar[j] - (v * ws[j] + w * vs[j]);
+  // rows after R: right application (creates the next bulge)
+  double y0 = 0.0, y1 = 0.0, y2 = 0.0, y3 = 0.0;
+#pragma unroll
+  for (int j = 0; j < B2; j += 4) {
+    y0 += ya[j] * vs[j];
+    y1 += ya[j + 1] * vs[j + 1];
+    y2 += ya[j + 2] * vs[j + 2];
+    y3 += ya[j + 3] * vs[j + 3];
+  }
+  const double y = tau * ((y0 + y1) + (y2 + y3));
+  if (last) {
+#pragma unroll
+    for (int j = 0; j < B2; ++j)
+      if (ly && (FULL || j < L)) pya[j * (LD - 1)] = ya[j] - y * vs[j];
+  } else {  // the next step's x and left block (stored by that step)
+    x = ya[0] - y * vs[0];
+#pragma unroll
+    for (int l = 0; l < B2 - 1; ++l) yl[l] = (FULL || l + 1 < L) ? ya[l + 1] - y * vs[l + 1] : 0.0;
+  }
+  return true;
+}
+
+// The sweeps of one matrix run on a cluster of CS CTAs (CS * CHASE_WARPS
+// warps; sweep s on global warp s mod (CS * CHASE_WARPS)).  Progress flags
+// live in each CTA's shared memory and are polled through DSMEM; with CS > 1
+// the band is read through L2 (__ldcg), since a peer SM may have rewritten a
+// line this SM's L1 still holds, and every step's stores are fenced at gpu
+// scope before its flag is published.
+template <bool CL>
+__global__ void __launch_bounds__(CHASE_WARPS * 32, 1) k_chase(const EigDev* __restrict__ jobs,
+                                                              int CS) {
+  const int crank = CL ? (int)(blockIdx.x % CS) : 0;
+  const EigDev J = jobs[CL ? blockIdx.x / CS : blockIdx.x];
+  const int n = J.n;
+  double* bb = J.band;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int W = CHASE_WARPS * (CL ? CS : 1);   // warps working on this matrix
+  const int gw = crank * CHASE_WARPS + warp;    // this warp's global index
+  __shared__ unsigned long long prog[CHASE_WARPS];
+  __shared__ double vsh[CHASE_WARPS][B2];
+  __shared__ double wsh[CHASE_WARPS][B2];
+  if (tid < CHASE_WARPS) prog[tid] = prog_encode(crank * CHASE_WARPS + tid - W, kSweepDone);
+  cg::cluster_group cluster = cg::this_cluster();
+  if (CL) cluster.sync();
+  else __syncthreads();
+  const int pg = (gw - 1 + W) % W;  // warp running sweep s-1
+  volatile unsigned long long* pprog =
+      CL ? cluster.map_shared_rank(prog, pg / CHASE_WARPS) + pg % CHASE_WARPS : prog + pg;
+  volatile unsigned long long* myprog = prog + warp;
+  // release-store of this warp's progress (cluster scope: the consumer may
+  // run on the peer SM and reads the band through L2 after its acquire)
+  auto publish = [&](unsigned long long val) {
+    if (CL) {
+      if (lane == 0)
+        asm volatile("st.release.cluster.u64 [%0], %1;\n" ::"l"(myprog), "l"(val) : "memory");
+    } else {
+      __threadfence_block();
+      if (lane == 0) *myprog = val;
+    }
+  };
+  unsigned long long seen = 0;  // last acquired progress of sweep s-1's warp
+  const int nsweeps = n - 2;
+  for (int s = gw; s < nsweeps; s += W) {
+    double cx, cyl[B2 - 1];  // x and left block, carried between consecutive steps
+    for (int k = 0;; ++k) {
+      const int r0 = s + 1 + k * B2;
+      if (r0 >= n) break;
+      const int r1 = min(n, r0 + B2), L = r1 - r0;
+      if (L < 2) break;
+      if (s > 0) {  // wait for sweep s-1 to be 3 steps ahead (or done)
+        const unsigned need = (unsigned)(k + 3);
+        auto ahead = [&](unsigned long long pv) {
+          const int vs = (int)(pv >> 32) - 1;
+          const unsigned st = (unsigned)(pv & 0xffffffffu);
+          return vs > s - 1 || (vs == s - 1 && st >= need);
+        };
+        // progress only grows: a value already acquired that suffices needs
+        // no new (remote) poll
+        if (!ahead(seen)) {
+          while (true) {
+            unsigned long long pv;
+            if (CL)
+              asm volatile("ld.acquire.cluster.u64 %0, [%1];\n"
+                           : "=l"(pv)
+                           : "l"(pprog)
+                           : "memory");
+            else
+              pv = *pprog;
+            if (ahead(pv)) {
+              seen = pv;
+              break;
+            }
+            __nanosleep(100);
+          }
+          if (!CL) __threadfence_block();
+        }
+      }
+      const int c = k == 0 ? s : s + 1 + (k - 1) * B2;
+      const int nl = r0 - c - 1;                // left-block columns (0 or B2-1)
+      const int na = min(n, r0 + 2 * B2) - r1;  // rows after R
+      double* rout = J.refl ? J.refl + (steps_before(n, s) + k) * (B2 + 1) : nullptr;
+      const bool last = r0 + B2 > n - 2;  // the loop's own continuation test
+      const bool ok =
+          (L == B2 && nl == B2 - 1)
+              ? chase_step<true, CL>(bb, c, r0, L, nl, na, lane, vsh[warp], wsh[warp], rout,
+                                     k > 0, last, cx, cyl)
+              : chase_step<false, CL>(bb, c, r0, L, nl, na, lane, vsh[warp], wsh[warp], rout,
+                                      k > 0, last, cx, cyl);
+      if (!ok) {  // no bulge left in this sweep: its remaining reflectors are I
+        if (J.refl && lane == 0)
+          for (int k2 = k; k2 < sweep_steps(n, s); ++k2)
+            J.refl[(steps_before(n, s) + k2) * (B2 + 1) + B2] = 0.0;
+        break;
+      }
+      __syncwarp();  // every lane's band stores before lane 0's release
+      publish(prog_encode(s, (unsigned)(k + 1)));
+    }
+    __syncwarp();
+    publish(prog_encode(s, kSweepDone));
+  }
+  if (CL) {
+    __threadfence();
+    cluster.sync();  // every sweep done; no DSMEM access after this
+    if (crank != 0) return;
+  } else {
+    __syncthreads();
+  }
+  for (int i = tid; i < n; i += blockDim.x) {
+    J.d[i] = band_ld<CL>(&band_at(bb, i, i));
+    if (i < n - 1) J.e[i] = band_ld<CL>(&band_at(bb, i + 1, i));
+  }
+}
+
+// Eigenvectors of the band matrix from those of its tridiagonal: Z <- Q2 Z
+// with Q2 the product of the chase reflectors in chase order, applied in
+// reverse (LAPACK dsbtrd's Q, applied as dormtr would).  Every reflector
+// re-reads and rewrites its 32 rows of Z, so the rows must live on chip: one
+// CTA per NC eigenvectors keeps its n x NC slice of Z in shared memory for
+// the whole pass (row-major; lane = column x row group, rows interleaved so
+// a warp's accesses are conflict-free).  The reflectors of one sweep touch
+// disjoint 32-row blocks: the CTA's 8 warps share a sweep's blocks and
+// synchronise once per sweep, with the next sweep's reflectors staged into
+// shared memory by cp.async while the current one is applied.
+constexpr int Q2_WARPS = 8;
+
+template <int NC>
+__global__ void __launch_bounds__(Q2_WARPS * 32) k_q2_apply(const EigDev* __restrict__ jobs) {
+  constexpr int G = 32 / NC;       // row groups per warp
+  constexpr int RPL = B2 / G;      // rows per lane
+  const EigDev J = jobs[blockIdx.y];
+  const int n = J.n, kk = J.kk;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nt = blockDim.x;
+  const int c0 = blockIdx.x * NC;
+  if (c0 >= kk || n < 3) return;
+  const int nc = min(NC, kk - c0);
+  const int kmax = sweep_steps(n, 0);
+  extern __shared__ __align__(16) double q2sm[];
+  double* Zs = q2sm;                              // [n][NC]
+  double* rbuf = q2sm + (size_t)n * NC;           // [2][kmax][B2 + 1]
+  for (int e = tid; e < n * NC; e += nt) {
+    const int r = e % n, q = e / n;
+    Zs[r * NC + q] = q < nc ? J.Z[r + (long long)(c0 + q) * J.ldz] : 0.0;
+  }
+  const double* R = J.refl;
+  auto stage = [&](int s, int buf) {
+    const double* src = R + steps_before(n, s) * (B2 + 1);
+    double* dst = rbuf + (size_t)buf * kmax * (B2 + 1);
+    const int cnt = sweep_steps(n, s) * (B2 + 1);
+    for (int e = tid; e < cnt; e += nt) {
+      const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst + e));
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src + e));
+    }
+  };
+  stage(n - 3, 0);
+  asm volatile("cp.async.commit_group;\n");
+  const int q = lane % NC, g = lane / NC;  // column, row group
+  int it = 0;
+  for (int s = n - 3; s >= 0; --s, ++it) {
+    const int sb = it & 1;
+    if (s > 0) stage(s - 1, sb ^ 1);
+    asm volatile("cp.async.commit_group;\n");
+    asm volatile("cp.async.wait_group 1;\n");
+    __syncthreads();
+    const double* rb = rbuf + (size_t)sb * kmax * (B2 + 1);
+    const int K = sweep_steps(n, s);
+    for (int k = warp; k < K; k += Q2_WARPS) {
+      const double* rv = rb + k * (B2 + 1);
+      const double tau = rv[B2];
+      if (tau == 0.0) continue;
+      const int r0 = s + 1 + k * B2, L = min(B2, n - r0);
+      double z[RPL], v[RPL];
+#pragma unroll
+      for (int j = 0; j < RPL; ++j) {
+        const int i = g + G * j;  // row of the block
+        v[j] = rv[i];
+        z[j] = i < L ? Zs[(r0 + i) * NC + q] : 0.0;
+      }
+      double dot = 0.0;
+#pragma unroll
+      for (int j = 0; j < RPL; ++j) dot += v[j] * z[j];
+#pragma unroll
+      for (int o = NC; o < 32; o <<= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+      dot *= tau;
+#pragma unroll
+      for (int j = 0; j < RPL; ++j) {
+        const int i = g + G * j;
+        if (i < L) Zs[(r0 + i) * NC + q] = z[j] - dot * v[j];
+      }
+    }
+    __syncthreads();  // next sweep: rows overlap, and this buffer is restaged
+  }
+  asm volatile("cp.async.wait_group 0;\n");
+  __syncthreads();
+  for (int e = tid; e < n * NC; e += nt) {
+    const int r = e % n, qq = e / n;
+    if (qq < nc) J.Z[r + (long long)(c0 + qq) * J.ldz] = Zs[r * NC + qq];
+  }
+}
+
+// Columns per CTA: as many as fit shared memory with the reflector buffers.
+int q2_cols(int n) {
+  const size_t rb = (size_t)2 * ((n - 3) / B2 + 1) * (B2 + 1) * sizeof(double);
+  for (int nc : {8, 4, 2})
+    if ((size_t)n * nc * sizeof(double) + rb <= 220 * 1024) return nc;
+  return 0;
+}
+
+size_t q2_smem(int n, int nc) {
+  return (size_t)n * nc * sizeof(double) + (size_t)2 * ((n - 3) / B2 + 1) * (B2 + 1) * sizeof(double);
+}
+
+// Eigenvectors of the band matrix (band0, bandwidth B2) by inverse
+// iteration, one warp per shift on a (cpm x count) grid.  The warp factors
+// (B - shift I) = P L U with partial pivoting in a (B2+1) x (2*B2+1)
+// shared-memory window (entering band rows prefetched two steps ahead),
+// streaming U rows and multipliers to its workspace; then three
+// forward/backward solves.  The solves keep the live part of the vector in
+// a 128-entry shared ring and prefetch U / L rows and vector entries one
+// INV_PF-step chunk ahead, so their step chain never waits on HBM.
+// k_band_mgs orthogonalises inside eigenvalue clusters afterwards.
+__device__ __forceinline__ double band_full(const double* b0, int n, int i, int j) {
+  if (i < 0 || j < 0 || i >= n || j >= n) return 0.0;
+  const int d = i - j;
+  if (d > B2 || d < -B2) return 0.0;
+  return d >= 0 ? b0[d + (long long)j * LDBB] : b0[-d + (long long)i * LDBB];
+}
+
+constexpr int INV_PF = 8;      // solve prefetch chunk (steps)
+constexpr int INV_RING = 128;  // vector ring entries per warp (>= 2*B2+1)
+
+__device__ __forceinline__ double invit_start(int r, int t) {
+  const unsigned h = hash32((unsigned)r * 2654435761u ^ hash32((unsigned)t + 0x9e3779b9u));
+  return ((double)h / 4294967296.0) * 2.0 - 1.0;
+}
+
+__global__ void __launch_bounds__(INV_WARPS * 32, 3) k_band_invit(const EigDev* __restrict__ jobs) {
+  const EigDev J = jobs[blockIdx.y];
+  const int n = J.n, kk = J.kk;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nt = blockDim.x;
+  constexpr int WR = B2 + 1, WC = 2 * B2 + 1;  // window rows / columns
+  extern __shared__ double sm[];
+  double* win = sm + (size_t)warp * WR * WC;
+  double* yw = sm + (size_t)INV_WARPS * WR * WC + (size_t)warp * INV_RING;
+  double* red = sm + (size_t)INV_WARPS * (WR * WC + INV_RING);
+  const double* b0 = J.band0;
+  // ||B||_inf for the pivot guard
+  double nb = 0.0;
+  for (int i = tid; i < n; i += nt) {
+    double s = 0.0;
+    for (int j = max(0, i - B2); j <= min(n - 1, i + B2); ++j) s += fabs(band_full(b0, n, i, j));
+    nb = fmax(nb, s);
+  }
+  const double bnorm = block_max(nb, red);
+  const double tiny = DBL_EPSILON * fmax(bnorm, DBL_MIN);
+  const int gw = blockIdx.x * INV_WARPS + warp, nw_total = gridDim.x * INV_WARPS;
+  // workspace of this warp: U rows (n x WC), multipliers (n x B2), pivots,
+  // forward result F, iterate X
+  double* U = J.lu + ((size_t)blockIdx.y * nw_total + gw) * (size_t)J.lu_slot;
+  double* Lm = U + (size_t)n * WC;
+  int* piv = reinterpret_cast<int*>(Lm + (size_t)n * B2);
+  double* F = Lm + (size_t)n * B2 + n;
+  double* X = F + n;
+  for (int t = gw; t < kk; t += nw_total) {
+    const double sh = J.shifts[t];
+    // ---- factorisation: window rows are slots (row % WR), columns (col % WC)
+    for (int e = lane; e < WR * WC; e += 32) win[e] = 0.0;
+    __syncwarp();
+    for (int i = 0; i <= B2 && i < n; ++i)
+      for (int c = lane; c <= 2 * B2; c += 32)
+        if (c < n) win[(i % WR) * WC + (c % WC)] = band_full(b0, n, i, c) - (i == c ? sh : 0.0);
+    __syncwarp();
+    double preA[3], preB[3];
+    // band row rn = jj + B2 + 1 at columns jj+1+cc, cc = lane + 32q: q = 0
+    // the strictly lower part (diagonal B2-lane of column rn-B2+lane), q = 1
+    // diagonal and upper part (column rn of the band, mirrored), q = 2
+    // (lane 0) the last upper element
+    auto fetch_row = [&](double* pre, int rn) {
+      const bool in = rn < n;
+      const double* crn = b0 + (long long)rn * LDBB;
+      pre[0] = in ? b0[(B2 - lane) + (long long)(rn - B2 + lane) * LDBB] : 0.0;
+      pre[1] = (in && rn + lane < n) ? crn[lane] - (lane == 0 ? sh : 0.0) : 0.0;
+      pre[2] = (in && lane == 0 && rn + B2 < n) ? crn[B2] : 0.0;
+    };
+    fetch_row(preA, B2 + 1);
+    fetch_row(preB, B2 + 2);
+    for (int j = 0; j < n; ++j) {
+      const int nw = min(WR, n - j);  // candidate rows j..j+nw-1
+      const int cj = j % WC;
+      // lane i holds candidate row j+i; lane 0 also row j+B2
+      double a = lane < nw ? fabs(win[((j + lane) % WR) * WC + cj]) : -1.0;
+      int p = lane;
+      if (lane == 0 && nw == WR) {
+        const double a2 = fabs(win[((j + B2) % WR) * WC + cj]);
+        if (a2 > a) {
+          a = a2;
+          p = B2;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ao = __shfl_xor_sync(0xffffffffu, a, o);
+        const int po = __shfl_xor_sync(0xffffffffu, p, o);
+        if (ao > a || (ao == a && po < p)) {
+          a = ao;
+          p = po;
+        }
+      }
+      const int sj = (j % WR) * WC, sp = ((j + p) % WR) * WC;
+      if (p != 0)
+        for (int c = lane; c < WC; c += 32) {
+          const double tmp = win[sj + c];
+          win[sj + c] = win[sp + c];
+          win[sp + c] = tmp;
+        }
+      __syncwarp();
+      double u = win[sj + cj];
+      if (fabs(u) < tiny) u = u < 0.0 ? -tiny : tiny;
+      const double ru = 1.0 / u;
+      const int ncol = min(2 * B2, n - 1 - j);
+      // columns j+1..j+ncol sit in slots cj+1..WC-1 then 0..(cj+ncol-WC)
+      // lane i (1..nw-1) eliminates row j+i over all 2*B2 window columns
+      // after j (columns past n hold zeros in both rows), eight at a time
+      // with the loads batched ahead of the stores
+      if (lane >= 1 && lane < nw) {
+        const int si = ((j + lane) % WR) * WC;
+        const double l = win[si + cj] * ru;
+        double* ri = win + si;
+        const double* rp = win + sj;
+#pragma unroll
+        for (int c0 = 1; c0 <= 2 * B2; c0 += 8) {
+          int cc[8];
+          double x[8], y[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int c = cj + c0 + q;
+            cc[q] = c >= WC ? c - WC : c;
+            x[q] = ri[cc[q]];
+            y[q] = rp[cc[q]];
+          }
+#pragma unroll
+          for (int q = 0; q < 8; ++q) ri[cc[q]] = x[q] - l * y[q];
+        }
+        Lm[(size_t)j * B2 + (lane - 1)] = l;
+      }
+      if (nw == WR) {  // row j+B2: its columns split over the lanes
+        const int si = ((j + B2) % WR) * WC;
+        const double l = win[si + cj] * ru;
+        for (int cc = 1 + lane; cc <= ncol; cc += 32) {
+          int c = cj + cc;
+          c -= c >= WC ? WC : 0;
+          win[si + c] -= l * win[sj + c];
+        }
+        if (lane == 0) Lm[(size_t)j * B2 + (B2 - 1)] = l;
+      }
+      __syncwarp();
+      // column j leaves; its slot becomes column j+2B2+1
+      if (lane >= 1 && lane < nw) win[((j + lane) % WR) * WC + cj] = 0.0;
+      if (lane == 0 && nw == WR) win[((j + B2) % WR) * WC + cj] = 0.0;
+      if (lane == 0) {
+        piv[j] = p;
+        win[sj + cj] = u;
+      }
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const int cc = lane + 32 * q;
+        if (cc < WC) {
+          int c = cj + cc;
+          c -= c >= WC ? WC : 0;
+          U[(size_t)j * WC + cc] = (cc <= ncol) ? win[sj + c] : 0.0;
+        }
+      }
+      __syncwarp();
+      // the slot of row j now holds row j+B2+1 (columns j+1..j+2B2+1)
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const int cc = lane + 32 * q;
+        if (cc < WC) {
+          int c = cj + 1 + cc;
+          c -= c >= WC ? WC : 0;
+          win[sj + c] = preA[q];
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 3; ++q) preA[q] = preB[q];
+      fetch_row(preB, j + B2 + 3);
+      __syncwarp();
+    }
+    __syncwarp();
+    // ---- three solves; iterate it reads X scaled by sc (it = 0: start vector)
+    double sc = 1.0;
+    bool unit = false;  // previous iterate degenerate: restart from e_t
+    for (int it = 0; it < 3; ++it) {
+      auto input = [&](int r) -> double {
+        if (r >= n) return 0.0;
+        if (it == 0) return invit_start(r, t);
+        if (unit) return r == t % n ? 1.0 : 0.0;
+        return X[r] * sc;
+      };
+      // forward: y <- L^-1 P y.  Ring holds y[j..j+B2] before step j.
+      for (int r = lane; r <= B2; r += 32) yw[r] = input(r);
+      __syncwarp();
+      {
+        // chunk j0..j0+INV_PF-1: lane d holds the pivot and the entering
+        // entry of step j0+d, every lane its multiplier of each step
+        double Lc[INV_PF], Ln[INV_PF];
+        int pc, pn;
+        double ec, en;
+        auto load = [&](int j0, double* Lx, int& px, double& ex) {
+#pragma unroll
+          for (int d = 0; d < INV_PF; ++d) {
+            const int j = j0 + d;
+            Lx[d] = j < n ? Lm[(size_t)j * B2 + lane] : 0.0;
+          }
+          const int jl = j0 + lane;
+          px = (lane < INV_PF && jl < n) ? piv[jl] : 0;
+          ex = lane < INV_PF ? input(jl + B2 + 1) : 0.0;
+        };
+        load(0, Lc, pc, ec);
+        for (int j0 = 0; j0 < n; j0 += INV_PF) {
+          load(j0 + INV_PF, Ln, pn, en);
+#pragma unroll
+          for (int d = 0; d < INV_PF; ++d) {
+            const int j = j0 + d;
+            const int p = __shfl_sync(0xffffffffu, pc, d);
+            const double e = __shfl_sync(0xffffffffu, ec, d);
+            if (j < n) {
+              if (p != 0 && lane == 0) {
+                const double tmp = yw[j & (INV_RING - 1)];
+                yw[j & (INV_RING - 1)] = yw[(j + p) & (INV_RING - 1)];
+                yw[(j + p) & (INV_RING - 1)] = tmp;
+              }
+              __syncwarp();
+              const double yj = yw[j & (INV_RING - 1)];
+              if (j + 1 + lane < n) yw[(j + 1 + lane) & (INV_RING - 1)] -= Lc[d] * yj;
+              if (lane == 0) {
+                F[j] = yj;
+                yw[(j + B2 + 1) & (INV_RING - 1)] = e;
+              }
+              __syncwarp();
+            }
+          }
+#pragma unroll
+          for (int d = 0; d < INV_PF; ++d) Lc[d] = Ln[d];
+          pc = pn;
+          ec = en;
+        }
+      }
+      __syncwarp();
+      // backward: U x = F.  Ring holds x[j+1..j+2B2] before step j.
+      for (int r = lane; r < INV_RING; r += 32) yw[r] = 0.0;
+      __syncwarp();
+      double nrm2 = 0.0;
+      {
+        // chunk j0, j0-1, ..: lane d holds 1/U[j0-d][0] and F[j0-d]
+        double Ac[INV_PF], Bc[INV_PF], An[INV_PF], Bn[INV_PF];
+        double rc, fc, rn, fn;
+        auto load = [&](int j0, double* Ax, double* Bx, double& rx, double& fx) {
+#pragma unroll
+          for (int d = 0; d < INV_PF; ++d) {
+            const int j = j0 - d;
+            const double* ur = U + (size_t)(j >= 0 ? j : 0) * WC;
+            Ax[d] = j >= 0 ? ur[1 + lane] : 0.0;
+            Bx[d] = j >= 0 ? ur[33 + lane] : 0.0;  // lanes 0..31 -> cc 33..64
+          }
+          const int jl = j0 - lane;
+          const bool ok = lane < INV_PF && jl >= 0;
+          rx = ok ? 1.0 / U[(size_t)jl * WC] : 0.0;
+          fx = ok ? F[jl] : 0.0;
+        };
+        load(n - 1, Ac, Bc, rc, fc);
+        for (int j0 = n - 1; j0 >= 0; j0 -= INV_PF) {
+          load(j0 - INV_PF, An, Bn, rn, fn);
+#pragma unroll
+          for (int d = 0; d < INV_PF; ++d) {
+            const int j = j0 - d;
+            const double rj = __shfl_sync(0xffffffffu, rc, d);
+            const double fj = __shfl_sync(0xffffffffu, fc, d);
+            if (j >= 0) {
+              double s = Ac[d] * yw[(j + 1 + lane) & (INV_RING - 1)] +
+                         Bc[d] * yw[(j + 33 + lane) & (INV_RING - 1)];
+              s = warp_sum(s);
+              const double x = (fj - s) * rj;
+              // (ring slots of x[j+2B2+1..] are only reused for indices
+              // that are written before they are read)
+              if (lane == 0) {
+                yw[j & (INV_RING - 1)] = x;
+                X[j] = x;
+              }
+              nrm2 += x * x;
+              __syncwarp();
+            }
+          }
+#pragma unroll
+          for (int d = 0; d < INV_PF; ++d) {
+            Ac[d] = An[d];
+            Bc[d] = Bn[d];
+          }
+          rc = rn;
+          fc = fn;
+        }
+      }
+      __syncwarp();
+      unit = !(nrm2 > 0.0 && isfinite(nrm2));
+      sc = unit ? 0.0 : 1.0 / sqrt(nrm2);
+    }
+    double* z = J.Z + (long long)t * J.ldz;
+    for (int r = lane; r < n; r += 32) z[r] = unit ? (r == t % n ? 1.0 : 0.0) : X[r] * sc;
+    __syncwarp();
+  }
+}
+}  // namespace
+
+void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& dev, int nmax,
+               int kkmax) {
+  const int count = static_cast<int>(dev.size());
+  const int npan = ceil_div(nmax, B2);
+  int kBandGroup = kBandGroupDefault;
+  // eigenvectors: inverse iteration on the tridiagonal + the chase
+  // reflectors (k_q2_apply), or inverse iteration on the band matrix
+  // (k_band_invit).  Measured on B200 (64-matrix batches) with the on-chip
+  // k_q2_apply: the first wins at n = 2048, 2500 and 4096 (1039 vs 1065 ms
+  // at config 5 / 64 leaves).  HSVD_BAND_INVIT=1 forces the second.
+  bool band_invit = nmax > kBandInvitMinN;
+  if (const char* env = std::getenv("HSVD_BAND_INVIT")) band_invit = std::atoi(env) != 0;
+  if (const char* env = std::getenv("HSVD_BAND_GROUP")) kBandGroup = std::max(1, std::atoi(env));
+  size_t lu_slot_max = 0;
+  for (int g = 0; g < count; ++g) {
+    EigDev& d = dev[g];
+    const int n = d.n;
+    d.band = ctx.arena.alloc_n<double>((size_t)LDBB * n);
+    d.band0 = band_invit ? ctx.arena.alloc_n<double>((size_t)LDBB * n) : nullptr;
+    d.Tp = ctx.arena.alloc_n<double>((size_t)ceil_div(n, B2) * B2 * B2);
+    d.psum = ctx.arena.alloc_n<double>((size_t)8 * B2 * B2);
+    d.VW = ctx.arena.alloc_n<double>((size_t)n * 2 * B2 * kBandGroup);
+    d.WV = ctx.arena.alloc_n<double>((size_t)n * 2 * B2 * kBandGroup);
+    d.Y = ctx.arena.alloc_n<double>((size_t)n * B2);
+    d.Z1 = ctx.arena.alloc_n<double>((size_t)2 * B2 * kBandGroup * B2);
+    d.P1 = ctx.arena.alloc_n<double>((size_t)B2 * B2);
+    d.Mb = ctx.arena.alloc_n<double>((size_t)B2 * B2);
+    d.shifts = ctx.arena.alloc_n<double>(d.kk);
+    d.cstarts = ctx.arena.alloc_n<int>(d.kk);
+    d.vals_only = band_invit ? 1 : 2;
+    if (!band_invit) {
+      long long steps = 0;  // chase reflectors of all sweeps
+      for (int s2 = 0; s2 <= n - 3; ++s2) steps += (n - 3 - s2) / B2 + 1;
+      d.refl = ctx.arena.alloc_n<double>((size_t)std::max(1LL, steps) * (B2 + 1));
+    }
+    HSVD_CUDA(cudaMemsetAsync(d.band, 0, (size_t)LDBB * n * sizeof(double), ctx.stream));
+    lu_slot_max = std::max(lu_slot_max, (size_t)n * (2 * B2 + 1 + B2 + 3));
+  }
+  // band LU workspaces (INV_WARPS slots per matrix; slot size of the largest n)
+  // shifts spread over cpm CTAs per matrix (3 CTAs fit an SM), workspace
+  // capped at 8 GB
+  int cpm = std::max(1, std::min(ceil_div(3 * ctx.num_sms, count), ceil_div(kkmax, INV_WARPS)));
+  while (cpm > 1 && lu_slot_max * sizeof(double) * INV_WARPS * cpm * count > (size_t(8) << 30)) --cpm;
+  const int q2nc = std::max(1, q2_cols(nmax));
+  const int q2x = ceil_div(kkmax, q2nc);
+  if (band_invit) {
+    double* lu = ctx.arena.alloc_n<double>(lu_slot_max * INV_WARPS * cpm * count);
+    for (int g = 0; g < count; ++g) {  // indexed by blockIdx.x in the kernel
+      dev[g].lu = lu;
+      dev[g].lu_slot = (long long)lu_slot_max;
+    }
+  }
+  const EigDev* dd = upload_jobs(ctx, dev);
+
+  // stage 1: dense -> band.  The trailing update is delayed over groups of
+  // kBandGroup panels: inside a group the panels' [V|W] pairs accumulate in
+  // VW / WV (64 columns per panel), the next panel's columns and its
+  // Y = A22 V are corrected with the pending pairs (small GEMMs with K = 64g),
+  // and one SYR2K with K = 64 * kBandGroup updates the trailing matrix at the
+  // end of the group (a quarter of the passes over A22).
+  SubPhase sp1(ctx, "band");
+  std::vector<GemmDesc> gc, g1, gz, gy, g2, g3, g4, g5, g6;
+  for (int p = 0; p < npan; ++p) {
+    const int j0 = p * B2, r0 = j0 + B2;
+    const int gi = p % kBandGroup;        // panel index inside its group
+    const int vcol = 2 * B2 * gi;         // its [V|W] columns in VW / WV
+    const bool last_in_group = gi == kBandGroup - 1 || p == npan - 1;
+    if (gi > 0) {  // columns j0..j0+B2 (rows j0..n) with the pending updates
+      SubPhase sc(ctx, "band.corr");
+      gc.clear();
+      for (int g = 0; g < count; ++g) {
+        const EigDev& e = dev[g];
+        if (j0 >= e.n) continue;
+        const int rows = e.n - j0, cols = std::min(B2, e.n - j0);
+        gc.push_back({e.VW + j0, e.WV + j0, e.A + j0 + (long long)j0 * e.lda, e.n, e.n, e.lda, rows,
+                      cols, vcol, -1.0, 1.0});
+      }
+      gemm_grouped(ctx, DType::F64, DType::F64, false, true, false, gc);
+    }
+    launch_panel_qr(ctx, count, std::max(0, nmax - r0), dd, j0, vcol);
+    g1.clear(); gz.clear(); gy.clear(); g2.clear(); g3.clear(); g4.clear(); g5.clear(); g6.clear();
+    for (int g = 0; g < count; ++g) {
+      const EigDev& e = dev[g];
+      const int n = e.n;
+      if (r0 > n - 2) continue;
+      const int m = n - r0;
+      double* A22 = e.A + r0 + (long long)r0 * e.lda;
+      const double* V = e.A + r0 + (long long)j0 * e.lda;
+      const double* Tp = e.Tp + (long long)p * B2 * B2;
+      double* X = e.VW + r0 + (long long)(vcol + B2) * n;
+      g1.push_back({A22, V, e.Y + r0, e.lda, e.lda, n, m, B2, m, 1.0, 0.0});       // Y = A22 V
+      if (gi > 0) {
+        gz.push_back({e.WV + r0, V, e.Z1, n, e.lda, vcol, vcol, B2, m, 1.0, 0.0});  // Z1 = WV^T V
+        gy.push_back({e.VW + r0, e.Z1, e.Y + r0, n, vcol, n, m, B2, vcol, -1.0, 1.0});  // Y -= VW Z1
+      }
+      g2.push_back({e.Y + r0, Tp, X, n, B2, n, m, B2, B2, 1.0, 0.0});               // X = Y T
+      g3.push_back({V, X, e.P1, e.lda, n, B2, B2, B2, m, 1.0, 0.0});                // P1 = V^T X
+      g4.push_back({Tp, e.P1, e.Mb, B2, B2, B2, B2, B2, B2, 1.0, 0.0});             // M = T^T P1
+      g5.push_back({V, e.Mb, X, e.lda, B2, n, m, B2, B2, -0.5, 1.0});               // W = X - V M/2
+      if (last_in_group)                                                             // syr2k
+        g6.push_back({e.VW + r0, e.WV + r0, A22, n, n, e.lda, m, m, vcol + 2 * B2, -1.0, 1.0});
+    }
+    if (g1.empty()) {
+      ctx.launch_begin();
+      k_copy_w<<<dim3(1, count), 256, 0, ctx.stream>>>(dd, j0, vcol);
+      ctx.check_launch("k_copy_w");
+      continue;
+    }
+    {
+      SubPhase sy(ctx, "band.y");
+      gemm_grouped(ctx, DType::F64, DType::F64, false, false, false, g1);
+      if (!gz.empty()) {
+        gemm_grouped(ctx, DType::F64, DType::F64, true, false, false, gz);
+        gemm_grouped(ctx, DType::F64, DType::F64, false, false, false, gy);
+      }
+    }
+    {
+      SubPhase sw(ctx, "band.w");
+      gemm_grouped(ctx, DType::F64, DType::F64, false, false, false, g2);
+      gemm_grouped(ctx, DType::F64, DType::F64, true, false, false, g3);
+      gemm_grouped(ctx, DType::F64, DType::F64, true, false, false, g4);
+      gemm_grouped(ctx, DType::F64, DType::F64, false, false, false, g5);
+      ctx.launch_begin();
+      k_copy_w<<<dim3(256, count), 256, 0, ctx.stream>>>(dd, j0, vcol);
+      ctx.check_launch("k_copy_w");
+    }
+    if (!g6.empty()) {
+      SubPhase s2k(ctx, "band.syr2k");
+      gemm_grouped(ctx, DType::F64, DType::F64, false, true, true, g6);
+    }
+  }
+  if (band_invit)  // the band before the chase, for the band inverse iteration
+    for (int g = 0; g < count; ++g)
+      HSVD_CUDA(cudaMemcpyAsync(dev[g].band0, dev[g].band, (size_t)LDBB * dev[g].n * sizeof(double),
+                                cudaMemcpyDeviceToDevice, ctx.stream));
+  // stage 2: band -> tridiagonal (values), eigenvalues by bisection
+  SubPhase sp2(ctx, "tri");
+  ctx.launch_begin();
+  // spread each matrix's sweeps over a cluster while SMs would idle
+  int ccs = 1;
+  while (ccs < 2 && count * ccs * 2 <= ctx.num_sms) ccs *= 2;  // 4 measured slower
+  if (const char* env = std::getenv("HSVD_CHASE_CS")) ccs = std::max(1, std::atoi(env));
+  if (ccs == 1) {
+    k_chase<false><<<count, CHASE_WARPS * 32, 0, ctx.stream>>>(dd, 1);
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(count * ccs);
+    cfg.blockDim = dim3(CHASE_WARPS * 32);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = ctx.stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = ccs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    HSVD_CUDA(cudaLaunchKernelEx(&cfg, k_chase<true>, dd, ccs));
+  }
+  ctx.check_launch("k_chase");
+  launch_steig(ctx, dd, count, nmax, kkmax);
+  // eigenvectors of the band matrix
+  if (!band_invit) {
+    launch_band_mgs(ctx, dd, count);  // clusters of the tridiagonal's vectors
+    ctx.launch_begin();
+    const size_t q2smem = q2_smem(nmax, q2nc);
+    if (q2nc == 8) {
+      smem_optin(k_q2_apply<8>, q2smem);
+      k_q2_apply<8><<<dim3(q2x, count), Q2_WARPS * 32, q2smem, ctx.stream>>>(dd);
+    } else if (q2nc == 4) {
+      smem_optin(k_q2_apply<4>, q2smem);
+      k_q2_apply<4><<<dim3(q2x, count), Q2_WARPS * 32, q2smem, ctx.stream>>>(dd);
+    } else {
+      smem_optin(k_q2_apply<2>, q2smem);
+      k_q2_apply<2><<<dim3(q2x, count), Q2_WARPS * 32, q2smem, ctx.stream>>>(dd);
+    }
+    ctx.check_launch("k_q2_apply");
+  } else {
+    const size_t smem =
+        ((size_t)INV_WARPS * ((B2 + 1) * (2 * B2 + 1) + INV_RING) + 64) * sizeof(double);
+    smem_optin(k_band_invit, smem);
+    ctx.launch_begin();
+    k_band_invit<<<dim3(cpm, count), INV_WARPS * 32, smem, ctx.stream>>>(dd);
+    ctx.check_launch("k_band_invit");
+    launch_band_mgs(ctx, dd, count);
+  }
+  // back through the stage-1 reflectors
+  SubPhase sp3(ctx, "back");
+  back_transform(ctx, jobs, dev, dd, nmax, B2);
+}
+
+}  // namespace syev_impl
+}  // namespace hsvdcu
