@@ -595,43 +595,103 @@ __global__ void __launch_bounds__(EIG_THREADS) k_steig(const EigDev* __restrict_
     return;
   }
   const double tiny = eps * tnorm;
+  // The iterates and pivots live in the scratch J.piv in row-major [n][kk]
+  // layout: thread t walks its vector row by row, so a warp's accesses to
+  // one row are coalesced.  They stream through registers IC rows at a time,
+  // the next chunk's loads issued before the current chunk's recurrence.
+  constexpr int IC = 8;
+  const long long nk = (long long)n * kk;
+  double* const Dt = J.piv;       // pivots of L D L^T = T - shift_t I (column t)
+  double* const Zt = J.piv + nk;  // iterates
   // start vectors (deterministic pseudo-random, dstein uses dlarnv uniform(-1,1))
-  for (int t = tid; t < kk; t += nt) {
-    double* z = J.Z + (long long)t * J.ldz;
-    for (int r = 0; r < n; ++r) {
-      const unsigned h = hash32((unsigned)r * 2654435761u ^ hash32((unsigned)t + 0x9e3779b9u));
-      z[r] = ((double)h / 4294967296.0) * 2.0 - 1.0;
-    }
+  for (long long e = tid; e < nk; e += nt) {
+    const int r = (int)(e / kk), t = (int)(e % kk);
+    const unsigned h = hash32((unsigned)r * 2654435761u ^ hash32((unsigned)t + 0x9e3779b9u));
+    Zt[e] = ((double)h / 4294967296.0) * 2.0 - 1.0;
   }
   __syncthreads();
 
   for (int it = 0; it < 3; ++it) {
     for (int t = tid; t < kk; t += nt) {
       const double s = shift[t];
-      double* z = J.Z + (long long)t * J.ldz;
-      double* Dw = J.piv + (long long)t * n;
+      double* z = Zt + t;  // row r at z[r * kk]
+      double* Dw = Dt + t;
+      auto at = [&](int r) { return (long long)r * kk; };
       double D = guard_pivot(dd[0] - s, tiny);
       Dw[0] = D;
       double y = z[0];
-      for (int r = 1; r < n; ++r) {
-        const double l = ee[r - 1] / D;
-        D = guard_pivot(dd[r] - s - l * ee[r - 1], tiny);
-        Dw[r] = D;
-        y = z[r] - l * y;
-        z[r] = y;
+      double nz[IC], nd[IC];
+#pragma unroll
+      for (int j = 0; j < IC; ++j) nz[j] = 1 + j < n ? z[at(1 + j)] : 0.0;
+      for (int r0 = 1; r0 < n; r0 += IC) {
+        double cz[IC], cd[IC];
+#pragma unroll
+        for (int j = 0; j < IC; ++j) cz[j] = nz[j];
+#pragma unroll
+        for (int j = 0; j < IC; ++j) nz[j] = r0 + IC + j < n ? z[at(r0 + IC + j)] : 0.0;
+#pragma unroll
+        for (int j = 0; j < IC; ++j) {
+          const int r = r0 + j;
+          if (r < n) {
+            const double l = ee[r - 1] / D;
+            D = guard_pivot(dd[r] - s - l * ee[r - 1], tiny);
+            cd[j] = D;
+            y = cz[j] - l * y;
+            cz[j] = y;
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < IC; ++j)
+          if (r0 + j < n) {
+            z[at(r0 + j)] = cz[j];
+            Dw[at(r0 + j)] = cd[j];
+          }
       }
-      double zr = z[n - 1] / Dw[n - 1];
-      z[n - 1] = zr;
+      double zr = z[at(n - 1)] / Dw[at(n - 1)];
+      z[at(n - 1)] = zr;
       double nrm2 = zr * zr;
-      for (int r = n - 2; r >= 0; --r) {
-        zr = (z[r] - ee[r] * zr) / Dw[r];
-        z[r] = zr;
-        nrm2 += zr * zr;
+#pragma unroll
+      for (int j = 0; j < IC; ++j) {
+        nz[j] = n - 2 - j >= 0 ? z[at(n - 2 - j)] : 0.0;
+        nd[j] = n - 2 - j >= 0 ? Dw[at(n - 2 - j)] : 1.0;
+      }
+      for (int r0 = n - 2; r0 >= 0; r0 -= IC) {
+        double cz[IC], cd[IC];
+#pragma unroll
+        for (int j = 0; j < IC; ++j) {
+          cz[j] = nz[j];
+          cd[j] = nd[j];
+        }
+#pragma unroll
+        for (int j = 0; j < IC; ++j) {
+          const int r = r0 - IC - j;
+          nz[j] = r >= 0 ? z[at(r)] : 0.0;
+          nd[j] = r >= 0 ? Dw[at(r)] : 1.0;
+        }
+#pragma unroll
+        for (int j = 0; j < IC; ++j) {
+          const int r = r0 - j;
+          if (r >= 0) {
+            zr = (cz[j] - ee[r] * zr) / cd[j];
+            cz[j] = zr;
+            nrm2 += zr * zr;
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < IC; ++j)
+          if (r0 - j >= 0) z[at(r0 - j)] = cz[j];
       }
       double sc = 1.0 / sqrt(nrm2);
       if (!isfinite(sc) || nrm2 == 0.0) sc = 0.0;
-      for (int r = 0; r < n; ++r) z[r] *= sc;
-      if (sc == 0.0) z[t % n] = 1.0;
+      for (int r0 = 0; r0 < n; r0 += IC) {
+        double cz[IC];
+#pragma unroll
+        for (int j = 0; j < IC; ++j) cz[j] = r0 + j < n ? z[at(r0 + j)] : 0.0;
+#pragma unroll
+        for (int j = 0; j < IC; ++j)
+          if (r0 + j < n) z[at(r0 + j)] = cz[j] * sc;
+      }
+      if (sc == 0.0) z[at(t % n)] = 1.0;
     }
     __syncthreads();
     if (it == 0 || J.vals_only == 2) continue;
@@ -639,28 +699,44 @@ __global__ void __launch_bounds__(EIG_THREADS) k_steig(const EigDev* __restrict_
     for (int t = 0; t < kk; ++t) {
       const int cs = cstart[t];
       if (cs == t) continue;
-      double* zt = J.Z + (long long)t * J.ldz;
+      double* zt = Zt + t;
       for (int rep = 0; rep < 2; ++rep) {
         for (int c = cs + warp; c < t; c += nwarps) {
-          const double* zc = J.Z + (long long)c * J.ldz;
+          const double* zc = Zt + c;
           double s = 0.0;
-          for (int r = lane; r < n; r += 32) s += zc[r] * zt[r];
+          for (int r = lane; r < n; r += 32) s += zc[(long long)r * kk] * zt[(long long)r * kk];
           s = warp_sum(s);
           if (lane == 0) dots[c - cs] = s;
         }
         __syncthreads();
         for (int r = tid; r < n; r += nt) {
-          double a = zt[r];
-          for (int c = cs; c < t; ++c) a -= dots[c - cs] * J.Z[r + (long long)c * J.ldz];
-          zt[r] = a;
+          double a = zt[(long long)r * kk];
+          for (int c = cs; c < t; ++c) a -= dots[c - cs] * Zt[(long long)r * kk + c];
+          zt[(long long)r * kk] = a;
         }
         __syncthreads();
       }
       double part = 0.0;
-      for (int r = tid; r < n; r += nt) part += zt[r] * zt[r];
+      for (int r = tid; r < n; r += nt) part += zt[(long long)r * kk] * zt[(long long)r * kk];
       const double nrm2 = block_sum(part, red);
       const double sc = nrm2 > 0.0 ? 1.0 / sqrt(nrm2) : 0.0;
-      for (int r = tid; r < n; r += nt) zt[r] *= sc;
+      for (int r = tid; r < n; r += nt) zt[(long long)r * kk] *= sc;
+      __syncthreads();
+    }
+  }
+  // iterates -> Z (column-major), R rows at a time through shared memory
+  // (the tridiagonal's dd, ee, e2 are dead: 3n doubles)
+  {
+    double* stage = sm;
+    const int R = max(1, min(n, 3 * n / kk));
+    for (int r0 = 0; r0 < n; r0 += R) {
+      const int rows = min(R, n - r0);
+      for (int e = tid; e < rows * kk; e += nt) stage[e] = Zt[(long long)r0 * kk + e];
+      __syncthreads();
+      for (int e = tid; e < rows * kk; e += nt) {
+        const int i = e % rows, t = e / rows;
+        J.Z[(long long)t * J.ldz + r0 + i] = stage[i * kk + t];
+      }
       __syncthreads();
     }
   }
@@ -999,7 +1075,7 @@ void eig_topk(Ctx& ctx, const std::vector<EigJob>& jobs_in) {
     d.lam = j.lam;
     d.Z = j.Z;
     d.ldz = j.ldz;
-    d.piv = ctx.arena.alloc_n<double>((size_t)j.n * j.kk);
+    d.piv = ctx.arena.alloc_n<double>((size_t)2 * j.n * j.kk);  // k_steig: pivots + iterates
     // inverse iteration without the in-iteration Gram-Schmidt; clusters are
     // orthonormalised once afterwards by the blocked k_band_mgs
     // (HSVD_STEIG_INLINE_GS=1: dstein's per-iteration MGS inside k_steig)

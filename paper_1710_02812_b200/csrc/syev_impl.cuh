@@ -46,7 +46,7 @@ struct EigDev {
   double* lam;
   double* Z;
   long long ldz;
-  double* piv;   // n * kk scratch (LDL^T pivots)
+  double* piv;   // 2 * n * kk scratch (k_steig: LDL^T pivots + iterates, [n][kk])
   double* T;     // (nblocks * NBT * NBT) compact-WY T factors
   double* S;     // (nblocks * NBT * NBT) V^T V of each reflector block
   double* VW;    // n x 2*NB panel [V | W] (blocked tridiagonalisation)
