@@ -504,10 +504,10 @@ __global__ void __launch_bounds__(CHASE_WARPS * 32, 1) k_chase(const EigDev* __r
 // CTA per NC eigenvectors keeps its n x NC slice of Z in shared memory for
 // the whole pass (row-major; lane = column x row group, rows interleaved so
 // a warp's accesses are conflict-free).  The reflectors of one sweep touch
-// disjoint 32-row blocks: the CTA's 8 warps share a sweep's blocks and
+// disjoint 32-row blocks: the CTA's Q2_WARPS warps share a sweep's blocks and
 // synchronise once per sweep, with the next sweep's reflectors staged into
 // shared memory by cp.async while the current one is applied.
-constexpr int Q2_WARPS = 8;
+constexpr int Q2_WARPS = 16;  // measured on B200 (cfg2 leaves): 8 -> 25.1 ms, 16 -> 21.9, 32 -> 23.5
 
 template <int NC>
 __global__ void __launch_bounds__(Q2_WARPS * 32) k_q2_apply(const EigDev* __restrict__ jobs) {

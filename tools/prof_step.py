@@ -16,6 +16,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=2)
 ap.add_argument("--steps", type=int, default=1)
 ap.add_argument("--rows", type=int, default=0, help="use only the first ROWS rows (P scaled)")
+ap.add_argument("--top", type=int, default=8, help="kernels listed")
 a = ap.parse_args()
 w = configs.WORKLOADS[a.config]
 if a.rows:
@@ -32,4 +33,4 @@ prof = ctx.profile_report()
 tot = sum(v[1] for v in prof.values())
 print(json.dumps({"workload": w.name, "total_ms": tot / a.steps,
                   "top": sorted(((k, v[0], round(v[1] / a.steps, 3)) for k, v in prof.items()),
-                                key=lambda t: -t[2])[:8]}))
+                                key=lambda t: -t[2])[:a.top]}))
