@@ -17,11 +17,13 @@
 // copies are coalesced and the fragment reads conflict-free.  Tiles: 64x64
 // (2x2 warps) or, for skinny outputs (N <= 32), 128x32 (4x1 warps); each
 // warp owns 32x32 = 4x4 DMMA tiles; BK = 16.  C reads are batched before the
-// stores.  Optional split-K with a deterministic fixed-order reduction
+// stores.  Split-K (chosen against the wave count of the resident CTA slots)
+// with a deterministic fixed-order reduction
 // (run-to-run bitwise stable).  SYRK mode computes the lower tile
 // triangle and mirrors it through a shared-memory transpose (or not, with
 // kGemmLowerOnly).
 #include <algorithm>
+#include <atomic>
 
 #include "gemm.h"
 
@@ -272,6 +274,63 @@ void launch_tile(Ctx& ctx, bool ta, bool tb, dim3 grid, const GemmDesc* dd, int 
   ctx.check_launch("k_gemm");
 }
 
+// Resident CTAs per SM of one instantiation (cached: every device of a run
+// is the same B200 part).
+template <typename TA, typename TB, bool TRA, bool TRB, int BM, int BN>
+int occupancy_t() {
+  static std::atomic<int> cached{0};
+  int occ = cached.load(std::memory_order_relaxed);
+  if (occ > 0) return occ;
+  constexpr size_t smem = GemmShape<TA, TB, TRA, TRB, BM, BN>::SMEM;
+  auto* k = k_gemm<TA, TB, TRA, TRB, BM, BN>;
+  smem_optin(k, smem);
+  HSVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NT, smem));
+  occ = std::max(1, occ);
+  cached.store(occ, std::memory_order_relaxed);
+  return occ;
+}
+
+template <typename TA, typename TB, int BM, int BN>
+int occupancy_tile(bool ta, bool tb) {
+  if (!ta && !tb) return occupancy_t<TA, TB, false, false, BM, BN>();
+  if (!ta && tb) return occupancy_t<TA, TB, false, true, BM, BN>();
+  if (ta && !tb) return occupancy_t<TA, TB, true, false, BM, BN>();
+  return occupancy_t<TA, TB, true, true, BM, BN>();
+}
+
+template <typename TA, typename TB>
+int occupancy_typed(bool ta, bool tb, bool skinny) {
+  return skinny ? occupancy_tile<TA, TB, 128, 32>(ta, tb) : occupancy_tile<TA, TB, 64, 64>(ta, tb);
+}
+
+int occupancy(DType a, DType b, bool ta, bool tb, bool skinny) {
+  if (a == DType::F64 && b == DType::F64) return occupancy_typed<double, double>(ta, tb, skinny);
+  if (a == DType::F32 && b == DType::F64) return occupancy_typed<float, double>(ta, tb, skinny);
+  if (a == DType::F64 && b == DType::F32) return occupancy_typed<double, float>(ta, tb, skinny);
+  return occupancy_typed<float, float>(ta, tb, skinny);
+}
+
+// Split-K factor: minimises (waves of CTAs) x (K per CTA + a fixed
+// prologue/epilogue cost), so a grid that would leave most of its last wave
+// empty is split instead (K per split >= 128; one extra cost unit for the
+// reduction launch).
+int choose_splits(long long tiles, int maxK, long long slots, int count) {
+  constexpr double kFixed = 64.0;
+  const int smax = std::min(128, maxK / 128);
+  int best = 1;
+  double best_cost = (double)((tiles + slots - 1) / slots) * (maxK + kFixed);
+  for (int s = 2; s <= smax; ++s) {
+    if ((long long)count * s > 65535) break;
+    const double waves = (double)((tiles * s + slots - 1) / slots);
+    const double cost = waves * ((double)maxK / s + kFixed) + kFixed;
+    if (cost < best_cost * 0.97) {
+      best_cost = cost;
+      best = s;
+    }
+  }
+  return best;
+}
+
 template <typename TA, typename TB>
 void launch_typed(Ctx& ctx, bool ta, bool tb, bool skinny, int maxM, int maxN, int count,
                   const GemmDesc* dd, int mode, int splits, double* ws, long long slot) {
@@ -312,13 +371,8 @@ void gemm_grouped(Ctx& ctx, DType ta, DType tb, bool trans_a, bool trans_b, bool
     flops += syrk ? (double)d.M * (d.M + 1) * d.K : 2.0 * d.M * d.N * d.K;
   }
 
-  int splits = 1;
-  const long long target = 4LL * ctx.num_sms;
-  if (tiles < target && maxK >= 2 * 256) {
-    splits = static_cast<int>(std::min<long long>((target + tiles - 1) / tiles, maxK / 256));
-    splits = std::max(1, std::min(splits, 128));
-    while (splits > 1 && (long long)count * splits > 65535) --splits;
-  }
+  const long long slots = (long long)ctx.num_sms * occupancy(ta, tb, trans_a, trans_b, skinny);
+  const int splits = choose_splits(tiles, maxK, slots, count);
   const GemmDesc* dd =
       static_cast<const GemmDesc*>(ctx.staging.put(live.data(), live.size() * sizeof(GemmDesc),
                                                    ctx.stream));
