@@ -16,7 +16,7 @@
 // keeps the memory-contiguous dimension contiguous in shared memory, so the
 // copies are coalesced and the fragment reads conflict-free.  Tiles: 64x64
 // (2x2 warps) or, for skinny outputs (N <= 32), 128x32 (4x1 warps); each
-// warp owns 32x32 = 4x4 DMMA tiles; BK = 16.  C reads are batched before the
+// warp owns 32x32 = 4x4 DMMA tiles; BK = 16, 3 stages (skinny: 2).  C reads are batched before the
 // stores.  Split-K (chosen against the wave count of the resident CTA slots)
 // with a deterministic fixed-order reduction
 // (run-to-run bitwise stable).  SYRK mode computes the lower tile
@@ -31,7 +31,21 @@ namespace hsvdcu {
 
 namespace {
 
-constexpr int BK = 16, NT = 128, STAGES = 3;
+constexpr int NT = 128;
+
+// k depth and pipeline stages per tile shape.  The skinny 128x32 tile
+// streams a large A against a small B and is bound by resident warps (4 CTAs
+// per SM at 128 registers): double buffering keeps its shared memory small
+// (measured on the config-2 Y = A22 V launches: BK/stages 16/3 -> 37.4 ms,
+// 8/4 -> 33.5, 16/2 -> 32.2; forcing 5-6 CTAs per SM spills and loses).
+template <int BM, int BN>
+struct TileCfg {
+  static constexpr int BK = 16, STAGES = 3;
+};
+template <>
+struct TileCfg<128, 32> {
+  static constexpr int BK = 16, STAGES = 2;
+};
 constexpr int kModeSyrk = 1, kModeLower = 2;  // mode bits
 
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
@@ -56,7 +70,7 @@ __device__ __forceinline__ void cp_async_wait() {
 // Shared layout of one operand tile (R rows of the output dimension, BK of
 // k): KF (k contiguous in memory) -> [R][BK + 4]; else [BK][R + pad] with
 // the pad chosen so a warp's 8x4 fragment reads hit distinct banks.
-template <typename T, int R, bool KF>
+template <typename T, int R, bool KF, int BK>
 struct OpTile {
   static constexpr int PAD = sizeof(T) == 4 ? 8 : 4;
   static constexpr int LD = KF ? BK + 4 : R + PAD;
@@ -67,8 +81,9 @@ struct OpTile {
 
 template <typename TA, typename TB, bool TRA, bool TRB, int BM, int BN>
 struct GemmShape {
-  using TAt = OpTile<TA, BM, TRA>;
-  using TBt = OpTile<TB, BN, !TRB>;
+  static constexpr int BK = TileCfg<BM, BN>::BK, STAGES = TileCfg<BM, BN>::STAGES;
+  using TAt = OpTile<TA, BM, TRA, BK>;
+  using TBt = OpTile<TB, BN, !TRB, BK>;
   static constexpr size_t STAGE_BYTES = TAt::BYTES + TBt::BYTES;
   static constexpr size_t TILE_BYTES = (size_t)BM * (BN + 1) * sizeof(double);  // mirror staging
   static constexpr size_t SMEM =
@@ -84,6 +99,7 @@ __global__ void __launch_bounds__(NT) k_gemm(const GemmDesc* __restrict__ descs,
   using Sh = GemmShape<TA, TB, TRA, TRB, BM, BN>;
   using TAt = typename Sh::TAt;
   using TBt = typename Sh::TBt;
+  constexpr int BK = Sh::BK, STAGES = Sh::STAGES;
   constexpr int WN = BN / 32;
   constexpr int LA = BM * BK / NT, LB = BN * BK / NT;
   extern __shared__ __align__(16) unsigned char smem[];
