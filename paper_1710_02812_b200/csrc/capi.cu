@@ -7,6 +7,8 @@
 #include <memory>
 #include <new>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "../../include/hsvd_cu.h"
 #include "comm.h"
@@ -219,6 +221,46 @@ int check_result(const hsvd_cu_result* r) {
   return HSVD_CU_OK;
 }
 
+// Device -> caller host memory.  Large results go through two pinned chunks
+// alternately: the DMA of one chunk overlaps the host copy of the previous
+// one, and that host copy (which also faults in the caller's fresh pages,
+// the slow part for pageable memory) is split over several threads.
+void copy_to_host(Ctx& c, void* dst, const void* src, size_t bytes) {
+  constexpr size_t kSmall = size_t(8) << 20;
+  if (bytes < kSmall) {
+    HSVD_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c.stream));
+    HSVD_CUDA(cudaStreamSynchronize(c.stream));
+    return;
+  }
+  c.ensure_d2h_stage();
+  constexpr size_t kChunk = Ctx::kD2hChunk;
+  char* d = static_cast<char*>(dst);
+  const char* s = static_cast<const char*>(src);
+  const size_t nch = (bytes + kChunk - 1) / kChunk;
+  auto len_of = [&](size_t i) { return std::min(kChunk, bytes - i * kChunk); };
+  auto issue = [&](size_t i) {
+    HSVD_CUDA(cudaMemcpyAsync(c.d2h_pin[i & 1], s + i * kChunk, len_of(i), cudaMemcpyDeviceToHost,
+                              c.stream));
+    HSVD_CUDA(cudaEventRecord(c.d2h_ev[i & 1], c.stream));
+  };
+  const unsigned hw = std::thread::hardware_concurrency();
+  const size_t nt = std::max(1u, std::min(8u, hw == 0 ? 1u : hw));
+  issue(0);
+  if (nch > 1) issue(1);
+  for (size_t i = 0; i < nch; ++i) {
+    HSVD_CUDA(cudaEventSynchronize(c.d2h_ev[i & 1]));
+    const size_t len = len_of(i), part = (len + nt - 1) / nt;
+    const char* from = static_cast<const char*>(c.d2h_pin[i & 1]);
+    char* to = d + i * kChunk;
+    std::vector<std::thread> th;
+    for (size_t t = 1; t < nt && t * part < len; ++t)
+      th.emplace_back([=] { std::memcpy(to + t * part, from + t * part, std::min(part, len - t * part)); });
+    std::memcpy(to, from, std::min(part, len));
+    for (auto& x : th) x.join();
+    if (i + 2 < nch) issue(i + 2);
+  }
+}
+
 int copy_side(const hsvd_cu_result* r, const double* src, long long ld, long long rows, double* out) {
   if (int s = check_result(r)) return s;
   if (!src) return fail(HSVD_CU_EINVAL, "result has no such factor");
@@ -228,8 +270,7 @@ int copy_side(const hsvd_cu_result* r, const double* src, long long ld, long lon
     Arena::Mark mk = c.arena.mark();
     double* tmp = c.arena.alloc_n<double>((size_t)rows * r->rank);
     colmajor_to_rowmajor(c, src, ld, (int)rows, r->rank, tmp, r->rank);
-    HSVD_CUDA(cudaMemcpyAsync(out, tmp, (size_t)rows * r->rank * 8, cudaMemcpyDeviceToHost, c.stream));
-    HSVD_CUDA(cudaStreamSynchronize(c.stream));
+    copy_to_host(c, out, tmp, (size_t)rows * r->rank * 8);
     c.arena.release(mk);
     return HSVD_CU_OK;
   });

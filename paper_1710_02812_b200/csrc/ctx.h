@@ -198,6 +198,16 @@ struct Ctx {
     }
     return h_dbl;
   }
+  // two pinned chunks for large device->host result copies (copy_to_host)
+  static constexpr size_t kD2hChunk = size_t(32) << 20;
+  void* d2h_pin[2] = {nullptr, nullptr};
+  cudaEvent_t d2h_ev[2] = {nullptr, nullptr};
+  void ensure_d2h_stage() {
+    for (int i = 0; i < 2; ++i) {
+      if (!d2h_pin[i]) HSVD_CUDA(cudaMallocHost(&d2h_pin[i], kD2hChunk));
+      if (!d2h_ev[i]) HSVD_CUDA(cudaEventCreateWithFlags(&d2h_ev[i], cudaEventDisableTiming));
+    }
+  }
   // side stream for host->device input copies that overlap the compute
   // stream, and the events marking the copied row chunks
   cudaStream_t copy_stream = nullptr;
@@ -222,6 +232,10 @@ struct Ctx {
     }
     if (h_ints) cudaFreeHost(h_ints);
     if (h_dbl) cudaFreeHost(h_dbl);
+    for (int i = 0; i < 2; ++i) {
+      if (d2h_ev[i]) cudaEventDestroy(d2h_ev[i]);
+      if (d2h_pin[i]) cudaFreeHost(d2h_pin[i]);
+    }
     for (auto& r : prof) {
       cudaEventDestroy(r.a);
       cudaEventDestroy(r.b);
