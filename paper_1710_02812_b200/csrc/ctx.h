@@ -99,8 +99,15 @@ class Arena {
   size_t cur_ = 0, off_ = 0, peak_ = 0;
 };
 
+// Device copy of `bytes` from pinned (mapped) host memory by a one-CTA
+// kernel on stream s: no copy engine involved (staging.cu).
+void copy_mapped_to_device(void* dst, const void* host_src, size_t bytes, cudaStream_t s);
+
 // Pinned host ring mirrored on the device: small descriptor arrays are
-// written on the host and copied with one cudaMemcpyAsync per launch.
+// written on the host and copied with one cudaMemcpyAsync per launch --
+// or, while a large input transfer occupies the host->device copy engine
+// (set_zero_copy), read straight from the mapped ring by a small kernel, so
+// the compute stream does not queue behind the whole input copy.
 class Staging {
  public:
   void init(size_t bytes) {
@@ -127,15 +134,20 @@ class Staging {
     char* h = static_cast<char*>(host_) + off_;
     char* d = dst ? static_cast<char*>(dst) : static_cast<char*>(dev_) + off_;
     std::memcpy(h, src, bytes);
-    HSVD_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s));
+    if (zero_copy_)
+      copy_mapped_to_device(d, h, bytes, s);
+    else
+      HSVD_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s));
     off_ += b;
     return d;
   }
+  void set_zero_copy(bool on) { zero_copy_ = on; }
 
  private:
   void* host_ = nullptr;
   void* dev_ = nullptr;
   size_t size_ = 0, off_ = 0;
+  bool zero_copy_ = false;
 };
 
 // Opt a kernel in to the device's full dynamic shared memory, once per
