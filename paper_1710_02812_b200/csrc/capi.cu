@@ -255,8 +255,14 @@ void copy_to_host(Ctx& c, void* dst, const void* src, size_t bytes) {
     const char* from = static_cast<const char*>(c.d2h_pin[i & 1]);
     char* to = d + i * kChunk;
     std::vector<std::thread> th;
-    for (size_t t = 1; t < nt && t * part < len; ++t)
-      th.emplace_back([=] { std::memcpy(to + t * part, from + t * part, std::min(part, len - t * part)); });
+    for (size_t t = 1; t < nt && t * part < len; ++t) {
+      auto piece = [=] { std::memcpy(to + t * part, from + t * part, std::min(part, len - t * part)); };
+      try {
+        th.emplace_back(piece);
+      } catch (...) {  // no thread available: copy this piece here
+        piece();
+      }
+    }
     std::memcpy(to, from, std::min(part, len));
     for (auto& x : th) x.join();
     if (i + 2 < nch) issue(i + 2);
