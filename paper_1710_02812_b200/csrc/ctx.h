@@ -114,6 +114,8 @@ class Staging {
     size_ = bytes;
     HSVD_CUDA(cudaMallocHost(&host_, bytes));
     HSVD_CUDA(cudaMalloc(&dev_, bytes));
+    // the device's address of the (mapped) pinned ring, for zero-copy reads
+    HSVD_CUDA(cudaHostGetDevicePointer(&host_dev_, host_, 0));
   }
   ~Staging() {
     if (host_) cudaFreeHost(host_);
@@ -135,7 +137,7 @@ class Staging {
     char* d = dst ? static_cast<char*>(dst) : static_cast<char*>(dev_) + off_;
     std::memcpy(h, src, bytes);
     if (zero_copy_)
-      copy_mapped_to_device(d, h, bytes, s);
+      copy_mapped_to_device(d, static_cast<char*>(host_dev_) + off_, bytes, s);
     else
       HSVD_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s));
     off_ += b;
@@ -145,6 +147,7 @@ class Staging {
 
  private:
   void* host_ = nullptr;
+  void* host_dev_ = nullptr;  // device address of host_
   void* dev_ = nullptr;
   size_t size_ = 0, off_ = 0;
   bool zero_copy_ = false;
