@@ -298,8 +298,6 @@ __device__ __forceinline__ bool chase_step(double* bb, int c, int r0, int L, int
     const double* pa = lane >= j ? pa1 + j * (LD - 1) : pa2 + j;
     ar[j] = (lx && (FULL || j < L)) ? band_ld<CG>(pa) : 0.0;
   }
-#pragma unroll
-  for (int j = 0; j < B2; ++j) ya[j] = (ly && (FULL || j < L)) ? band_ld<CG>(pya + j * (LD - 1)) : 0.0;
   const double xn2 = warp_sum(lane >= 1 ? x * x : 0.0);
   const double alpha = __shfl_sync(0xffffffffu, x, 0);
   if (xn2 == 0.0) {  // no bulge left: a carried block still has to reach memory
@@ -346,6 +344,10 @@ __device__ __forceinline__ bool chase_step(double* bb, int c, int r0, int L, int
       if (lx && (FULL || l < nl)) pyl[l * (LD - 1)] = yl[l] - d * v;
     }
   }
+  // rows-after block, loaded once the left block is done (fewer live
+  // registers through the butterfly); the R update hides its latency
+#pragma unroll
+  for (int j = 0; j < B2; ++j) ya[j] = (ly && (FULL || j < L)) ? band_ld<CG>(pya + j * (LD - 1)) : 0.0;
   __syncwarp();
   // R x R: two-sided (symmetric, lower storage); p = tau R v
   double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
