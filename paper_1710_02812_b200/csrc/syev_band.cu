@@ -337,11 +337,14 @@ __device__ __forceinline__ bool chase_step(double* bb, int c, int r0, int L, int
         t[j] = (up ? t[j + ofs] : t[j]) + got;
       }
     }
-    const double dl = tau * t[0];
+    ws[lane] = tau * t[0];  // d_l, read back as broadcasts (ws is rewritten after the next syncwarp)
+    __syncwarp();
+    const double2* d2 = reinterpret_cast<const double2*>(ws);
 #pragma unroll
-    for (int l = 0; l < B2 - 1; ++l) {
-      const double d = __shfl_sync(0xffffffffu, dl, l);
-      if (lx && (FULL || l < nl)) pyl[l * (LD - 1)] = yl[l] - d * v;
+    for (int l = 0; l < B2 - 1; l += 2) {
+      const double2 d = d2[l / 2];
+      if (lx && (FULL || l < nl)) pyl[l * (LD - 1)] = yl[l] - d.x * v;
+      if (l + 1 < B2 - 1 && lx && (FULL || l + 1 < nl)) pyl[(l + 1) * (LD - 1)] = yl[l + 1] - d.y * v;
     }
   }
   // rows-after block, loaded once the left block is done (fewer live
@@ -406,7 +409,7 @@ __global__ void __launch_bounds__(CHASE_WARPS * 32, 1) k_chase(const EigDev* __r
   const int gw = crank * CHASE_WARPS + warp;    // this warp's global index
   __shared__ unsigned long long prog[CHASE_WARPS];
   __shared__ double vsh[CHASE_WARPS][B2];
-  __shared__ double wsh[CHASE_WARPS][B2];
+  __shared__ __align__(16) double wsh[CHASE_WARPS][B2];
   if (tid < CHASE_WARPS) prog[tid] = prog_encode(crank * CHASE_WARPS + tid - W, kSweepDone);
   cg::cluster_group cluster = cg::this_cluster();
   if (CL) cluster.sync();
