@@ -353,13 +353,17 @@ __device__ __forceinline__ bool chase_step(double* bb, int c, int r0, int L, int
   for (int j = 0; j < B2; ++j) ya[j] = (ly && (FULL || j < L)) ? band_ld<CG>(pya + j * (LD - 1)) : 0.0;
   __syncwarp();
   // R x R: two-sided (symmetric, lower storage); p = tau R v
+  // (vs, ws: 16-byte aligned per-warp rows, read as double2 broadcasts)
+  const double2* vs2 = reinterpret_cast<const double2*>(vs);
+  const double2* ws2 = reinterpret_cast<const double2*>(ws);
   double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
 #pragma unroll
   for (int j = 0; j < B2; j += 4) {
-    p0 += ar[j] * vs[j];
-    p1 += ar[j + 1] * vs[j + 1];
-    p2 += ar[j + 2] * vs[j + 2];
-    p3 += ar[j + 3] * vs[j + 3];
+    const double2 a = vs2[j / 2], b = vs2[j / 2 + 1];
+    p0 += ar[j] * a.x;
+    p1 += ar[j + 1] * a.y;
+    p2 += ar[j + 2] * b.x;
+    p3 += ar[j + 3] * b.y;
   }
   const double pp = tau * ((p0 + p1) + (p2 + p3));
   const double al = -0.5 * tau * warp_sum(pp * v);
@@ -367,16 +371,21 @@ __device__ __forceinline__ bool chase_step(double* bb, int c, int r0, int L, int
   ws[lane] = w;
   __syncwarp();
 #pragma unroll
-  for (int j = 0; j < B2; ++j)
-    if (lx && lane >= j && (FULL || j < L)) pa1[j * (LD - 1)] = ar[j] - (v * ws[j] + w * vs[j]);
+  for (int j = 0; j < B2; j += 2) {
+    const double2 wj = ws2[j / 2], vj = vs2[j / 2];
+    if (lx && lane >= j && (FULL || j < L)) pa1[j * (LD - 1)] = ar[j] - (v * wj.x + w * vj.x);
+    if (lx && lane >= j + 1 && (FULL || j + 1 < L))
+      pa1[(j + 1) * (LD - 1)] = ar[j + 1] - (v * wj.y + w * vj.y);
+  }
   // rows after R: right application (creates the next bulge)
   double y0 = 0.0, y1 = 0.0, y2 = 0.0, y3 = 0.0;
 #pragma unroll
   for (int j = 0; j < B2; j += 4) {
-    y0 += ya[j] * vs[j];
-    y1 += ya[j + 1] * vs[j + 1];
-    y2 += ya[j + 2] * vs[j + 2];
-    y3 += ya[j + 3] * vs[j + 3];
+    const double2 a = vs2[j / 2], b = vs2[j / 2 + 1];
+    y0 += ya[j] * a.x;
+    y1 += ya[j + 1] * a.y;
+    y2 += ya[j + 2] * b.x;
+    y3 += ya[j + 3] * b.y;
   }
   const double y = tau * ((y0 + y1) + (y2 + y3));
   if (last) {
@@ -408,7 +417,7 @@ __global__ void __launch_bounds__(CHASE_WARPS * 32, 1) k_chase(const EigDev* __r
   const int W = CHASE_WARPS * (CL ? CS : 1);   // warps working on this matrix
   const int gw = crank * CHASE_WARPS + warp;    // this warp's global index
   __shared__ unsigned long long prog[CHASE_WARPS];
-  __shared__ double vsh[CHASE_WARPS][B2];
+  __shared__ __align__(16) double vsh[CHASE_WARPS][B2];
   __shared__ __align__(16) double wsh[CHASE_WARPS][B2];
   if (tid < CHASE_WARPS) prog[tid] = prog_encode(crank * CHASE_WARPS + tid - W, kSweepDone);
   cg::cluster_group cluster = cg::this_cluster();
