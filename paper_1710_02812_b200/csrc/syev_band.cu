@@ -390,12 +390,21 @@ __device__ __forceinline__ bool chase_step(double* bb, int c, int r0, int L, int
   const double y = tau * ((y0 + y1) + (y2 + y3));
   if (last) {
 #pragma unroll
-    for (int j = 0; j < B2; ++j)
-      if (ly && (FULL || j < L)) pya[j * (LD - 1)] = ya[j] - y * vs[j];
+    for (int j = 0; j < B2; j += 2) {
+      const double2 a = vs2[j / 2];
+      if (ly && (FULL || j < L)) pya[j * (LD - 1)] = ya[j] - y * a.x;
+      if (ly && (FULL || j + 1 < L)) pya[(j + 1) * (LD - 1)] = ya[j + 1] - y * a.y;
+    }
   } else {  // the next step's x and left block (stored by that step)
-    x = ya[0] - y * vs[0];
+    const double2 a0 = vs2[0];
+    x = ya[0] - y * a0.x;
+    yl[0] = (FULL || 1 < L) ? ya[1] - y * a0.y : 0.0;
 #pragma unroll
-    for (int l = 0; l < B2 - 1; ++l) yl[l] = (FULL || l + 1 < L) ? ya[l + 1] - y * vs[l + 1] : 0.0;
+    for (int j = 2; j < B2; j += 2) {
+      const double2 a = vs2[j / 2];
+      yl[j - 1] = (FULL || j < L) ? ya[j] - y * a.x : 0.0;
+      yl[j] = (FULL || j + 1 < L) ? ya[j + 1] - y * a.y : 0.0;
+    }
   }
   return true;
 }
