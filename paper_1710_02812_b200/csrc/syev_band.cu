@@ -40,9 +40,8 @@ __global__ void __launch_bounds__(512, 1) k_panel_qr(const EigDev* __restrict__ 
   const int ldp = mc + 1;
   extern __shared__ double psm[];
   double* Pl = psm;                          // [B2][ldp]
-  double* xbuf = Pl + (size_t)B2 * ldp;      // [CS][2]   norm partial, alpha
-  double* dbuf = xbuf + 2 * CS;              // [CS][B2]  column-dot partials
-  __shared__ double beta_s[B2], tau_s[B2], red[32];
+  double* dbuf = Pl + (size_t)B2 * ldp;      // [2][CS][2][B2] per-column exchange
+  __shared__ double beta_s[B2], tau_s[B2];
   __shared__ double S[B2][B2 + 1], T[B2][B2 + 1];
   cluster.sync();  // peers' shared memory is live before any DSMEM write
   if (j0 >= n) {
@@ -64,21 +63,31 @@ __global__ void __launch_bounds__(512, 1) k_panel_qr(const EigDev* __restrict__ 
   __syncthreads();
   for (int t = 0; t < nr; ++t) {
     double* pt = Pl + t * ldp;
-    // (a) norm of rows t+1.. and alpha = P[t][t]
-    double part = 0.0;
-    for (int i = max(0, t + 1 - lo) + tid; i < ml; i += nt) part += pt[i] * pt[i];
-    part = block_sum(part, red);
     const bool own_t = t >= lo && t < hi;
-    if (tid == 0)
-      for (int c = 0; c < CS; ++c) {
-        double* px = cluster.map_shared_rank(xbuf, c);
-        px[2 * crank] = part;
-        if (own_t) px[1] = pt[t - lo];  // slot 1 of rank 0's pair is unused
+    const int i0 = max(0, t + 1 - lo);
+    double* db = dbuf + (size_t)(t & 1) * CS * 2 * B2;  // [CS][2][B2], by column parity
+    // One exchange per column: with x = P[t+1:, t] unscaled, the partial
+    // norm x.x (slot u = t) and dots x.P[t+1:, u] (u > t), and from the CTA
+    // owning row t its entries P[t][t..] (alpha and the pending columns'
+    // row t).  Then s_u = P[t][u] + scal (x.P[:, u]) with v = scal x.
+    for (int u = t + warp; u < jb; u += nwarps) {
+      const double* pu = Pl + u * ldp;
+      double sp = 0.0;
+      for (int i = i0 + lane; i < ml; i += 32) sp += pt[i] * pu[i];
+      sp = warp_sum(sp);
+      const double rt = own_t ? pu[t - lo] : 0.0;
+      if (lane < CS) {
+        double* peer = cluster.map_shared_rank(db, lane);
+        peer[(2 * crank) * B2 + u] = sp;
+        peer[(2 * crank + 1) * B2 + u] = rt;
       }
+    }
     cluster.sync();
-    double xn2 = 0.0;
-    for (int c = 0; c < CS; ++c) xn2 += xbuf[2 * c];
-    const double alpha = xbuf[1];
+    double xn2 = 0.0, alpha = 0.0;
+    for (int c = 0; c < CS; ++c) {
+      xn2 += db[(2 * c) * B2 + t];
+      alpha += db[(2 * c + 1) * B2 + t];
+    }
     double tau = 0.0, beta = alpha, scal = 0.0;
     if (xn2 > 0.0) {
       const double nrm = sqrt(alpha * alpha + xn2);
@@ -86,36 +95,29 @@ __global__ void __launch_bounds__(512, 1) k_panel_qr(const EigDev* __restrict__ 
       tau = (beta - alpha) / beta;
       scal = 1.0 / (alpha - beta);
     }
-    for (int i = max(0, t + 1 - lo) + tid; i < ml; i += nt) pt[i] *= scal;
     if (tid == 0) {
       beta_s[t] = beta;
       tau_s[t] = tau;
       if (crank == 0) J.tau[j0 + t] = tau;
     }
-    __syncthreads();
-    // (c) s_u = P[t][u] + sum_{i>t} v_i P[i][u] for u > t (partials)
-    for (int u = t + 1 + warp; u < jb; u += nwarps) {
-      const double* pu = Pl + u * ldp;
-      double sp = 0.0;
-      for (int i = max(0, t + 1 - lo) + lane; i < ml; i += 32) sp += pt[i] * pu[i];
-      sp = warp_sum(sp);
-      if (own_t) sp += pu[t - lo];
-      if (lane < CS) cluster.map_shared_rank(dbuf, lane)[crank * B2 + u] = sp;
-    }
-    cluster.sync();
-    // (d) P[i][u] -= tau s_u v_i
+    // P[i][u] -= tau s_u v_i  (v_i = scal x_i, rounded as it is stored)
     if (tau != 0.0) {
       for (int u = t + 1 + warp; u < jb; u += nwarps) {
-        double su = 0.0;
-        for (int c = 0; c < CS; ++c) su += dbuf[c * B2 + u];
-        su *= tau;
+        double dot = 0.0, ptu = 0.0;
+        for (int c = 0; c < CS; ++c) {
+          dot += db[(2 * c) * B2 + u];
+          ptu += db[(2 * c + 1) * B2 + u];
+        }
+        const double su = tau * (ptu + scal * dot);
         double* pu = Pl + u * ldp;
         if (own_t && lane == 0) pu[t - lo] -= su;
-        for (int i = max(0, t + 1 - lo) + lane; i < ml; i += 32) pu[i] -= su * pt[i];
+        for (int i = i0 + lane; i < ml; i += 32) pu[i] -= su * (pt[i] * scal);
       }
     }
-    __syncthreads();
+    __syncthreads();  // column t's x read by every update
+    for (int i = i0 + tid; i < ml; i += nt) pt[i] *= scal;  // v (column t is not read again in the loop)
   }
+  __syncthreads();
   if (tid < B2 && tid >= nr) {
     tau_s[tid] = 0.0;
     if (crank == 0 && tid < jb) J.tau[j0 + tid] = 0.0;
@@ -182,7 +184,7 @@ __global__ void __launch_bounds__(512, 1) k_panel_qr(const EigDev* __restrict__ 
 
 constexpr size_t kPanelSmemMax = 200 * 1024;
 size_t panel_smem(int mc, int cs) {
-  return ((size_t)B2 * (mc + 1) + 2 * cs + (size_t)cs * B2) * sizeof(double);
+  return ((size_t)B2 * (mc + 1) + (size_t)4 * cs * B2) * sizeof(double);
 }
 
 void launch_panel_qr(Ctx& ctx, int count, int mmax, const EigDev* dd, int j0, int vcol) {
