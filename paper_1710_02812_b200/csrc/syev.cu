@@ -323,7 +323,8 @@ __global__ void __launch_bounds__(LAT, 1) k_latrd(const EigDev* __restrict__ job
       int ic[R];
 #pragma unroll
       for (int q = 0; q < R; ++q) ic[q] = min(max(tid + q * LAT, j + 1), n - 1);
-      constexpr int U = (R <= 3) ? 8 : (R <= 6 ? 6 : 3);
+      // columns per batch: loads in flight per thread (R rows each)
+      constexpr int U = R == 1 ? 24 : R == 2 ? 12 : (R <= 3) ? 8 : (R <= 6 ? 6 : 3);
       int k = kb;
       for (; k + U <= ke; k += U) {
         const double* c0 = A + (long long)k * lda;
