@@ -77,7 +77,6 @@ void begin(hsvd_cu_ctx* ctx) {
   if (!ctx) throw Error(kInvalid, "null context");
   HSVD_CUDA(cudaSetDevice(ctx->c.device));
   ctx->c.arena.reset();
-  ctx->c.staging.set_zero_copy(false);
   ++ctx->generation;
 }
 
@@ -110,7 +109,6 @@ XView stage_x(Ctx& c, const void* x, int dtype, int64_t m, int64_t n, int64_t ld
   }
   // the arena block may still be in use by earlier work on the compute stream
   cudaStream_t cs = c.get_copy_stream();
-  c.staging.set_zero_copy(true);  // until x_wait_rows(all): the H2D engine is busy
   cudaEvent_t start = c.get_chunk_event(0);
   HSVD_CUDA(cudaEventRecord(start, c.stream));
   HSVD_CUDA(cudaStreamWaitEvent(cs, start, 0));

@@ -104,10 +104,12 @@ class Arena {
 void copy_mapped_to_device(void* dst, const void* host_src, size_t bytes, cudaStream_t s);
 
 // Pinned host ring mirrored on the device: small descriptor arrays are
-// written on the host and copied with one cudaMemcpyAsync per launch --
-// or, while a large input transfer occupies the host->device copy engine
-// (set_zero_copy), read straight from the mapped ring by a small kernel, so
-// the compute stream does not queue behind the whole input copy.
+// written on the host and copied to the device by a one-CTA kernel reading
+// the mapped ring (cudaMemcpyAsync when the ring cannot be mapped).  The
+// kernel copy keeps these per-launch transfers off the copy engines: a
+// host->device cudaMemcpyAsync per GEMM queued behind the chunked input
+// transfer (the compute stream then waited for the whole input), and even
+// on an idle engine it cost ~3 ms per config-2 step against the kernel.
 class Staging {
  public:
   void init(size_t bytes) {
@@ -115,7 +117,10 @@ class Staging {
     HSVD_CUDA(cudaMallocHost(&host_, bytes));
     HSVD_CUDA(cudaMalloc(&dev_, bytes));
     // the device's address of the (mapped) pinned ring, for zero-copy reads
-    HSVD_CUDA(cudaHostGetDevicePointer(&host_dev_, host_, 0));
+    if (cudaHostGetDevicePointer(&host_dev_, host_, 0) != cudaSuccess) {
+      (void)cudaGetLastError();
+      host_dev_ = nullptr;  // copy-engine path only
+    }
   }
   ~Staging() {
     if (host_) cudaFreeHost(host_);
@@ -136,21 +141,19 @@ class Staging {
     char* h = static_cast<char*>(host_) + off_;
     char* d = dst ? static_cast<char*>(dst) : static_cast<char*>(dev_) + off_;
     std::memcpy(h, src, bytes);
-    if (zero_copy_)
+    if (host_dev_)
       copy_mapped_to_device(d, static_cast<char*>(host_dev_) + off_, bytes, s);
     else
       HSVD_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s));
     off_ += b;
     return d;
   }
-  void set_zero_copy(bool on) { zero_copy_ = on; }
 
  private:
   void* host_ = nullptr;
   void* host_dev_ = nullptr;  // device address of host_
   void* dev_ = nullptr;
   size_t size_ = 0, off_ = 0;
-  bool zero_copy_ = false;
 };
 
 // Opt a kernel in to the device's full dynamic shared memory, once per

@@ -74,9 +74,6 @@ void x_wait_rows(Ctx& ctx, const XView& x, long long row_end) {
     HSVD_CUDA(cudaStreamWaitEvent(ctx.stream, c.ev, 0));
     prev = c.row_end;
   }
-  // the stream now follows the whole input copy: staging copies can use the
-  // copy engine again without queueing behind it
-  if (row_end < 0) ctx.staging.set_zero_copy(false);
 }
 
 // ---------------------------------------------------------------------------
