@@ -48,6 +48,13 @@ struct TileCfg<128, 32> {
 };
 constexpr int kModeSyrk = 1, kModeLower = 2;  // mode bits
 
+// Up to kPackMax descriptors travel in the launch parameters (read from the
+// constant bank); larger groups go through the staging ring.
+constexpr int kPackMax = 64;
+struct DescPack {
+  GemmDesc d[kPackMax];
+};
+
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c[0]), "+d"(c[1])
@@ -93,7 +100,7 @@ struct GemmShape {
 template <typename TA, typename TB, bool TRA, bool TRB, int BM, int BN>
 __global__ void __launch_bounds__(NT) k_gemm(const GemmDesc* __restrict__ descs, int mode,
                                              int splits, double* __restrict__ ws,
-                                             long long ws_slot) {
+                                             long long ws_slot, const __grid_constant__ DescPack pack) {
   // A element (m, k): !TRA -> A[m + k lda] (m contiguous), TRA -> A[k + m lda]
   // B element (k, n): !TRB -> B[k + n ldb] (k contiguous), TRB -> B[n + k ldb]
   using Sh = GemmShape<TA, TB, TRA, TRB, BM, BN>;
@@ -106,7 +113,7 @@ __global__ void __launch_bounds__(NT) k_gemm(const GemmDesc* __restrict__ descs,
 
   const int g = blockIdx.z / splits;
   const int split = blockIdx.z - g * splits;
-  const GemmDesc d = descs[g];
+  const GemmDesc d = descs ? descs[g] : pack.d[g];
   const int tm = blockIdx.x, tn = blockIdx.y;
   if (tm * BM >= d.M || tn * BN >= d.N) return;
   const bool syrk = (mode & kModeSyrk) != 0;
@@ -250,9 +257,10 @@ __global__ void __launch_bounds__(NT) k_gemm(const GemmDesc* __restrict__ descs,
 }
 
 __global__ void k_splitk_reduce(const GemmDesc* __restrict__ descs, int splits, int mode,
-                                const double* __restrict__ ws, long long ws_slot) {
+                                const double* __restrict__ ws, long long ws_slot,
+                                const __grid_constant__ DescPack pack) {
   const int g = blockIdx.y;
-  const GemmDesc d = descs[g];
+  const GemmDesc d = descs ? descs[g] : pack.d[g];
   const bool syrk = (mode & kModeSyrk) != 0, mirror = syrk && !(mode & kModeLower);
   const long long total = (long long)d.M * d.N;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
@@ -272,21 +280,21 @@ __global__ void k_splitk_reduce(const GemmDesc* __restrict__ descs, int splits, 
 
 template <typename TA, typename TB, bool TRA, bool TRB, int BM, int BN>
 void launch_t(Ctx& ctx, dim3 grid, const GemmDesc* dd, int mode, int splits, double* ws,
-              long long slot) {
+              long long slot, const DescPack& pack) {
   constexpr size_t smem = GemmShape<TA, TB, TRA, TRB, BM, BN>::SMEM;
   auto* k = k_gemm<TA, TB, TRA, TRB, BM, BN>;
   smem_optin(k, smem);
-  k<<<grid, NT, smem, ctx.stream>>>(dd, mode, splits, ws, slot);
+  k<<<grid, NT, smem, ctx.stream>>>(dd, mode, splits, ws, slot, pack);
 }
 
 template <typename TA, typename TB, int BM, int BN>
 void launch_tile(Ctx& ctx, bool ta, bool tb, dim3 grid, const GemmDesc* dd, int mode, int splits,
-                 double* ws, long long slot) {
+                 double* ws, long long slot, const DescPack& pack) {
   ctx.launch_begin();
-  if (!ta && !tb) launch_t<TA, TB, false, false, BM, BN>(ctx, grid, dd, mode, splits, ws, slot);
-  else if (!ta && tb) launch_t<TA, TB, false, true, BM, BN>(ctx, grid, dd, mode, splits, ws, slot);
-  else if (ta && !tb) launch_t<TA, TB, true, false, BM, BN>(ctx, grid, dd, mode, splits, ws, slot);
-  else launch_t<TA, TB, true, true, BM, BN>(ctx, grid, dd, mode, splits, ws, slot);
+  if (!ta && !tb) launch_t<TA, TB, false, false, BM, BN>(ctx, grid, dd, mode, splits, ws, slot, pack);
+  else if (!ta && tb) launch_t<TA, TB, false, true, BM, BN>(ctx, grid, dd, mode, splits, ws, slot, pack);
+  else if (ta && !tb) launch_t<TA, TB, true, false, BM, BN>(ctx, grid, dd, mode, splits, ws, slot, pack);
+  else launch_t<TA, TB, true, true, BM, BN>(ctx, grid, dd, mode, splits, ws, slot, pack);
   ctx.check_launch("k_gemm");
 }
 
@@ -349,13 +357,14 @@ int choose_splits(long long tiles, int maxK, long long slots, int count) {
 
 template <typename TA, typename TB>
 void launch_typed(Ctx& ctx, bool ta, bool tb, bool skinny, int maxM, int maxN, int count,
-                  const GemmDesc* dd, int mode, int splits, double* ws, long long slot) {
+                  const GemmDesc* dd, int mode, int splits, double* ws, long long slot,
+                  const DescPack& pack) {
   if (skinny) {
     dim3 grid(ceil_div(maxM, 128), ceil_div(maxN, 32), count * splits);
-    launch_tile<TA, TB, 128, 32>(ctx, ta, tb, grid, dd, mode, splits, ws, slot);
+    launch_tile<TA, TB, 128, 32>(ctx, ta, tb, grid, dd, mode, splits, ws, slot, pack);
   } else {
     dim3 grid(ceil_div(maxM, 64), ceil_div(maxN, 64), count * splits);
-    launch_tile<TA, TB, 64, 64>(ctx, ta, tb, grid, dd, mode, splits, ws, slot);
+    launch_tile<TA, TB, 64, 64>(ctx, ta, tb, grid, dd, mode, splits, ws, slot, pack);
   }
 }
 
@@ -389,9 +398,14 @@ void gemm_grouped(Ctx& ctx, DType ta, DType tb, bool trans_a, bool trans_b, bool
 
   const long long slots = (long long)ctx.num_sms * occupancy(ta, tb, trans_a, trans_b, skinny);
   const int splits = choose_splits(tiles, maxK, slots, count);
-  const GemmDesc* dd =
-      static_cast<const GemmDesc*>(ctx.staging.put(live.data(), live.size() * sizeof(GemmDesc),
-                                                   ctx.stream));
+  // descriptors: in the launch parameters when they fit, else staged
+  static thread_local DescPack pack;
+  const GemmDesc* dd = nullptr;
+  if (count <= kPackMax)
+    std::copy(live.begin(), live.end(), pack.d);
+  else
+    dd = static_cast<const GemmDesc*>(ctx.staging.put(live.data(), live.size() * sizeof(GemmDesc),
+                                                      ctx.stream));
   double* ws = nullptr;
   long long slot = 0;
   Arena::Mark mk = ctx.arena.mark();
@@ -403,21 +417,21 @@ void gemm_grouped(Ctx& ctx, DType ta, DType tb, bool trans_a, bool trans_b, bool
   ctx.pending_flops = flops;
   if (ta == DType::F64 && tb == DType::F64)
     launch_typed<double, double>(ctx, trans_a, trans_b, skinny, maxM, maxN, count, dd, mode,
-                                 splits, ws, slot);
+                                 splits, ws, slot, pack);
   else if (ta == DType::F32 && tb == DType::F64)
     launch_typed<float, double>(ctx, trans_a, trans_b, skinny, maxM, maxN, count, dd, mode,
-                                splits, ws, slot);
+                                splits, ws, slot, pack);
   else if (ta == DType::F64 && tb == DType::F32)
     launch_typed<double, float>(ctx, trans_a, trans_b, skinny, maxM, maxN, count, dd, mode,
-                                splits, ws, slot);
+                                splits, ws, slot, pack);
   else
     launch_typed<float, float>(ctx, trans_a, trans_b, skinny, maxM, maxN, count, dd, mode, splits,
-                               ws, slot);
+                               ws, slot, pack);
   if (splits > 1) {
     const long long elems = (long long)maxM * maxN;
     int bx = static_cast<int>(std::min<long long>((elems + 255) / 256, 4096));
     ctx.launch_begin();
-    k_splitk_reduce<<<dim3(bx, count), 256, 0, ctx.stream>>>(dd, splits, mode, ws, slot);
+    k_splitk_reduce<<<dim3(bx, count), 256, 0, ctx.stream>>>(dd, splits, mode, ws, slot, pack);
     ctx.check_launch("k_splitk_reduce");
   }
   ctx.arena.release(mk);
