@@ -290,28 +290,38 @@ def run_ours(args, w):
     for _ in range(args.warmup):
         step(x)
     ctx.synchronize()
-    # timed region (device-resident input)
-    ctx.profile(True)
-    ctx.profile_report()
+    def timed_pass(profiled):
+        """K steps bracketed by barrier + synchronize, timed with CUDA events
+        on the library's stream; with per-launch events when profiled."""
+        ctx.profile(profiled)
+        ctx.profile_report()
+        barrier()
+        ctx.synchronize()
+        torch.cuda.synchronize()
+        l0 = ctx.launch_count()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            r = step(x)
+        e1.record(stream)
+        ctx.synchronize()
+        torch.cuda.synchronize()
+        barrier()
+        launches = (ctx.launch_count() - l0) // args.steps
+        ms = e0.elapsed_time(e1) / args.steps
+        prof = ctx.profile_report() if profiled else None
+        ctx.profile(False)
+        return r, ms, launches, prof
+
+    # timed region (device-resident input): the headline pass runs without
+    # per-launch events (they cost ~3% of the step in host launch time); the
+    # per-kernel breakdown and the roofline come from a second timed pass of
+    # the same K steps with them
     clocks = Clocks(local)
-    barrier()
-    ctx.synchronize()
-    torch.cuda.synchronize()
-    l0 = ctx.launch_count()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        rank_k = step(x)
-    e1.record(stream)
-    ctx.synchronize()
-    torch.cuda.synchronize()
-    barrier()
+    rank_k, ms, launches, _ = timed_pass(False)
     clk = clocks.stop()
-    launches = (ctx.launch_count() - l0) // args.steps
-    ms = e0.elapsed_time(e1) / args.steps
-    prof = ctx.profile_report()
-    ctx.profile(False)
+    _, ms_prof, _, prof = timed_pass(True)
     if ws > 1:
         t = torch.tensor([ms], device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -355,6 +365,9 @@ def run_ours(args, w):
         pass
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     roof = roofline(prof, args.steps, w, hbm_peak, lambda: fp64_peak_tflops(torch, dev))
+    roof["measured"] = ("per-launch CUDA events over a second timed pass of the same K steps "
+                        "(the headline pass runs without them)")
+    roof["profiled_pass_ms_per_step"] = ms_prof
 
     cpu = None
     if not args.no_cpu_baseline and ws == 1:
