@@ -3,10 +3,14 @@
 
 Metric (BASELINE.json): HSVD input GB/s = m*n*sizeof(dtype) / t per rank-k
 SVD, whole job.  One step = one full rank-k HSVD of the workload matrix.
-Default workload: BASELINE config 2 (20000x20000 fp32, 8x8 grid, k=100).
+Default workload: BASELINE config 5 (65536x65536 fp32, 16x16 grid, k=200),
+the largest configuration that fits one B200.
 
   python bench.py [--gpus N --steps K --warmup W --config C]
   python bench.py --impl reference ...   (CPU oracle arm, rank 0 only)
+
+--gpus N without a torchrun environment re-launches this script under
+torch.distributed.run with N ranks (one per GPU, rendezvous on 127.0.0.1).
 
 Timing: W untimed warm-up steps, then K steps bracketed by barrier +
 cudaStreamSynchronize, CUDA events on the library's stream, max over ranks.
@@ -39,11 +43,49 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cpu-single", action="store_true",
+                    help="skip the single-thread CPU leaf timing")
     ap.add_argument("--cpu-threads", type=int, default=0)
+    ap.add_argument("--launcher-selftest", action="store_true",
+                    help="(CPU tests) spawn --gpus ranks over gloo, rendezvous, print n_gpus")
     return ap.parse_args()
+
+
+def free_port() -> int:
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def relaunch(args) -> int:
+    """--gpus N > WORLD_SIZE: run this script under torch.distributed.run with
+    N ranks on this node (the same command the driver uses for N > 1)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1")
+    return subprocess.call(cmd, env=env)
+
+
+def launcher_selftest(args) -> int:
+    """Rank body of --launcher-selftest: gloo rendezvous + an all-reduce, then
+    rank 0 prints the contract's n_gpus."""
+    import torch
+    import torch.distributed as dist
+    ws, rank, _ = dist_env()
+    dist.init_process_group("gloo")
+    t = torch.tensor([float(rank + 1)])
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.barrier()
+    if rank == 0:
+        print(json.dumps({"n_gpus": ws, "world_size": dist.get_world_size(),
+                          "max_rank_plus_1": float(t.item())}), flush=True)
+    dist.destroy_process_group()
+    return 0
 
 
 def dist_env():
@@ -57,41 +99,70 @@ def dist_env():
 # CPU arm (oracle port on the host cores)
 # ---------------------------------------------------------------------------
 
-def cpu_slice_sample(w, threads):
-    """Row slice 0 of workload w through the CPU oracle: its Q leaf SVDs,
-    column merges and V-recovery (1/P of the leaf work).  Returns
-    (seconds, slice bytes, sample description)."""
+def host_leaves(w, count):
+    """The first `count` leaf blocks of row slice 0 (host fp32/fp64 copies) of
+    the exact matrix the GPU arm times: generated on cuda:0 with the bench's
+    generator and seed.  Without a GPU (CPU tests) the numpy generator of the
+    same recipe stands in; the returned description says which."""
+    from paper_1710_02812_b200 import configs
+    count = max(1, min(count, w.Q))
+    try:
+        import torch
+        cuda = torch.cuda.is_available()
+    except Exception:  # pragma: no cover
+        cuda = False
+    if cuda:
+        x = configs.generate_torch(w, device=torch.device("cuda", 0))
+        blocks = [x[:w.d, j * w.c:(j + 1) * w.c].cpu().numpy() for j in range(count)]
+        full = x.cpu().numpy() if w.input_bytes <= (64 << 20) else None
+        del x
+        torch.cuda.empty_cache()
+        src = "bytes of configs.generate_torch on cuda:0 (the GPU arm's input)"
+    else:
+        full = configs.generate_numpy(w)
+        blocks = [full[:w.d, j * w.c:(j + 1) * w.c].copy() for j in range(count)]
+        src = "configs.generate_numpy (no GPU on this host)"
+    return blocks, full, src
+
+
+def whole_pipeline_fits(w):
+    """Small workloads (config 1) run the complete reference pipeline per step."""
+    return w.input_bytes <= (64 << 20)
+
+
+def cpu_step(w, blocks, full, i, threads):
+    """One CPU step of the reference algorithm (oracle port): the complete
+    rank-k HSVD (hierarchical_svd + recover_left_vectors, hierarchy.cpp:65-112)
+    when the workload is small, else leaf i of row slice 0 through full_svd +
+    truncate_factor (hierarchy.cpp:57, kernels.cpp:21-48) -- the leaf SVDs
+    are > 95% of the reference's flops at configs 2-5; the
+    column/row merges and the recoveries are not in this sample.
+    Returns (seconds, bytes of X covered, description)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import numpy as np
     import hsvd_oracle as O
-    from paper_1710_02812_b200 import configs
-    rng = np.random.default_rng(configs.SEED_BASE + w.cfg)
-    d = w.d
-    if w.kind == "modes":
-        full = configs.generate_numpy(w.scaled(d, w.n, P=1), seed=configs.SEED_BASE + w.cfg)
-        xs = full
-    else:
-        u = np.linalg.qr(rng.standard_normal((w.m, w.r)))[0][:d]
-        v = np.linalg.qr(rng.standard_normal((w.n, w.r)))[0]
-        s = w.spectrum(np.arange(1, w.r + 1, dtype=np.float64))
-        xs = (u * s) @ v.T + w.noise * rng.standard_normal((d, w.n))
-        xs = xs.astype(np.float32 if w.dtype == "f32" else np.float64)
-    try:
-        from threadpoolctl import threadpool_limits
-    except Exception:  # pragma: no cover
-        threadpool_limits = None
-    t0 = time.perf_counter()
-    if threadpool_limits is not None and threads > 1 and w.Q > 1:
+    from threadpoolctl import threadpool_limits
+    if full is not None and whole_pipeline_fits(w):
+        cfg = O.MatConfig(gamma=GAMMA, row_block_rows=w.d, col_block_cols=w.c, max_rank=w.k)
+        t0 = time.perf_counter()
         with threadpool_limits(1):
-            um = O.svd_of_col_slices(xs, w.c, GAMMA, w.k, workers=threads)
-    else:
-        um = O.svd_of_col_slices(xs, w.c, GAMMA, w.k, workers=1)
-    rec = O.full_svd(um.u.T @ xs.astype(np.float64))
-    O.truncate_factor(rec, GAMMA, w.k)
+            r = O.hierarchical_svd(full, cfg, workers=threads)
+        with threadpool_limits(threads):
+            O.recover_left_vectors(full, r.v)
+        sec = time.perf_counter() - t0
+        return sec, full.nbytes, (f"complete rank-k HSVD of the {w.m}x{w.n} matrix "
+                                  f"(hierarchical_svd + recover_left_vectors), numpy/LAPACK "
+                                  f"oracle port, {threads} threads")
+    blk = blocks[i % len(blocks)]
+    t0 = time.perf_counter()
+    with threadpool_limits(threads):
+        f = O.full_svd(np.asarray(blk, dtype=np.float64))
+        O.truncate_factor(f, GAMMA, w.k)
     sec = time.perf_counter() - t0
-    desc = (f"row slice 0 of {w.P} ({d}x{w.n}): {w.Q} leaf SVDs + {w.Q - 1} column merges + "
-            f"V-recovery, numpy/LAPACK oracle, {threads} threads")
-    return sec, xs.nbytes, desc
+    return sec, blk.nbytes, (f"one {w.d}x{w.c} leaf of row slice 0 per step (leaf "
+                             f"{i % len(blocks)}), full_svd + truncate_factor, numpy/LAPACK "
+                             f"(dgesdd) oracle port, {threads} threads; merges and recoveries "
+                             f"(< 5% of the reference's flops) not sampled")
 
 
 def arm_config(w, ws):
@@ -108,15 +179,17 @@ def run_reference(args, w):
     if rank != 0:
         return 0
     threads = args.cpu_threads or os.cpu_count() or 1
-    times = []
-    sample_bytes = 0
+    blocks, full, src = host_leaves(w, args.warmup + args.steps)
+    times, nbytes = [], []
     desc = ""
     for i in range(args.warmup + args.steps):
-        sec, sample_bytes, desc = cpu_slice_sample(w, threads)
+        sec, nb, desc = cpu_step(w, blocks, full, i, threads)
         if i >= args.warmup:
             times.append(sec)
+            nbytes.append(nb)
     ms = 1000.0 * statistics.mean(times)
-    value = sample_bytes / (ms / 1000.0) / 1e9
+    value = sum(nbytes) / sum(times) / 1e9
+    desc = f"{desc}; input: {src}"
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -131,6 +204,22 @@ def run_reference(args, w):
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def cpu_baseline(args, w):
+    """cpu_baseline of the GPU arm (rank 0, N=1): one sample step on all host
+    threads, plus the reference's own single-thread mode (Eigen runs
+    single-threaded, bench.cpp:81) on one leaf."""
+    threads = args.cpu_threads or os.cpu_count() or 1
+    blocks, full, src = host_leaves(w, 1)
+    sec, nb, desc = cpu_step(w, blocks, full, 0, threads)
+    out = {"value": nb / sec / 1e9, "unit": "GB/s", "cores": threads, "kind": "port",
+           "sample": f"{desc}; input: {src}", "seconds": sec}
+    if not args.no_cpu_single:
+        sec1, nb1, desc1 = cpu_step(w, blocks, full, 0, 1)
+        out["single_thread"] = {"value": nb1 / sec1 / 1e9, "unit": "GB/s", "cores": 1,
+                                "seconds": sec1, "sample": desc1}
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -328,29 +417,44 @@ def run_ours(args, w):
         ms = float(t.item())
     value = w.input_bytes / (ms / 1000.0) / 1e9  # one matrix per step, whole job
 
-    # e2e through the public API with host buffers (H2D of X, D2H of U, sigma, V)
-    e2e = None
+    # e2e through the public API with host buffers (H2D of X, D2H of U, sigma,
+    # V): first from pageable memory -- what the C++ drop-in's DenseMatrix
+    # (std::vector storage) passes, staged by the library through its pinned
+    # ring -- the headline e2e; then from pinned memory (DMA straight from the
+    # caller's buffer) as e2e_pinned
+    e2e = e2e_pinned = None
     if not args.no_e2e:
-        xh = x.cpu().pin_memory()
+        reps = max(1, min(args.steps, 3))
+
+        def time_host(xh):
+            step(xh, fetch=True)  # warm
+            barrier()
+            ctx.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(reps):
+                f = step(xh, fetch=True)
+            ctx.synchronize()
+            sec = (time.perf_counter() - t0) / reps
+            barrier()
+            if ws > 1:
+                t = torch.tensor([sec], device=dev)
+                torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+                sec = float(t.item())
+            d2h = 8 * (f.u.size + f.v.size + f.sigma.size)
+            return {"value": w.input_bytes / sec / 1e9, "unit": "GB/s",
+                    "h2d_bytes_per_step": int(w.input_bytes),
+                    "d2h_bytes_per_step": int(d2h) * ws, "ms_per_step": 1000.0 * sec,
+                    "timed": f"wall clock over {reps} calls of the public rank_k_svd with "
+                             f"host X, results copied back (max over ranks)"}
+
+        xh = x.cpu()
         del x
         torch.cuda.empty_cache()
-        step(xh, fetch=True)  # warm
-        barrier()
-        ctx.synchronize()
-        t0 = time.perf_counter()
-        for _ in range(max(1, min(args.steps, 3))):
-            f = step(xh, fetch=True)
-        ctx.synchronize()
-        sec = (time.perf_counter() - t0) / max(1, min(args.steps, 3))
-        barrier()
-        if ws > 1:
-            t = torch.tensor([sec], device=dev)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            sec = float(t.item())
-        d2h = 8 * (f.u.size + f.v.size + f.sigma.size)
-        e2e = {"value": w.input_bytes / sec / 1e9, "unit": "GB/s",
-               "h2d_bytes_per_step": int(w.input_bytes), "d2h_bytes_per_step": int(d2h) * ws,
-               "ms_per_step": 1000.0 * sec}
+        e2e = dict(time_host(xh), host_memory="pageable (torch CPU tensor / std::vector "
+                                              "storage: the drop-in path)")
+        xh = xh.pin_memory()
+        e2e_pinned = dict(time_host(xh), host_memory="pinned (cudaHostAlloc)")
+        del xh
     if rank != 0:
         return 0
 
@@ -372,10 +476,7 @@ def run_ours(args, w):
     cpu = None
     if not args.no_cpu_baseline and ws == 1:
         try:
-            threads = args.cpu_threads or os.cpu_count() or 1
-            sec, sb, desc = cpu_slice_sample(w, threads)
-            cpu = {"value": sb / sec / 1e9, "unit": "GB/s", "cores": threads, "kind": "port",
-                   "sample": desc, "seconds": sec}
+            cpu = cpu_baseline(args, w)
         except Exception as exc:  # pragma: no cover
             cpu = {"error": str(exc)}
 
@@ -385,7 +486,7 @@ def run_ours(args, w):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded BASELINE.json recipe, generated on device)",
         "config": dict(arm_config(w, ws), rank_out=rank_k),
-        "e2e": e2e, "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu,
+        "e2e": e2e, "e2e_pinned": e2e_pinned, "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu,
         "clocks": clk,
         "tflops_tc": w.flops_tc() / (ms / 1000.0) / 1e12,
         "kernels": [{"name": k, "launches": n, "ms": round(t, 4), "share": round(s, 4)}
@@ -397,6 +498,14 @@ def run_ours(args, w):
 
 def main():
     args = parse()
+    ws, _, _ = dist_env()
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args)
+    if args.launcher_selftest:
+        return launcher_selftest(args)
+    if args.impl == "ours" and ws != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}", file=sys.stderr)
+        return 2
     from paper_1710_02812_b200 import configs
     w = configs.WORKLOADS[args.config]
     if args.impl == "reference":

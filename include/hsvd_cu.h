@@ -101,7 +101,17 @@ int64_t hsvd_cu_profile_report(hsvd_cu_ctx* ctx, char* buf, int64_t len);
 int hsvd_cu_validate(const hsvd_cu_config* cfg);
 
 /* x: m x n row-major with leading dimension ldx, dtype HSVD_CU_F32/F64, in
- * host (where = HSVD_CU_HOST) or device memory.  Result: (sigma, V), u absent. */
+ * host (where = HSVD_CU_HOST) or device memory.  Result: (sigma, V), u absent.
+ *
+ * Stream contract for device inputs (where = HSVD_CU_DEVICE, every entry
+ * point): the library reads device buffers on the context's stream
+ * (hsvd_cu_ctx_stream, created cudaStreamNonBlocking) and does not order
+ * itself after any other stream.  The buffer must live on the context's
+ * device and be ready on the context's stream when the call is made: a
+ * producer on another stream records an event that the context stream waits
+ * on (cudaStreamWaitEvent), or synchronizes.  The Python mirror does this for
+ * torch tensors (torch's current stream) and rejects tensors on another
+ * device.  Host inputs are read synchronously inside the call. */
 int hsvd_cu_hierarchical_svd(hsvd_cu_ctx* ctx, const void* x, int dtype, int64_t m, int64_t n,
                              int64_t ldx, int where, const hsvd_cu_config* cfg,
                              hsvd_cu_result** out);
@@ -186,6 +196,11 @@ int hsvd_cu_tree_merge(hsvd_cu_ctx* ctx, int orient, const hsvd_cu_factor_in* fa
  * lam (kk, descending), z (n x kk, column-major). */
 int hsvd_cu_syevx_topk(hsvd_cu_ctx* ctx, const double* a, int64_t n, int64_t kk, double* lam,
                        double* z);
+/* The same for a batch of `count` matrices in one launch set (the form the
+ * leaf stage runs): a = count consecutive n x n matrices, lam = count x kk,
+ * z = count consecutive n x kk column-major blocks. */
+int hsvd_cu_syevx_topk_batch(hsvd_cu_ctx* ctx, const double* a, int64_t count, int64_t n,
+                             int64_t kk, double* lam, double* z);
 
 /* ---- multi-GPU (one process / thread per GPU, rows sharded) ---------- */
 typedef struct hsvd_cu_group hsvd_cu_group;

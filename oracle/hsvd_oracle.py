@@ -403,12 +403,42 @@ def _row_slice_factor(x: np.ndarray, j: int, s0: int, cnt: int, cfg: MatConfig,
         x_j = x[s0:s0 + cnt]
         col_merged = svd_of_col_slices(x_j, cfg.col_block_cols, cfg.gamma,
                                        cfg.max_rank, workers)
-        b = col_merged.u.T @ np.asarray(x_j, dtype=np.float64)  # hierarchy.cpp:83
+        b = _ut_x(col_merged.u, x_j)  # hierarchy.cpp:83
         recovered = full_svd(b)
         recovered.u = None
         return truncate_factor(recovered, cfg.gamma, cfg.max_rank)
     except DecompositionError as err:  # hierarchy.cpp:86-89
         raise DecompositionError(f"row slice {j}: {err}", err.rows, err.cols) from err
+
+
+_CHUNK_ELEMS = 1 << 25  # fp64 promotion done in pieces of <= 256 MB
+
+
+def _ut_x(u: np.ndarray, x_j: np.ndarray) -> np.ndarray:
+    """B = U^T X_j with X_j promoted to fp64 a column chunk at a time (the
+    same column-by-column product; bounds host memory at full BASELINE
+    sizes, where one promoted row slice would be GBs per thread)."""
+    rows, cols = x_j.shape
+    step = max(1, _CHUNK_ELEMS // max(1, rows))
+    if step >= cols:
+        return u.T @ np.asarray(x_j, dtype=np.float64)
+    b = np.empty((u.shape[1], cols))
+    for c0 in range(0, cols, step):
+        b[:, c0:c0 + step] = u.T @ np.asarray(x_j[:, c0:c0 + step], dtype=np.float64)
+    return b
+
+
+def _x_v(x: np.ndarray, v: np.ndarray) -> np.ndarray:
+    """Y = X V with X promoted to fp64 a row chunk at a time (row by row the
+    same product)."""
+    rows, cols = x.shape
+    step = max(1, _CHUNK_ELEMS // max(1, cols))
+    if step >= rows:
+        return np.asarray(x, dtype=np.float64) @ v
+    y = np.empty((rows, v.shape[1]))
+    for r0 in range(0, rows, step):
+        y[r0:r0 + step] = np.asarray(x[r0:r0 + step], dtype=np.float64) @ v
+    return y
 
 
 def hierarchical_svd(x: np.ndarray, cfg: MatConfig, workers: int = 1) -> SvdFactor:
@@ -440,7 +470,7 @@ def recover_left_vectors(x: np.ndarray, v_r: np.ndarray) -> SvdFactor:
     defect = np.abs(v_r.T @ v_r - np.eye(r)).max()
     if defect > 1e-6:
         raise ValueError("recover_left_vectors: v_r columns are not orthonormal")
-    y = full_svd(np.asarray(x, dtype=np.float64) @ v_r)
+    y = full_svd(_x_v(x, v_r))
     return SvdFactor(u=y.u, sigma=y.sigma, v=v_r @ y.v)
 
 

@@ -3,8 +3,10 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <condition_variable>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <new>
 #include <string>
 #include <thread>
@@ -86,11 +88,110 @@ DType dtype_of(int dt) {
   throw Error(kInvalid, "dtype must be HSVD_CU_F32 or HSVD_CU_F64");
 }
 
+// Pageable host input (the C++ drop-in's std::vector storage): a copy
+// straight from it is staged by the driver and serialises with the caller.
+// Instead a host thread copies row chunks into a ring of pinned buffers
+// (the memcpy split over several threads) and issues each chunk's DMA on the
+// copy stream, while the calling thread launches the Grams of the chunks
+// already issued (x_wait_chunk blocks only until a chunk is issued).
+class PageableStager final : public HostStager {
+ public:
+  PageableStager(Ctx& c, char* dst, const char* src, int64_t row_bytes, int64_t src_pitch,
+                 std::vector<int64_t> ends, std::vector<cudaEvent_t> evs)
+      : c_(c), dst_(dst), src_(src), row_bytes_(row_bytes), pitch_(src_pitch),
+        ends_(std::move(ends)), evs_(std::move(evs)) {
+    th_ = std::thread([this] { run(); });
+  }
+  ~PageableStager() override {
+    if (th_.joinable()) th_.join();
+  }
+  void wait_issued(size_t i) override {
+    std::unique_lock<std::mutex> lk(mu_);
+    cv_.wait(lk, [&] { return issued_ > i || failed_; });
+    if (failed_) throw Error(kCuda, "host staging of the input failed: " + why_);
+  }
+
+ private:
+  void run() {
+    try {
+      HSVD_CUDA(cudaSetDevice(c_.device));
+      cudaStream_t cs = c_.get_copy_stream();
+      const unsigned hw = std::thread::hardware_concurrency();
+      const size_t nt = std::max(1u, std::min(8u, hw == 0 ? 1u : hw));
+      int64_t r0 = 0;
+      for (size_t i = 0; i < ends_.size(); ++i) {
+        const int slot = static_cast<int>(i % Ctx::kH2dSlots);
+        HSVD_CUDA(cudaEventSynchronize(c_.h2d_ev[slot]));  // slot's previous DMA done
+        char* pin = static_cast<char*>(c_.h2d_pin[slot]);
+        const int64_t rows = ends_[i] - r0;
+        const int64_t per = (rows + (int64_t)nt - 1) / (int64_t)nt;
+        auto piece = [&](int64_t a, int64_t b) {
+          if (pitch_ == row_bytes_) {
+            std::memcpy(pin + a * row_bytes_, src_ + (r0 + a) * pitch_, (size_t)((b - a) * row_bytes_));
+          } else {
+            for (int64_t r = a; r < b; ++r)
+              std::memcpy(pin + r * row_bytes_, src_ + (r0 + r) * pitch_, (size_t)row_bytes_);
+          }
+        };
+        std::vector<std::thread> th;
+        for (int64_t a = per; a < rows; a += per) {
+          const int64_t b = std::min(rows, a + per);
+          try {
+            th.emplace_back(piece, a, b);
+          } catch (...) {
+            piece(a, b);
+          }
+        }
+        piece(0, std::min(rows, per));
+        for (auto& t : th) t.join();
+        HSVD_CUDA(cudaMemcpyAsync(dst_ + r0 * row_bytes_, pin, (size_t)(rows * row_bytes_),
+                                  cudaMemcpyHostToDevice, cs));
+        HSVD_CUDA(cudaEventRecord(c_.h2d_ev[slot], cs));
+        HSVD_CUDA(cudaEventRecord(evs_[i], cs));
+        {
+          std::lock_guard<std::mutex> lk(mu_);
+          issued_ = i + 1;
+        }
+        cv_.notify_all();
+        r0 = ends_[i];
+      }
+    } catch (const std::exception& e) {
+      std::lock_guard<std::mutex> lk(mu_);
+      failed_ = true;
+      why_ = e.what();
+      cv_.notify_all();
+    }
+  }
+  Ctx& c_;
+  char* dst_;
+  const char* src_;
+  int64_t row_bytes_, pitch_;
+  std::vector<int64_t> ends_;
+  std::vector<cudaEvent_t> evs_;
+  std::thread th_;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  size_t issued_ = 0;
+  bool failed_ = false;
+  std::string why_;
+};
+
+bool is_pageable(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return a.type == cudaMemoryTypeUnregistered;
+}
+
 // Brings x to the device (contiguous, ld = n) unless it already is there.
 // Host input: copied into the arena.  With chunk_rows > 0 the copy runs on
 // the context's copy stream in row chunks of that height (one per row slice
 // of the plan), each marked by an event, so the leaf Grams of the first
 // slices overlap the transfer of the later ones (XView::ready).
+constexpr size_t kPageableMin = size_t(64) << 20;  // smaller inputs: one driver-staged copy
+
 XView stage_x(Ctx& c, const void* x, int dtype, int64_t m, int64_t n, int64_t ldx, int where,
               int64_t chunk_rows = 0) {
   if (!x) throw Error(kInvalid, "x is null");
@@ -103,6 +204,39 @@ XView stage_x(Ctx& c, const void* x, int dtype, int64_t m, int64_t n, int64_t ld
   void* d = c.arena.alloc((size_t)m * n * es);
   v.X = d;
   v.ld = n;
+  const int64_t row_bytes = n * (int64_t)es;
+  if ((size_t)(m * row_bytes) >= kPageableMin && row_bytes <= (int64_t)Ctx::kH2dChunk &&
+      is_pageable(x)) {
+    c.ensure_h2d_stage();
+    // chunk ends: pinned-buffer sized, and cut at the row-slice boundaries
+    const int64_t per = std::max<int64_t>(1, (int64_t)Ctx::kH2dChunk / row_bytes);
+    std::vector<int64_t> ends;
+    for (int64_t r = 0; r < m;) {
+      int64_t e = std::min(m, r + per);
+      if (chunk_rows > 0) e = std::min(e, (r / chunk_rows + 1) * chunk_rows);
+      ends.push_back(e);
+      r = e;
+    }
+    std::vector<cudaEvent_t> evs;
+    for (size_t i = 0; i < ends.size(); ++i) {
+      evs.push_back(c.get_chunk_event(i + 1));
+      v.ready.push_back({ends[i], evs.back()});
+    }
+    // the arena block may still be in use by earlier work on the compute stream
+    cudaStream_t cs = c.get_copy_stream();
+    cudaEvent_t start = c.get_chunk_event(0);
+    HSVD_CUDA(cudaEventRecord(start, c.stream));
+    HSVD_CUDA(cudaStreamWaitEvent(cs, start, 0));
+    v.stager = std::make_shared<PageableStager>(c, static_cast<char*>(d),
+                                                static_cast<const char*>(x), row_bytes,
+                                                ldx * (int64_t)es, std::move(ends), std::move(evs));
+    if (chunk_rows <= 0 || chunk_rows >= m) {
+      // the caller reads any row: order the compute stream after every chunk
+      x_wait_rows(c, v);
+      v.ready.clear();
+    }
+    return v;
+  }
   if (chunk_rows <= 0 || chunk_rows >= m) {
     HSVD_CUDA(cudaMemcpy2DAsync(d, n * es, x, ldx * es, n * es, m, cudaMemcpyHostToDevice, c.stream));
     return v;
@@ -797,6 +931,28 @@ int hsvd_cu_syevx_topk(hsvd_cu_ctx* ctx, const double* a, int64_t n, int64_t kk,
     eig_topk(c, {{A, n, (int)n, (int)kk, L, Z, n}});
     HSVD_CUDA(cudaMemcpyAsync(lam, L, kk * 8, cudaMemcpyDeviceToHost, c.stream));
     HSVD_CUDA(cudaMemcpyAsync(z, Z, (size_t)n * kk * 8, cudaMemcpyDeviceToHost, c.stream));
+    HSVD_CUDA(cudaStreamSynchronize(c.stream));
+    return HSVD_CU_OK;
+  });
+}
+
+int hsvd_cu_syevx_topk_batch(hsvd_cu_ctx* ctx, const double* a, int64_t count, int64_t n,
+                             int64_t kk, double* lam, double* z) {
+  return guarded([&] {
+    if (!a || !lam || !z || count < 1 || n < 1 || kk < 1 || kk > n)
+      throw Error(kInvalid, "syevx_topk_batch: bad arguments");
+    begin(ctx);
+    Ctx& c = ctx->c;
+    double* A = c.arena.alloc_n<double>((size_t)count * n * n);
+    double* L = c.arena.alloc_n<double>((size_t)count * kk);
+    double* Z = c.arena.alloc_n<double>((size_t)count * n * kk);
+    HSVD_CUDA(cudaMemcpyAsync(A, a, (size_t)count * n * n * 8, cudaMemcpyHostToDevice, c.stream));
+    std::vector<EigJob> jobs;
+    for (int64_t g = 0; g < count; ++g)
+      jobs.push_back({A + g * n * n, n, (int)n, (int)kk, L + g * kk, Z + g * n * kk, n});
+    eig_topk(c, jobs);
+    HSVD_CUDA(cudaMemcpyAsync(lam, L, (size_t)count * kk * 8, cudaMemcpyDeviceToHost, c.stream));
+    HSVD_CUDA(cudaMemcpyAsync(z, Z, (size_t)count * n * kk * 8, cudaMemcpyDeviceToHost, c.stream));
     HSVD_CUDA(cudaStreamSynchronize(c.stream));
     return HSVD_CU_OK;
   });

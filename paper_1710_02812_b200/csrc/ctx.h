@@ -226,6 +226,17 @@ struct Ctx {
       if (!d2h_ev[i]) HSVD_CUDA(cudaEventCreateWithFlags(&d2h_ev[i], cudaEventDisableTiming));
     }
   }
+  // pinned ring for pageable host inputs (PageableStager, capi.cu)
+  static constexpr size_t kH2dChunk = size_t(64) << 20;
+  static constexpr int kH2dSlots = 3;
+  void* h2d_pin[kH2dSlots] = {nullptr, nullptr, nullptr};
+  cudaEvent_t h2d_ev[kH2dSlots] = {nullptr, nullptr, nullptr};
+  void ensure_h2d_stage() {
+    for (int i = 0; i < kH2dSlots; ++i) {
+      if (!h2d_pin[i]) HSVD_CUDA(cudaMallocHost(&h2d_pin[i], kH2dChunk));
+      if (!h2d_ev[i]) HSVD_CUDA(cudaEventCreateWithFlags(&h2d_ev[i], cudaEventDisableTiming));
+    }
+  }
   // side stream for host->device input copies that overlap the compute
   // stream, and the events marking the copied row chunks
   cudaStream_t copy_stream = nullptr;
@@ -250,6 +261,10 @@ struct Ctx {
     }
     if (h_ints) cudaFreeHost(h_ints);
     if (h_dbl) cudaFreeHost(h_dbl);
+    for (int i = 0; i < kH2dSlots; ++i) {
+      if (h2d_ev[i]) cudaEventDestroy(h2d_ev[i]);
+      if (h2d_pin[i]) cudaFreeHost(h2d_pin[i]);
+    }
     for (int i = 0; i < 2; ++i) {
       if (d2h_ev[i]) cudaEventDestroy(d2h_ev[i]);
       if (d2h_pin[i]) cudaFreeHost(d2h_pin[i]);

@@ -67,12 +67,17 @@ void fetch_ranks(Ctx& ctx, const int* d_ranks, int count, std::vector<int>& out)
   std::memcpy(out.data(), h, count * sizeof(int));
 }
 
+void x_wait_chunk(Ctx& ctx, const XView& x, size_t i) {
+  if (x.stager) x.stager->wait_issued(i);
+  HSVD_CUDA(cudaStreamWaitEvent(ctx.stream, x.ready[i].ev, 0));
+}
+
 void x_wait_rows(Ctx& ctx, const XView& x, long long row_end) {
   long long prev = 0;
-  for (const RowChunk& c : x.ready) {
+  for (size_t i = 0; i < x.ready.size(); ++i) {
     if (row_end >= 0 && prev >= row_end) break;
-    HSVD_CUDA(cudaStreamWaitEvent(ctx.stream, c.ev, 0));
-    prev = c.row_end;
+    x_wait_chunk(ctx, x, i);
+    prev = x.ready[i].row_end;
   }
 }
 
@@ -131,7 +136,8 @@ std::vector<DFac> block_svd_batch(Ctx& ctx, const XView& x, const std::vector<Bl
     // (the copy stream is in order: chunk c done implies every earlier one)
     std::vector<GemmDesc> gt, gw;
     long long prev = 0;
-    for (const RowChunk& c : x.ready) {
+    for (size_t ci = 0; ci < x.ready.size(); ++ci) {
+      const RowChunk& c = x.ready[ci];
       gt.clear();
       gw.clear();
       size_t it = 0, iw = 0;
@@ -142,7 +148,8 @@ std::vector<DFac> block_svd_batch(Ctx& ctx, const XView& x, const std::vector<Bl
         if (bl.r0 + bl.d <= prev || bl.r0 + bl.d > c.row_end) continue;
         (tall ? gt : gw).push_back(gd);
       }
-      HSVD_CUDA(cudaStreamWaitEvent(ctx.stream, c.ev, 0));
+      if (gt.empty() && gw.empty()) continue;  // no block ends in this chunk
+      x_wait_chunk(ctx, x, ci);
       gemm_grouped(ctx, x.dt, x.dt, false, true, true, gt);
       gemm_grouped(ctx, x.dt, x.dt, true, false, true, gw);
       prev = c.row_end;

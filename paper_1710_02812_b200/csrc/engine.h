@@ -2,6 +2,7 @@
 // (and, with a communicator, on the row shards of several).
 #pragma once
 
+#include <memory>
 #include <vector>
 
 #include "ctx.h"
@@ -29,6 +30,14 @@ struct RowChunk {
   cudaEvent_t ev;
 };
 
+// Host thread that copies a pageable host input through pinned buffers
+// (capi.cu): chunk i's DMA and event are issued once wait_issued(i) returns.
+class HostStager {
+ public:
+  virtual ~HostStager() = default;
+  virtual void wait_issued(size_t i) = 0;
+};
+
 struct XView {
   const void* X;
   DType dt;
@@ -37,7 +46,13 @@ struct XView {
   // non-empty when X is still being copied in on the context's copy stream:
   // work on rows < row_end must wait for the chunk's event first
   std::vector<RowChunk> ready = {};
+  // set when the chunks are issued by a host staging thread (pageable input)
+  std::shared_ptr<HostStager> stager = {};
 };
+
+// Orders ctx.stream after chunk i of a staged input (waits on the host for
+// a staging thread to have issued it first).
+void x_wait_chunk(Ctx& ctx, const XView& x, size_t i);
 
 // Orders ctx.stream after the copies of rows [0, row_end) (all rows: -1).
 void x_wait_rows(Ctx& ctx, const XView& x, long long row_end = -1);

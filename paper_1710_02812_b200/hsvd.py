@@ -90,7 +90,7 @@ EXPORTED = [
     "hsvd_cu_thread_group_free", "hsvd_cu_ctx_join_group", "hsvd_cu_shard_rows",
     "hsvd_cu_rank_k_svd_sharded", "hsvd_cu_syevx_topk", "hsvd_cu_refine_factors",
     "hsvd_cu_factor_diff_norm", "hsvd_cu_rank_k_error", "hsvd_cu_residual_norm",
-    "hsvd_cu_load_hsvd1",
+    "hsvd_cu_load_hsvd1", "hsvd_cu_syevx_topk_batch",
 ]
 
 
@@ -177,6 +177,7 @@ def load_library(path: str = LIB_PATH):
         lib.hsvd_cu_shard_rows.argtypes = [I64, I64, I32, I32, C.POINTER(I64), C.POINTER(I64)]
         lib.hsvd_cu_rank_k_svd_sharded.argtypes = xargs + [I64, I64, C.POINTER(_Config), pp]
         lib.hsvd_cu_syevx_topk.argtypes = [P, P, I64, I64, P, P]
+        lib.hsvd_cu_syevx_topk_batch.argtypes = [P, P, I64, I64, I64, P, P]
         _lib = lib
         return lib
 
@@ -448,7 +449,7 @@ def rank_k_svd_sharded(x_local, m_total: int, row0: int, cfg: MatConfig, ctx: Co
         elif x_local is not None:
             dt = F32 if np.asarray(x_local).dtype == np.float32 else F64
     else:
-        p, dt, m, n, ld, where, _keep = _matrix_arg(x_local)
+        p, dt, m, n, ld, where, _keep = _matrix_arg(x_local, ctx)
     h = C.c_void_p()
     cc = cfg._c()
     _check(ctx.lib.hsvd_cu_rank_k_svd_sharded(ctx.handle, p, dt, m, n, ld, where, int(m_total),
@@ -477,9 +478,27 @@ def default_context() -> Context:
 # marshalling
 # --------------------------------------------------------------------------
 
-def _matrix_arg(x):
+def _order_after_torch(x, ctx: "Context") -> None:
+    """A CUDA tensor is produced on torch's current stream of its device; the
+    library reads it on the context's own (non-blocking) stream.  Reject a
+    tensor on another device, then make the context stream wait for
+    everything already queued on torch's stream (the producer of x, and of
+    the .contiguous() copy made here) -- the stream contract of
+    HSVD_CU_DEVICE inputs (include/hsvd_cu.h)."""
+    import torch
+    if x.device.index != ctx.device:
+        raise ValueError(f"matrix is on cuda:{x.device.index} but the context is on "
+                         f"cuda:{ctx.device}")
+    ev = torch.cuda.Event()
+    ev.record(torch.cuda.current_stream(x.device))
+    torch.cuda.ExternalStream(ctx.stream, device=x.device).wait_event(ev)
+
+
+def _matrix_arg(x, ctx: Optional["Context"] = None):
     """(pointer, dtype code, m, n, ld, where, keepalive) for numpy / torch /
-    a DeviceMatrix from load_hsvd1."""
+    a DeviceMatrix from load_hsvd1.  CUDA tensors are ordered after torch's
+    current stream on the context's stream (ctx defaults to the default
+    context)."""
     if isinstance(x, DeviceMatrix):
         return (x.ptr, F64, x.shape[0], x.shape[1], x.shape[1], DEVICE, x)
     mod = type(x).__module__
@@ -493,6 +512,8 @@ def _matrix_arg(x):
         if dt is None:
             raise ValueError("matrix dtype must be float32 or float64")
         where = DEVICE if x.is_cuda else HOST
+        if x.is_cuda:
+            _order_after_torch(x, _ctx(ctx))
         return (x.data_ptr(), dt, x.shape[0], x.shape[1], x.stride(0), where, x)
     a = np.asarray(x)
     if a.ndim != 2:
@@ -555,7 +576,7 @@ def hierarchical_svd(x, cfg: MatConfig, ctx: Optional[Context] = None) -> SvdFac
     """hsvd::hierarchical_svd (hierarchy.cpp:65-94) -> (Sigma, V), u absent."""
     validate(cfg)
     c = _ctx(ctx)
-    p, dt, m, n, ld, where, _keep = _matrix_arg(x)
+    p, dt, m, n, ld, where, _keep = _matrix_arg(x, c)
     if m == 0 or n == 0:
         raise ValueError("hierarchical_svd: matrix is empty")
     h = C.c_void_p()
@@ -568,7 +589,7 @@ def hierarchical_svd(x, cfg: MatConfig, ctx: Optional[Context] = None) -> SvdFac
 def recover_left_vectors(x, v_r, ctx: Optional[Context] = None) -> SvdFactor:
     """hsvd::recover_left_vectors (hierarchy.cpp:96-112) -> (U, Sigma, V)."""
     c = _ctx(ctx)
-    p, dt, m, n, ld, where, _keep = _matrix_arg(x)
+    p, dt, m, n, ld, where, _keep = _matrix_arg(x, c)
     vr = np.ascontiguousarray(np.asarray(v_r, dtype=np.float64))
     if vr.ndim != 2 or vr.shape[0] != n:
         raise ValueError("recover_left_vectors: v_r must have x.cols() rows")
@@ -593,7 +614,7 @@ def refine_factors(x, v_hat, sigma_hat, epsilon: float, max_iters: int,
     X V and U_outer^T X on the device until the relative sigma change is
     <= epsilon or max_iters is reached; non-convergence is reported."""
     c = _ctx(ctx)
-    p, dt, m, n, ld, where, _keep = _matrix_arg(x)
+    p, dt, m, n, ld, where, _keep = _matrix_arg(x, c)
     vh = np.ascontiguousarray(np.asarray(v_hat, dtype=np.float64))
     sh = np.ascontiguousarray(np.asarray(sigma_hat, dtype=np.float64).reshape(-1))
     if vh.ndim != 2:
@@ -685,7 +706,7 @@ def rank_k_error(full_of_x_or_x, approx: SvdFactor, k: int,
 def residual_norm(x, f: SvdFactor, ctx: Optional[Context] = None) -> float:
     """||X - U S V^T||_F on the device (x host/device, fp32/fp64)."""
     c = _ctx(ctx)
-    p, dt, m, n, ld, where, _keep = _matrix_arg(x)
+    p, dt, m, n, ld, where, _keep = _matrix_arg(x, c)
     sf, kf = _uv(f, "residual_norm")
     out = C.c_double(0.0)
     _check(c.lib.hsvd_cu_residual_norm(c.handle, p, dt, m, n, ld, where, C.byref(sf),
@@ -697,7 +718,7 @@ def rank_k_svd(x, cfg: MatConfig, ctx: Optional[Context] = None, want_u: bool = 
     """hierarchical_svd + recover_left_vectors in one device-resident call."""
     validate(cfg)
     c = _ctx(ctx)
-    p, dt, m, n, ld, where, _keep = _matrix_arg(x)
+    p, dt, m, n, ld, where, _keep = _matrix_arg(x, c)
     h = C.c_void_p()
     cc = cfg._c()
     _check(c.lib.hsvd_cu_rank_k_svd(c.handle, p, dt, m, n, ld, where, C.byref(cc), C.byref(h)))
@@ -707,7 +728,7 @@ def rank_k_svd(x, cfg: MatConfig, ctx: Optional[Context] = None, want_u: bool = 
 def rank_k_svd_device(x, cfg: MatConfig, ctx: Context) -> int:
     """rank_k_svd with the result left in device memory (benchmarks): returns
     the rank; no host copies are made."""
-    p, dt, m, n, ld, where, _keep = _matrix_arg(x)
+    p, dt, m, n, ld, where, _keep = _matrix_arg(x, ctx)
     h = C.c_void_p()
     cc = cfg._c()
     _check(ctx.lib.hsvd_cu_rank_k_svd(ctx.handle, p, dt, m, n, ld, where, C.byref(cc),
@@ -733,11 +754,24 @@ def syevx_topk(a, kk: int, ctx: Optional[Context] = None):
     return lam, z.T.copy()
 
 
+def syevx_topk_batch(a, kk: int, ctx: Optional[Context] = None):
+    """Top-kk eigenpairs of a batch of symmetric matrices (count x n x n) in
+    one launch set: (lam count x kk desc, Z count x n x kk)."""
+    cx = _ctx(ctx)
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+    count, n = a.shape[0], a.shape[1]
+    lam = np.empty((count, kk))
+    z = np.empty((count, kk, n))  # per matrix column-major n x kk
+    _check(cx.lib.hsvd_cu_syevx_topk_batch(cx.handle, a.ctypes.data, count, n, int(kk),
+                                           lam.ctypes.data, z.ctypes.data))
+    return lam, np.ascontiguousarray(z.transpose(0, 2, 1))
+
+
 def svd_of_col_slices(x_slice, c: int, gamma: float, max_rank: Optional[int] = None,
                       ctx: Optional[Context] = None) -> SvdFactor:
     """hsvd::svd_of_col_slices (hierarchy.cpp:50-63) -> (U, Sigma), v absent."""
     cx = _ctx(ctx)
-    p, dt, m, n, ld, where, _keep = _matrix_arg(x_slice)
+    p, dt, m, n, ld, where, _keep = _matrix_arg(x_slice, cx)
     h = C.c_void_p()
     _check(cx.lib.hsvd_cu_svd_of_col_slices(cx.handle, p, dt, m, n, ld, where, int(c),
                                             float(gamma), int(max_rank or 0), C.byref(h)))

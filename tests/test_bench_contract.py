@@ -26,3 +26,23 @@ def test_reference_arm_json_line():
     assert d["config"]["workload"].startswith("cfg1_")
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] == 2
+
+
+def test_gpus_n_spawns_ranks():
+    """`bench.py --gpus N` outside torchrun re-launches itself with N ranks
+    (torch.distributed.run, rendezvous on 127.0.0.1); rank 0 reports n_gpus = N.
+    The selftest rank body uses gloo so the launcher is checked without GPUs."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--launcher-selftest",
+                          "--gpus", "2"], capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["world_size"] == 2 and d["max_rank_plus_1"] == 2.0
+
+
+def test_gpus_mismatch_fails_loudly():
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2"],
+                         capture_output=True, text=True, timeout=120, cwd=ROOT, env=env)
+    assert out.returncode == 2 and "WORLD_SIZE=1" in out.stderr

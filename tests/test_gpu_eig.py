@@ -50,3 +50,50 @@ def test_syevx_topk_max_size(path, monkeypatch):
     res = np.abs(a @ z - z * lam).max()
     assert res <= 1e-10 * lam_true[0], res
     assert np.abs(z.T @ z - np.eye(kk)).max() < 1e-10
+
+
+def _check_batch(a, lam, z, kk, tol_lam=1e-12, tol_res=1e-11):
+    for g in range(a.shape[0]):
+        w, _ = np.linalg.eigh(a[g])
+        w = w[::-1][:kk]
+        assert np.abs(lam[g] - w).max() <= tol_lam * w[0], g
+        res = np.abs(a[g] @ z[g] - z[g] * lam[g]).max()
+        assert res <= tol_res * w[0], (g, res)
+        assert np.abs(z[g].T @ z[g] - np.eye(kk)).max() < 1e-10, g
+
+
+def test_batch_over_74_runs_one_cta_chase(monkeypatch):
+    """Batches of more than 74 matrices run the bulge chase one CTA per
+    matrix (k_chase<false>, syev_band.cu) -- the variant config 5's 256
+    leaves use; every matrix against LAPACK."""
+    import paper_1710_02812_b200 as H
+    monkeypatch.setenv("HSVD_TWO_STAGE_MIN_N", "1")
+    n, kk, count = 288, 40, 80
+    a = np.stack([_gram(n, 1000 + g, 5.0) for g in range(count)])
+    lam, z = H.syevx_topk_batch(a, kk)
+    _check_batch(a, lam, z, kk)
+
+
+def test_chase_cs1_forced(monkeypatch):
+    """HSVD_CHASE_CS=1 forces the one-CTA chase on a small batch too."""
+    import paper_1710_02812_b200 as H
+    monkeypatch.setenv("HSVD_TWO_STAGE_MIN_N", "1")
+    monkeypatch.setenv("HSVD_CHASE_CS", "1")
+    n, kk, count = 640, 64, 3
+    a = np.stack([_gram(n, 2000 + g, 6.0) for g in range(count)])
+    lam, z = H.syevx_topk_batch(a, kk)
+    _check_batch(a, lam, z, kk)
+
+
+def test_n4096_q2_apply_four_columns():
+    """n = 4096, kk = 200: config 5's leaf eigenproblem (two-stage by size,
+    Q2 back-transform with 4 eigenvector columns per CTA, k_q2_apply<4>)."""
+    import paper_1710_02812_b200 as H
+    n, kk, count = 4096, 200, 2
+    rng = np.random.default_rng(4096)
+    a = np.empty((count, n, n))
+    for g in range(count):
+        x = rng.standard_normal((n, n)) * np.exp(-np.linspace(0, 7, n))[None, :]
+        a[g] = x.T @ x
+    lam, z = H.syevx_topk_batch(a, kk)
+    _check_batch(a, lam, z, kk, tol_lam=1e-11, tol_res=1e-10)
