@@ -202,6 +202,13 @@ int hsvd_cu_syevx_topk(hsvd_cu_ctx* ctx, const double* a, int64_t n, int64_t kk,
 int hsvd_cu_syevx_topk_batch(hsvd_cu_ctx* ctx, const double* a, int64_t count, int64_t n,
                              int64_t kk, double* lam, double* z);
 
+/* Building block: the leaf Gram G = X_b^T X_b (c x c, written row-major =
+ * column-major, symmetric full storage) of a d x c row-major block, computed
+ * as the leaf stage does: fp32 blocks on the tcgen05 int8 tensor cores
+ * (Ozaki slices, fp64-grade), fp64 blocks on the fp64 DMMA SYRK. */
+int hsvd_cu_block_gram(hsvd_cu_ctx* ctx, const void* x, int dtype, int64_t d, int64_t c,
+                       int64_t ldx, int where, double* g);
+
 /* ---- multi-GPU (one process / thread per GPU, rows sharded) ---------- */
 typedef struct hsvd_cu_group hsvd_cu_group;
 /* NCCL: rank 0 creates the 128-byte id and shares it; every rank inits. */

@@ -17,6 +17,7 @@
 #include "engine.h"
 #include "factor_ops.h"
 #include "metrics.h"
+#include "ozaki.h"
 #include "syev.h"
 
 using namespace hsvdcu;
@@ -954,6 +955,23 @@ int hsvd_cu_syevx_topk_batch(hsvd_cu_ctx* ctx, const double* a, int64_t count, i
     HSVD_CUDA(cudaMemcpyAsync(lam, L, (size_t)count * kk * 8, cudaMemcpyDeviceToHost, c.stream));
     HSVD_CUDA(cudaMemcpyAsync(z, Z, (size_t)count * n * kk * 8, cudaMemcpyDeviceToHost, c.stream));
     HSVD_CUDA(cudaStreamSynchronize(c.stream));
+    return HSVD_CU_OK;
+  });
+}
+
+int hsvd_cu_block_gram(hsvd_cu_ctx* ctx, const void* x, int dtype, int64_t d, int64_t c,
+                       int64_t ldx, int where, double* g) {
+  return guarded([&] {
+    if (!g) throw Error(kInvalid, "block_gram: g is null");
+    begin(ctx);
+    Ctx& cc = ctx->c;
+    XView xv = stage_x(cc, x, dtype, d, c, ldx, where);
+    if (c > 65536 || d > 65536) throw Error(kInvalid, "block_gram: block too large");
+    double* G = cc.arena.alloc_n<double>((size_t)c * c);
+    std::vector<GemmDesc> one{{xv.X, xv.X, G, xv.ld, xv.ld, c, (int)c, (int)c, (int)d, 1.0, 0.0}};
+    leaf_gram_tall(cc, xv.dt, one);
+    HSVD_CUDA(cudaMemcpyAsync(g, G, (size_t)c * c * 8, cudaMemcpyDeviceToHost, cc.stream));
+    HSVD_CUDA(cudaStreamSynchronize(cc.stream));
     return HSVD_CU_OK;
   });
 }

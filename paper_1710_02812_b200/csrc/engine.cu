@@ -9,6 +9,7 @@
 #include <string>
 
 #include "engine.h"
+#include "ozaki.h"
 #include "factor_ops.h"
 #include "syev.h"
 
@@ -81,6 +82,16 @@ void x_wait_rows(Ctx& ctx, const XView& x, long long row_end) {
   }
 }
 
+// Leaf Grams G = Xt Xt^T of tall blocks: fp32 blocks on the tcgen05 int8
+// tensor cores (Ozaki slices, fp64-grade; ozaki_gram.cu), fp64 blocks (and
+// HSVD_GRAM=dmma) on the fp64 DMMA SYRK.
+void leaf_gram_tall(Ctx& ctx, DType dt, const std::vector<GemmDesc>& descs) {
+  std::vector<GemmDesc> oz, dm;
+  for (const GemmDesc& g : descs) (ozaki_gram_applicable(dt, g) ? oz : dm).push_back(g);
+  ozaki_gram_batch(ctx, oz);
+  gemm_grouped(ctx, dt, dt, false, true, true, dm);
+}
+
 // ---------------------------------------------------------------------------
 // block SVD (leaves): Gram of the smaller side + top-k eigenpairs + projection
 // ---------------------------------------------------------------------------
@@ -128,7 +139,7 @@ std::vector<DFac> block_svd_batch(Ctx& ctx, const XView& x, const std::vector<Bl
   }
   ctx.phase = "leaf.gram";
   if (x.ready.empty()) {
-    gemm_grouped(ctx, x.dt, x.dt, false, true, true, gram_t);
+    leaf_gram_tall(ctx, x.dt, gram_t);
     gemm_grouped(ctx, x.dt, x.dt, true, false, true, gram_w);
   } else {
     // input still arriving: one Gram launch per row-chunk group of blocks,
@@ -150,7 +161,7 @@ std::vector<DFac> block_svd_batch(Ctx& ctx, const XView& x, const std::vector<Bl
       }
       if (gt.empty() && gw.empty()) continue;  // no block ends in this chunk
       x_wait_chunk(ctx, x, ci);
-      gemm_grouped(ctx, x.dt, x.dt, false, true, true, gt);
+      leaf_gram_tall(ctx, x.dt, gt);
       gemm_grouped(ctx, x.dt, x.dt, true, false, true, gw);
       prev = c.row_end;
     }

@@ -76,6 +76,10 @@ struct HsvdConfig {
   int cap = 0;  // max_rank, 0 = none
 };
 
+// Leaf Grams G = Xt Xt^T (tall blocks, SYRK descriptors): fp32 on the
+// tcgen05 int8 Ozaki path, fp64 on the DMMA SYRK (engine.cu).
+void leaf_gram_tall(Ctx& ctx, DType dt, const std::vector<GemmDesc>& descs);
+
 // Exact thin SVD of each block, truncated (hierarchy.cpp:57: truncate_factor
 // (full_svd(block))).  keep_both: also return the other side in B2.
 std::vector<DFac> block_svd_batch(Ctx& ctx, const XView& x, const std::vector<Block>& blocks,

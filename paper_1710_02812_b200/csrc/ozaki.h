@@ -1,0 +1,21 @@
+// Leaf block Gram on tcgen05 kind::i8 (Ozaki slicing, fp64-grade): ozaki_gram.cu
+#pragma once
+
+#include <vector>
+
+#include "ctx.h"
+#include "gemm.h"
+
+namespace hsvdcu {
+
+// True when the SYRK descriptor (G = Xt Xt^T of a row-major fp32 block, as
+// block_svd_batch builds it) runs on the int8 tensor-core Gram.  Disabled by
+// HSVD_GRAM=dmma (then the fp64 DMMA SYRK runs).
+bool ozaki_gram_applicable(DType dt, const GemmDesc& d);
+
+// G (full symmetric storage, column-major ldc) = A A^T for every descriptor
+// (A = the row-major d x c fp32 block viewed column-major c x d, lda; M = N =
+// c, K = d).
+void ozaki_gram_batch(Ctx& ctx, const std::vector<GemmDesc>& descs);
+
+}  // namespace hsvdcu

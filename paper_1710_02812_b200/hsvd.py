@@ -90,7 +90,7 @@ EXPORTED = [
     "hsvd_cu_thread_group_free", "hsvd_cu_ctx_join_group", "hsvd_cu_shard_rows",
     "hsvd_cu_rank_k_svd_sharded", "hsvd_cu_syevx_topk", "hsvd_cu_refine_factors",
     "hsvd_cu_factor_diff_norm", "hsvd_cu_rank_k_error", "hsvd_cu_residual_norm",
-    "hsvd_cu_load_hsvd1", "hsvd_cu_syevx_topk_batch",
+    "hsvd_cu_load_hsvd1", "hsvd_cu_syevx_topk_batch", "hsvd_cu_block_gram",
 ]
 
 
@@ -178,6 +178,7 @@ def load_library(path: str = LIB_PATH):
         lib.hsvd_cu_rank_k_svd_sharded.argtypes = xargs + [I64, I64, C.POINTER(_Config), pp]
         lib.hsvd_cu_syevx_topk.argtypes = [P, P, I64, I64, P, P]
         lib.hsvd_cu_syevx_topk_batch.argtypes = [P, P, I64, I64, I64, P, P]
+        lib.hsvd_cu_block_gram.argtypes = [P, P, I32, I64, I64, I64, I32, P]
         _lib = lib
         return lib
 
@@ -765,6 +766,16 @@ def syevx_topk_batch(a, kk: int, ctx: Optional[Context] = None):
     _check(cx.lib.hsvd_cu_syevx_topk_batch(cx.handle, a.ctypes.data, count, n, int(kk),
                                            lam.ctypes.data, z.ctypes.data))
     return lam, np.ascontiguousarray(z.transpose(0, 2, 1))
+
+
+def block_gram(x, ctx: Optional[Context] = None) -> np.ndarray:
+    """Leaf Gram X^T X of a d x c block as the leaf stage computes it (fp32:
+    tcgen05 int8 Ozaki slices; fp64: DMMA SYRK)."""
+    cx = _ctx(ctx)
+    p, dt, m, n, ld, where, _keep = _matrix_arg(x, cx)
+    g = np.empty((n, n))
+    _check(cx.lib.hsvd_cu_block_gram(cx.handle, p, dt, m, n, ld, where, g.ctypes.data))
+    return g
 
 
 def svd_of_col_slices(x_slice, c: int, gamma: float, max_rank: Optional[int] = None,
