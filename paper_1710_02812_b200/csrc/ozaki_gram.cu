@@ -30,9 +30,12 @@
 //                 ring, warp 1 issues tcgen05.mma (M=128, N=256, K=32 per
 //                 instruction) into one of two TMEM accumulators (levels
 //                 alternate, 2 x 256 columns), warps 2-5 drain a finished level
-//                 (tcgen05.ld) and accumulate it in fp64 into G while the next
-//                 level is being multiplied
-//   k_oz_mirror   strict upper triangle <- lower (full storage for the
+//                 (tcgen05.ld) to an int32 level tile in global memory while
+//                 the next level is being multiplied (store-only: an epilogue
+//                 that read-modify-wrote fp64 G per level held the MMA warp on
+//                 the TMEM-empty barrier; ncu, profiles/r02_oz_gram_cfg5.md)
+//   k_oz_combine  G = scales * sum_t 2^-w(t) P_t in fp64 for j >= l, mirrored
+//                 to the strict upper triangle (full storage for the
 //                 eigensolver)
 #include <cuda.h>
 
@@ -246,7 +249,8 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, int (&v)[32]) {
 
 __global__ void __launch_bounds__(kGramThreads, 1)
     k_oz_gram(const __grid_constant__ CUtensorMap tmap, const OzLeaf* __restrict__ leaves,
-              const OzTile* __restrict__ tiles, long long plane_rows, int nk) {
+              const OzTile* __restrict__ tiles, long long plane_rows, int nk,
+              int* __restrict__ part) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -344,36 +348,24 @@ __global__ void __launch_bounds__(kGramThreads, 1)
       }
     }
   } else {
-    // ---------------- epilogue: TMEM -> fp64 accumulation in G ----------------
+    // ---------------- epilogue: TMEM -> int32 level tiles (store only) ----------------
+    // level t of this tile -> P[tile][t-2][col][row] (a warp stores 32
+    // consecutive rows of one column: 128 contiguous bytes); no global reads,
+    // so a drained accumulator is released as fast as TMEM can be read
     const int quarter = warp & 3;  // TMEM lanes 32*quarter .. +31 (warp % 4 rule)
     const int r = quarter * 32 + lane;
-    const int row = T.jb * kBM + r;
-    const bool row_ok = row < L.q;
-    const double srow = row_ok ? L.scale[row] : 0.0;
-    double* grow = L.G + row;
+    int* P = part + (long long)blockIdx.x * (kS * kBN * kBM) + r;
     for (int t = 2; t <= kS + 1; ++t) {
       const int buf = t & 1;
       mbar_wait(&tfull[buf], ((t - 2) >> 1) & 1);
       tc_fence_after();
-      const double w = ldexp(1.0, -(12 + 7 * (t - 2)));
-      const bool last = t == kS + 1;
+      int* Pt = P + (t - 2) * (kBN * kBM);
 #pragma unroll 1
       for (int c0 = 0; c0 < kBN; c0 += 32) {
         int v[32];
         tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + buf * kBN + c0, v);
-        const int col0 = T.lb * kBN + c0;
-        if (row_ok) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const int col = col0 + i;
-            if (col < L.q) {
-              double* g = grow + (long long)col * L.ldg;
-              double acc = (t == 2 ? 0.0 : *g) + w * (double)v[i];
-              if (last) acc *= srow * __ldg(L.scale + col);
-              *g = acc;
-            }
-          }
-        }
+        for (int i = 0; i < 32; ++i) Pt[(c0 + i) * kBM] = v[i];
       }
       tc_fence_before();
       __syncwarp();
@@ -388,22 +380,43 @@ __global__ void __launch_bounds__(kGramThreads, 1)
   }
 }
 
-// strict upper triangle <- lower, 32x32 tiles through shared memory
-__global__ void k_oz_mirror(const OzLeaf* __restrict__ leaves) {
-  __shared__ double tile[32][33];
-  const OzLeaf L = leaves[blockIdx.z];
-  const int bi = blockIdx.x, bj = blockIdx.y;  // source tile: rows bi (lower), cols bj
-  if (bi < bj || bi * 32 >= L.q) return;
-  const int tx = threadIdx.x, ty = threadIdx.y;
-  for (int y = ty; y < 32; y += 8) {
-    const int row = bi * 32 + y, col = bj * 32 + tx;
-    if (row < L.q && col < L.q) tile[y][tx] = L.G[row + (long long)col * L.ldg];
-  }
-  __syncthreads();
-  for (int y = ty; y < 32; y += 8) {
-    // destination (row' = col, col' = row) with row' < col'
-    const int drow = bj * 32 + tx, dcol = bi * 32 + y;
-    if (drow < L.q && dcol < L.q && drow < dcol) L.G[drow + (long long)dcol * L.ldg] = tile[y][tx];
+// G from the int32 level tiles: G_jl = 2^(e_j+e_l) sum_t 2^-(12+7(t-2)) P_t
+// (most significant level first, fp64), written for j >= l and mirrored to
+// (l, j) through a shared-memory transpose (full symmetric storage for the
+// eigensolver).  One CTA per Gram tile, 32x32 sub-blocks.
+__global__ void __launch_bounds__(256) k_oz_combine(const OzLeaf* __restrict__ leaves,
+                                                    const OzTile* __restrict__ tiles,
+                                                    const int* __restrict__ part) {
+  __shared__ double sub[32][33];
+  const OzTile T = tiles[blockIdx.x];
+  const OzLeaf L = leaves[T.leaf];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int* P = part + (long long)blockIdx.x * (kS * kBN * kBM);
+  for (int rb = 0; rb < kBM; rb += 32) {
+    const int row0 = T.jb * kBM + rb;
+    for (int cb = 0; cb < kBN; cb += 32) {
+      const int col0 = T.lb * kBN + cb;
+      if (row0 + 31 < col0 || row0 >= L.q || col0 >= L.q) continue;  // no j >= l element
+      const int row = row0 + tx;
+      const double sr = row < L.q ? L.scale[row] : 0.0;
+      for (int y = ty; y < 32; y += 8) {
+        const int col = col0 + y;
+        const int* p = P + (cb + y) * kBM + rb + tx;
+        double acc = 0.0;
+#pragma unroll
+        for (int t = 0; t < kS; ++t) acc += ldexp((double)__ldcs(p + t * kBN * kBM), -(12 + 7 * t));
+        acc *= sr * (col < L.q ? L.scale[col] : 0.0);
+        sub[y][tx] = acc;
+        if (row < L.q && col < L.q && row >= col) L.G[row + (long long)col * L.ldg] = acc;
+      }
+      __syncthreads();
+      for (int y = ty; y < 32; y += 8) {
+        // mirror: (row0 + y, col0 + tx) <- sub[tx][y] when row0 + y > col0 + tx
+        const int mrow = col0 + tx, mcol = row0 + y;
+        if (mcol < L.q && mrow < L.q && mcol > mrow) L.G[mrow + (long long)mcol * L.ldg] = sub[tx][y];
+      }
+      __syncthreads();
+    }
   }
 }
 
@@ -456,8 +469,10 @@ void ozaki_gram_batch(Ctx& ctx, const std::vector<GemmDesc>& descs) {
     long long rows = 0;
     while (i1 < descs.size()) {
       const long long qp = (long long)ceil_div(descs[i1].M, kBN) * kBN;
-      if (i1 > i0 && (size_t)((rows + kS * qp) * kpad) > kPlaneBudget) break;
-      rows += kS * qp;
+      // planes (S q_pad K_pad bytes) + level tiles (~ S q_pad^2 / 2 int32)
+      const long long need = kS * qp * kpad + 2LL * kS * qp * (qp + kBN);
+      if (i1 > i0 && (size_t)(rows + need) > kPlaneBudget) break;
+      rows += need;
       ++i1;
     }
     Arena::Mark mk = ctx.arena.mark();
@@ -515,14 +530,14 @@ void ozaki_gram_batch(Ctx& ctx, const std::vector<GemmDesc>& descs) {
     for (int l = 0; l < nl; ++l)
       flops += (double)descs[i0 + l].M * (descs[i0 + l].M + 1) * descs[i0 + l].K;
     ctx.pending_flops = flops;  // algorithmic (fp64-equivalent SYRK) flops
+    int* part = ctx.arena.alloc_n<int>(ht.size() * (size_t)kS * kBN * kBM);
     ctx.launch_begin();
     k_oz_gram<<<(unsigned)ht.size(), kGramThreads, kGramSmem, ctx.stream>>>(
-        tmap, dl, dt, plane_rows, static_cast<int>(kpad / kBK));
+        tmap, dl, dt, plane_rows, static_cast<int>(kpad / kBK), part);
     ctx.check_launch("k_oz_gram");
-    const int nb = ceil_div(max_qp, 32);
     ctx.launch_begin();
-    k_oz_mirror<<<dim3(nb, nb, nl), dim3(32, 8), 0, ctx.stream>>>(dl);
-    ctx.check_launch("k_oz_mirror");
+    k_oz_combine<<<(unsigned)ht.size(), 256, 0, ctx.stream>>>(dl, dt, part);
+    ctx.check_launch("k_oz_combine");
     ctx.arena.release(mk);
     i0 = i1;
   }
