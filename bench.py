@@ -283,6 +283,50 @@ def fp64_peak_tflops(torch, dev):
     return 2.0 * n ** 3 / (best / 1000.0) / 1e12
 
 
+def int8_peak_tops(torch, dev):
+    """Measured int8 tensor throughput (cuBLASLt through torch._int_mm,
+    8192^3, best of 5): the roofline denominator of k_oz_gram (the
+    MEASURED_PEAKS.json figures are bf16 only).  None if unavailable."""
+    n = 8192
+    try:
+        a = torch.randint(-64, 64, (n, n), dtype=torch.int8, device=dev)
+        b = torch.randint(-64, 64, (n, n), dtype=torch.int8, device=dev).t().contiguous().t()
+        torch._int_mm(a, b)
+        best = 1e9
+        for _ in range(6):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch._int_mm(a, b)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        del a, b
+        return 2.0 * n ** 3 / (best / 1000.0) / 1e12
+    except Exception:  # pragma: no cover
+        return None
+
+
+def ozaki_roofline(prof, steps, torch, dev):
+    """k_oz_gram (leaf Gram on tcgen05 kind::i8): achieved int8 tensor ops per
+    second (every tile x 28 slice products x padded K, counted by the
+    library) against the measured int8 GEMM peak."""
+    fam = kernel_families(prof)
+    if "k_oz_gram" not in fam:
+        return None
+    cnt, ms, ops = fam["k_oz_gram"]
+    achieved = ops / (ms / 1000.0) / 1e12
+    peak = int8_peak_tops(torch, dev)
+    nominal = 4500.0
+    return {"kernel": "k_oz_gram", "bound": "tensor", "achieved": achieved,
+            "peak": peak if peak else nominal, "unit": "TOP/s (int8)",
+            "frac": achieved / (peak if peak else nominal),
+            "frac_of_nominal_4500": achieved / nominal,
+            "peak_source": ("int8 cuBLASLt GEMM 8192^3 (torch._int_mm) measured in this run"
+                            if peak else "nominal B200 dense int8 4.5 POP/s (no measurement)"),
+            "algorithmic_ops_per_launch": ops / cnt, "avg_launch_ms": ms / cnt,
+            "launches_per_step": cnt / steps}
+
+
 def kernel_families(prof):
     """{kernel name: (launches, ms, flops)} summed over phases."""
     fam = {}
@@ -472,6 +516,9 @@ def run_ours(args, w):
     roof["measured"] = ("per-launch CUDA events over a second timed pass of the same K steps "
                         "(the headline pass runs without them)")
     roof["profiled_pass_ms_per_step"] = ms_prof
+    oz = ozaki_roofline(prof, args.steps, torch, dev)
+    if oz is not None:
+        roof["leaf_gram_int8"] = oz
 
     cpu = None
     if not args.no_cpu_baseline and ws == 1:

@@ -15,6 +15,7 @@
  *   hsvd_cu_merge_pair           hsvd::merge_pair_qr /       merge.hpp:19-30, merge.cpp:42-117
  *                                hsvd::merge_pair_naive
  *   hsvd_cu_full_svd             hsvd::full_svd              kernels.hpp:26, kernels.cpp:21-48
+ *   hsvd_cu_qr_thin              hsvd::qr_thin               kernels.hpp:29, kernels.cpp:50-61
  *   hsvd_cu_refine_factors       hsvd::refine_factors        refine.hpp:18-21, refine.cpp:26-72
  *
  * Matrices crossing the boundary use the reference's DenseMatrix layout:
@@ -201,6 +202,14 @@ int hsvd_cu_syevx_topk(hsvd_cu_ctx* ctx, const double* a, int64_t n, int64_t kk,
  * z = count consecutive n x kk column-major blocks. */
 int hsvd_cu_syevx_topk_batch(hsvd_cu_ctx* ctx, const double* a, int64_t count, int64_t n,
                              int64_t kk, double* lam, double* z);
+
+/* hsvd::qr_thin (kernels.hpp:29, kernels.cpp:50-61): Householder thin QR of
+ * the m x n row-major a (host, lda): q (m x p row-major), r (p x n row-major,
+ * upper trapezoidal), p = min(m, n); dgeqrf/Eigen sign convention (R_jj =
+ * -sign(a_jj) * ||column||).  EINVAL "qr_thin: matrix is empty" for m or n = 0
+ * (kernels.cpp:51-53). */
+int hsvd_cu_qr_thin(hsvd_cu_ctx* ctx, const double* a, int64_t m, int64_t n, int64_t lda,
+                    double* q, double* r);
 
 /* Building block: the leaf Gram G = X_b^T X_b (c x c, written row-major =
  * column-major, symmetric full storage) of a d x c row-major block, computed

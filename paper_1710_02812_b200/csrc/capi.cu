@@ -16,6 +16,7 @@
 #include "comm.h"
 #include "engine.h"
 #include "factor_ops.h"
+#include "jacobi.h"
 #include "metrics.h"
 #include "ozaki.h"
 #include "syev.h"
@@ -955,6 +956,30 @@ int hsvd_cu_syevx_topk_batch(hsvd_cu_ctx* ctx, const double* a, int64_t count, i
     HSVD_CUDA(cudaMemcpyAsync(lam, L, (size_t)count * kk * 8, cudaMemcpyDeviceToHost, c.stream));
     HSVD_CUDA(cudaMemcpyAsync(z, Z, (size_t)count * n * kk * 8, cudaMemcpyDeviceToHost, c.stream));
     HSVD_CUDA(cudaStreamSynchronize(c.stream));
+    return HSVD_CU_OK;
+  });
+}
+
+int hsvd_cu_qr_thin(hsvd_cu_ctx* ctx, const double* a, int64_t m, int64_t n, int64_t lda,
+                    double* q, double* r) {
+  return guarded([&] {
+    if (!a || m <= 0 || n <= 0) throw Error(kInvalid, "qr_thin: matrix is empty");
+    if (!q || !r || lda < n) throw Error(kInvalid, "qr_thin: bad arguments");
+    if (m > 0x7fffffffLL || n > 0x7fffffffLL) throw Error(kInvalid, "qr_thin: dimension too large");
+    begin(ctx);
+    Ctx& c = ctx->c;
+    const int64_t p = std::min(m, n);
+    double* A = stage_rowmajor(c, a, m, n, lda, HSVD_CU_HOST);  // column-major m x n
+    double* Q = c.arena.alloc_n<double>((size_t)m * p);
+    householder_qr(c, A, (int)m, (int)n, Q);
+    std::vector<double> ha((size_t)m * n), hq((size_t)m * p);
+    HSVD_CUDA(cudaMemcpyAsync(ha.data(), A, ha.size() * 8, cudaMemcpyDeviceToHost, c.stream));
+    HSVD_CUDA(cudaMemcpyAsync(hq.data(), Q, hq.size() * 8, cudaMemcpyDeviceToHost, c.stream));
+    HSVD_CUDA(cudaStreamSynchronize(c.stream));
+    for (int64_t i = 0; i < m; ++i)
+      for (int64_t j = 0; j < p; ++j) q[i * p + j] = hq[i + j * m];
+    for (int64_t i = 0; i < p; ++i)
+      for (int64_t j = 0; j < n; ++j) r[i * n + j] = j >= i ? ha[i + j * m] : 0.0;
     return HSVD_CU_OK;
   });
 }

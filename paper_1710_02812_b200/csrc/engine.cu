@@ -9,6 +9,7 @@
 #include <string>
 
 #include "engine.h"
+#include "jacobi.h"
 #include "ozaki.h"
 #include "factor_ops.h"
 #include "syev.h"
@@ -101,7 +102,7 @@ std::vector<DFac> block_svd_batch(Ctx& ctx, const XView& x, const std::vector<Bl
   std::vector<DFac> out(nb);
   if (nb == 0) return out;
   struct Tmp {
-    bool tall;
+    bool tall, jac;
     int q, kk, s;
     double *G, *lam, *Z, *P, *Bp, *sig;
     int* perm;
@@ -109,6 +110,7 @@ std::vector<DFac> block_svd_batch(Ctx& ctx, const XView& x, const std::vector<Bl
   std::vector<Tmp> t(nb);
   std::vector<GemmDesc> gram_t, gram_w, proj_t, proj_w;
   std::vector<EigJob> ej;
+  std::vector<JacJob> jj;
   int* d_rd = ctx.arena.alloc_n<int>(2 * (size_t)nb);
   for (int b = 0; b < nb; ++b) {
     const Block& bl = blocks[b];
@@ -118,14 +120,30 @@ std::vector<DFac> block_svd_batch(Ctx& ctx, const XView& x, const std::vector<Bl
     const int p = std::min(bl.d, bl.c);
     m.kk = cap > 0 ? std::min(cap, p) : p;
     m.s = m.tall ? bl.d : bl.c;
-    m.G = ctx.arena.alloc_n<double>((size_t)m.q * m.q);
-    m.lam = ctx.arena.alloc_n<double>(m.kk);
-    m.Z = ctx.arena.alloc_n<double>((size_t)m.q * m.kk);
-    m.P = ctx.arena.alloc_n<double>((size_t)m.s * m.kk);
+    // kernels.cpp:28: the smaller side <= 32 -> one-sided Jacobi on the block
+    // itself (all q columns, ordered by norm; the cap is finalize's)
+    m.jac = small_svd_jacobi(m.s, m.q);
     m.Bp = ctx.arena.alloc_n<double>((size_t)m.s * m.kk);
     m.sig = ctx.arena.alloc_n<double>(m.kk);
     m.perm = ctx.arena.alloc_n<int>(m.kk);
     const void* base = xptr(x, bl.r0, bl.c0);
+    if (m.jac) {
+      m.G = m.lam = nullptr;
+      m.Z = ctx.arena.alloc_n<double>((size_t)m.q * m.q);
+      m.P = ctx.arena.alloc_n<double>((size_t)m.s * m.q);
+      const int f64 = x.dt == DType::F64 ? 1 : 0;
+      if (m.tall)  // columns of the block: (i, j) at base + i*ld + j
+        jj.push_back({base, f64, x.ld, 1, m.q, nullptr, nullptr, 0, 0, nullptr, m.s, nullptr,
+                      m.P, m.s, m.Z, m.q});
+      else  // columns of the block's transpose: (i, j) at base + j*ld + i
+        jj.push_back({base, f64, 1, x.ld, m.q, nullptr, nullptr, 0, 0, nullptr, m.s, nullptr,
+                      m.P, m.s, m.Z, m.q});
+      continue;
+    }
+    m.G = ctx.arena.alloc_n<double>((size_t)m.q * m.q);
+    m.lam = ctx.arena.alloc_n<double>(m.kk);
+    m.Z = ctx.arena.alloc_n<double>((size_t)m.q * m.kk);
+    m.P = ctx.arena.alloc_n<double>((size_t)m.s * m.kk);
     // column-major view of the row-major block: Xt (c x d, ld = x.ld)
     if (m.tall)  // G = X_b^T X_b = Xt Xt^T
       gram_t.push_back({base, base, m.G, x.ld, x.ld, m.q, m.q, m.q, bl.d, 1.0, 0.0});
@@ -153,6 +171,7 @@ std::vector<DFac> block_svd_batch(Ctx& ctx, const XView& x, const std::vector<Bl
       gw.clear();
       size_t it = 0, iw = 0;
       for (int b = 0; b < nb; ++b) {
+        if (t[b].jac) continue;
         const bool tall = t[b].tall;
         const GemmDesc& gd = tall ? gram_t[it++] : gram_w[iw++];
         const Block& bl = blocks[b];
@@ -172,6 +191,8 @@ std::vector<DFac> block_svd_batch(Ctx& ctx, const XView& x, const std::vector<Bl
   ctx.phase = "leaf.proj";
   gemm_grouped(ctx, x.dt, DType::F64, true, false, false, proj_t);
   gemm_grouped(ctx, x.dt, DType::F64, false, false, false, proj_w);
+  ctx.phase = "leaf.jacobi";
+  jacobi_svd_batch(ctx, jj);
   ctx.phase = "leaf.fin";
   std::vector<FinJob> fj;
   for (int b = 0; b < nb; ++b) {
@@ -241,6 +262,7 @@ std::vector<DFac> merge_batch(Ctx& ctx, const std::vector<std::pair<DFac, DFac>>
   std::vector<Tmp> t(np);
   std::vector<GemmDesc> gsy, gx, p1, p2;
   std::vector<EigJob> ej;
+  std::vector<JacJob> jj;
   std::vector<ScaleSymJob> ss;
   std::vector<ScaleRowsJob> sr;
   int* d_rd = ctx.arena.alloc_n<int>(2 * (size_t)np);
@@ -255,14 +277,24 @@ std::vector<DFac> merge_batch(Ctx& ctx, const std::vector<std::pair<DFac, DFac>>
     m.q = m.k1 + m.k2;
     m.kk = std::min(m.q, m.s);
     if (cap > 0) m.kk = std::min(m.kk, cap);
+    m.Bn = ctx.arena.alloc_n<double>((size_t)m.s * m.kk);
+    m.sig = ctx.arena.alloc_n<double>(m.kk);
+    if (small_svd_jacobi(m.s, m.q)) {
+      // SVD of [B1 S1 | B2 S2] by one-sided Jacobi (k + l <= 32: the
+      // reference's full_svd of E / of the concatenation goes to JacobiSVD)
+      m.G = m.w = m.lam = m.Zh = nullptr;
+      m.Z = ctx.arena.alloc_n<double>((size_t)m.q * m.q);
+      m.P = ctx.arena.alloc_n<double>((size_t)m.s * m.q);
+      jj.push_back({a.B, 1, 1, a.ld, m.k1, a.sigma, b.B, b.ld, m.k2, b.sigma, m.s, nullptr, m.P,
+                    m.s, m.Z, m.q});
+      continue;
+    }
     m.G = ctx.arena.alloc_n<double>((size_t)m.q * m.q);
     m.w = ctx.arena.alloc_n<double>(m.q);
     m.lam = ctx.arena.alloc_n<double>(m.kk);
     m.Z = ctx.arena.alloc_n<double>((size_t)m.q * m.kk);
     m.Zh = ctx.arena.alloc_n<double>((size_t)m.q * m.kk);
     m.P = ctx.arena.alloc_n<double>((size_t)m.s * m.kk);
-    m.Bn = ctx.arena.alloc_n<double>((size_t)m.s * m.kk);
-    m.sig = ctx.arena.alloc_n<double>(m.kk);
     HSVD_CUDA(cudaMemcpyAsync(m.w, a.sigma, m.k1 * sizeof(double), cudaMemcpyDeviceToDevice,
                               ctx.stream));
     HSVD_CUDA(cudaMemcpyAsync(m.w + m.k1, b.sigma, m.k2 * sizeof(double),
@@ -291,6 +323,8 @@ std::vector<DFac> merge_batch(Ctx& ctx, const std::vector<std::pair<DFac, DFac>>
   scale_rows(ctx, sr);
   gemm_grouped(ctx, DType::F64, DType::F64, false, false, false, p1);
   gemm_grouped(ctx, DType::F64, DType::F64, false, false, false, p2);
+  ctx.phase = "merge.jacobi";
+  jacobi_svd_batch(ctx, jj);
   ctx.phase = "merge.fin";
   std::vector<FinJob> fj;
   for (int i = 0; i < np; ++i) {
@@ -356,6 +390,7 @@ std::vector<DFac> vrecover_batch(Ctx& ctx, const XView& x, const std::vector<Sli
   const int n = static_cast<int>(x.n);
   std::vector<GemmDesc> g1, g2, g3;
   std::vector<EigJob> ej;
+  std::vector<JacJob> jj;
   int* d_rd = ctx.arena.alloc_n<int>(2 * (size_t)ns);
   for (int j = 0; j < ns; ++j) {
     Tmp& m = t[j];
@@ -364,15 +399,23 @@ std::vector<DFac> vrecover_batch(Ctx& ctx, const XView& x, const std::vector<Sli
     m.kk = std::min(m.r, n);
     if (cap > 0) m.kk = std::min(m.kk, cap);
     m.Bt = ctx.arena.alloc_n<double>((size_t)n * m.r);
-    m.H = ctx.arena.alloc_n<double>((size_t)m.r * m.r);
-    m.lam = ctx.arena.alloc_n<double>(m.kk);
-    m.Z = ctx.arena.alloc_n<double>((size_t)m.r * m.kk);
-    m.V = ctx.arena.alloc_n<double>((size_t)n * m.kk);
     m.Vn = ctx.arena.alloc_n<double>((size_t)n * m.kk);
     m.sig = ctx.arena.alloc_n<double>(m.kk);
     const void* base = xptr(x, rows[j].start, 0);
     // B^T = X_j^T U_j (n x r): Xt (n x d_j) * U_j
     g1.push_back({base, u.B, m.Bt, x.ld, u.ld, n, n, m.r, (int)rows[j].count, 1.0, 0.0});
+    if (m.r <= n && small_svd_jacobi(n, m.r)) {  // kernels.cpp:28 on B (r x n, r <= 32)
+      m.H = m.lam = nullptr;
+      m.Z = ctx.arena.alloc_n<double>((size_t)m.r * m.r);
+      m.V = ctx.arena.alloc_n<double>((size_t)n * m.r);
+      jj.push_back({m.Bt, 1, 1, n, m.r, nullptr, nullptr, 0, 0, nullptr, n, nullptr, m.V, n, m.Z,
+                    m.r});
+      continue;
+    }
+    m.H = ctx.arena.alloc_n<double>((size_t)m.r * m.r);
+    m.lam = ctx.arena.alloc_n<double>(m.kk);
+    m.Z = ctx.arena.alloc_n<double>((size_t)m.r * m.kk);
+    m.V = ctx.arena.alloc_n<double>((size_t)n * m.kk);
     g2.push_back({m.Bt, m.Bt, m.H, n, n, m.r, m.r, m.r, n, 1.0, 0.0});
     ej.push_back({m.H, m.r, m.r, m.kk, m.lam, m.Z, m.r});
     g3.push_back({m.Bt, m.Z, m.V, n, m.r, n, n, m.kk, m.r, 1.0, 0.0});
@@ -385,6 +428,8 @@ std::vector<DFac> vrecover_batch(Ctx& ctx, const XView& x, const std::vector<Sli
   eig_topk(ctx, ej);
   ctx.phase = "vrec.back";
   gemm_grouped(ctx, DType::F64, DType::F64, false, false, false, g3);
+  ctx.phase = "vrec.jacobi";
+  jacobi_svd_batch(ctx, jj);
   ctx.phase = "vrec.fin";
   std::vector<FinJob> fj;
   for (int j = 0; j < ns; ++j) {
@@ -478,13 +523,21 @@ DFac recover_left_vectors(Ctx& ctx, const XView& x, const double* v_r, long long
   ctx.phase = "urec.proj";
   gemm_grouped(ctx, x.dt, DType::F64, true, false, false,
                {{x.X, v_r, Y, x.ld, ldv, m, m, r, n, 1.0, 0.0}});
-  ctx.phase = "urec.gram";
-  gemm_grouped(ctx, DType::F64, DType::F64, true, false, true, {{Y, Y, H, m, m, r, r, r, m, 1.0, 0.0}});
-  ctx.phase = "urec.eig";
-  eig_topk(ctx, {{H, r, r, kk, lam, Z, r}});
-  ctx.phase = "urec.back";
-  gemm_grouped(ctx, DType::F64, DType::F64, false, false, false,
-               {{Y, Z, Yh, m, r, m, m, kk, r, 1.0, 0.0}});
+  if (kk == r && small_svd_jacobi(m, r)) {  // kernels.cpp:28: full_svd(Y), r <= 32
+    ctx.phase = "urec.jacobi";
+    std::vector<JacJob> jj{{Y, 1, 1, m, r, nullptr, nullptr, 0, 0, nullptr, m, nullptr, Yh, m, Z,
+                            r}};
+    jacobi_svd_batch(ctx, jj);
+  } else {
+    ctx.phase = "urec.gram";
+    gemm_grouped(ctx, DType::F64, DType::F64, true, false, true,
+                 {{Y, Y, H, m, m, r, r, r, m, 1.0, 0.0}});
+    ctx.phase = "urec.eig";
+    eig_topk(ctx, {{H, r, r, kk, lam, Z, r}});
+    ctx.phase = "urec.back";
+    gemm_grouped(ctx, DType::F64, DType::F64, false, false, false,
+                 {{Y, Z, Yh, m, r, m, m, kk, r, 1.0, 0.0}});
+  }
   ctx.phase = "urec.fin";
   finalize(ctx, {{Yh, m, m, kk, 0.0, 0, U, m, sig, perm, d_rd, d_rd + 1, 1}});
   gather_cols(ctx, {{Zp, r, Z, r, r, kk, perm}});
@@ -563,14 +616,21 @@ DFac refine_factors(Ctx& ctx, const XView& x, const double* v_hat, long long ldv
     ctx.phase = "refine.proj";  // B^T = X^T U_outer (n x p): Xt is n x m, ld x.ld
     gemm_grouped(ctx, x.dt, DType::F64, false, false, false,
                  {{x.X, Uo, Bt, x.ld, L.ld, n, n, p, m, 1.0, 0.0}});
-    ctx.phase = "refine.gram";
-    gemm_grouped(ctx, DType::F64, DType::F64, true, false, true,
-                 {{Bt, Bt, H, n, n, p, p, p, n, 1.0, 0.0}});
-    ctx.phase = "refine.eig";
-    eig_topk(ctx, {{H, p, p, kk, lam, Z, p}});
-    ctx.phase = "refine.back";
-    gemm_grouped(ctx, DType::F64, DType::F64, false, false, false,
-                 {{Bt, Z, P, n, p, n, n, kk, p, 1.0, 0.0}});
+    if (kk == p && small_svd_jacobi(n, p)) {  // kernels.cpp:28: full_svd(U^T X), p <= 32
+      ctx.phase = "refine.jacobi";
+      std::vector<JacJob> jj{{Bt, 1, 1, n, p, nullptr, nullptr, 0, 0, nullptr, n, nullptr, P, n,
+                              Z, p}};
+      jacobi_svd_batch(ctx, jj);
+    } else {
+      ctx.phase = "refine.gram";
+      gemm_grouped(ctx, DType::F64, DType::F64, true, false, true,
+                   {{Bt, Bt, H, n, n, p, p, p, n, 1.0, 0.0}});
+      ctx.phase = "refine.eig";
+      eig_topk(ctx, {{H, p, p, kk, lam, Z, p}});
+      ctx.phase = "refine.back";
+      gemm_grouped(ctx, DType::F64, DType::F64, false, false, false,
+                   {{Bt, Z, P, n, p, n, n, kk, p, 1.0, 0.0}});
+    }
     ctx.phase = "refine.fin";
     finalize(ctx, {{P, n, n, kk, 0.0, 0, Vn, n, sig, perm, d_rd, d_rd + 1, 1}});
     gather_cols(ctx, {{Zp, p, Z, p, p, kk, perm}});

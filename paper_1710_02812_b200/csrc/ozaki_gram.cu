@@ -526,10 +526,9 @@ void ozaki_gram_batch(Ctx& ctx, const std::vector<GemmDesc>& descs) {
                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (cr != CUDA_SUCCESS) throw Error(kCuda, "cuTensorMapEncodeTiled failed");
-    double flops = 0.0;
-    for (int l = 0; l < nl; ++l)
-      flops += (double)descs[i0 + l].M * (descs[i0 + l].M + 1) * descs[i0 + l].K;
-    ctx.pending_flops = flops;  // algorithmic (fp64-equivalent SYRK) flops
+    // tensor-pipe work of the launch: int8 multiply-adds x 2 over every
+    // tile, product and padded K (the profiler's "flops" for this kernel)
+    ctx.pending_flops = (double)ht.size() * (kS * (kS + 1) / 2) * 2.0 * kBM * kBN * (double)kpad;
     int* part = ctx.arena.alloc_n<int>(ht.size() * (size_t)kS * kBN * kBM);
     ctx.launch_begin();
     k_oz_gram<<<(unsigned)ht.size(), kGramThreads, kGramSmem, ctx.stream>>>(

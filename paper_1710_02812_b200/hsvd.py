@@ -91,6 +91,7 @@ EXPORTED = [
     "hsvd_cu_rank_k_svd_sharded", "hsvd_cu_syevx_topk", "hsvd_cu_refine_factors",
     "hsvd_cu_factor_diff_norm", "hsvd_cu_rank_k_error", "hsvd_cu_residual_norm",
     "hsvd_cu_load_hsvd1", "hsvd_cu_syevx_topk_batch", "hsvd_cu_block_gram",
+    "hsvd_cu_qr_thin",
 ]
 
 
@@ -179,6 +180,7 @@ def load_library(path: str = LIB_PATH):
         lib.hsvd_cu_syevx_topk.argtypes = [P, P, I64, I64, P, P]
         lib.hsvd_cu_syevx_topk_batch.argtypes = [P, P, I64, I64, I64, P, P]
         lib.hsvd_cu_block_gram.argtypes = [P, P, I32, I64, I64, I64, I32, P]
+        lib.hsvd_cu_qr_thin.argtypes = [P, P, I64, I64, I64, P, P]
         _lib = lib
         return lib
 
@@ -766,6 +768,22 @@ def syevx_topk_batch(a, kk: int, ctx: Optional[Context] = None):
     _check(cx.lib.hsvd_cu_syevx_topk_batch(cx.handle, a.ctypes.data, count, n, int(kk),
                                            lam.ctypes.data, z.ctypes.data))
     return lam, np.ascontiguousarray(z.transpose(0, 2, 1))
+
+
+def qr_thin(a, ctx: Optional[Context] = None):
+    """hsvd::qr_thin (kernels.cpp:50-61): Householder thin QR on the device,
+    (q rows x p, r p x cols), p = min(rows, cols)."""
+    cx = _ctx(ctx)
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+    if a.ndim != 2 or a.shape[0] == 0 or a.shape[1] == 0:
+        raise ValueError("qr_thin: matrix is empty")
+    m, n = a.shape
+    p = min(m, n)
+    q = np.empty((m, p))
+    r = np.empty((p, n))
+    _check(cx.lib.hsvd_cu_qr_thin(cx.handle, a.ctypes.data, m, n, n, q.ctypes.data,
+                                  r.ctypes.data))
+    return q, r
 
 
 def block_gram(x, ctx: Optional[Context] = None) -> np.ndarray:
