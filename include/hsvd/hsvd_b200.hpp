@@ -6,7 +6,7 @@
 //   hierarchy.hpp:18-50   BlockPlan, MergeStats, tree_merge, svd_of_col_slices,
 //                         hierarchical_svd, recover_left_vectors
 //   merge.hpp:12-30       MergeOrientation, merge_pair_naive, merge_pair_qr
-//   kernels.hpp:12-26     DecompositionError, full_svd
+//   kernels.hpp:12-29     DecompositionError, full_svd, qr_thin
 //   svd_factor.hpp:14-49  SvdFactor, MatConfig, validate, retained_count,
 //                         truncate_factor, reconstruct
 //   refine.hpp:9-21       RefineResult, refine_factors
@@ -23,6 +23,7 @@
 #include <optional>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../hsvd_cu.h"
@@ -58,7 +59,46 @@ class DenseMatrix {
   std::vector<double> d_;
 };
 
-using Vector = std::vector<double>;
+// Eigen::VectorXd stand-in: a std::vector<double> with Eigen-style element
+// access (sigma(i), size()), so call sites like hsvd_main.cpp:100 compile.
+class Vector : public std::vector<double> {
+ public:
+  using std::vector<double>::vector;
+  Vector() = default;
+  Vector(const std::vector<double>& v) : std::vector<double>(v) {}  // NOLINT
+  double& operator()(Index i) { return (*this)[(size_t)i]; }
+  double operator()(Index i) const { return (*this)[(size_t)i]; }
+  Index size() const { return (Index)std::vector<double>::size(); }
+};
+
+// fp32 input matrix (the BASELINE configs' dtype): row-major float, the same
+// accessors as DenseMatrix.  The reference promotes to its fp64 DenseMatrix;
+// here fp32 crosses the C ABI as is (HSVD_CU_F32) and is computed on in fp64
+// grade on the device.
+class DenseMatrixF32 {
+ public:
+  DenseMatrixF32() = default;
+  DenseMatrixF32(Index rows, Index cols) : r_(rows), c_(cols), d_((size_t)(rows * cols), 0.0f) {}
+  Index rows() const { return r_; }
+  Index cols() const { return c_; }
+  float* data() { return d_.data(); }
+  const float* data() const { return d_.data(); }
+  float& operator()(Index i, Index j) { return d_[(size_t)(i * c_ + j)]; }
+  float operator()(Index i, Index j) const { return d_[(size_t)(i * c_ + j)]; }
+
+ private:
+  Index r_ = 0, c_ = 0;
+  std::vector<float> d_;
+};
+
+// A matrix already resident on the device (row-major, leading dimension ld,
+// HSVD_CU_F32 or HSVD_CU_F64), e.g. produced by a CUDA kernel of the caller;
+// it must be ready on the context's stream (see hsvd_cu.h).
+struct DeviceMatrixView {
+  const void* data = nullptr;
+  int dtype = HSVD_CU_F32;
+  Index rows = 0, cols = 0, ld = 0;
+};
 
 inline double frobenius_norm(const DenseMatrix& a) {
   double s = 0.0;
@@ -120,20 +160,23 @@ struct MergeStats {
 
 namespace detail {
 
-// One B200 context per thread (the C ABI context is not shared across threads).
-inline hsvd_cu_ctx* ctx() {
-  struct Holder {
-    hsvd_cu_ctx* c = nullptr;
-    ~Holder() {
-      if (c) hsvd_cu_ctx_destroy(c);
-    }
-  };
-  thread_local Holder h;
-  if (!h.c) {
-    int dev = 0;
-    if (hsvd_cu_ctx_create(dev, &h.c) != HSVD_CU_OK)
-      throw std::runtime_error(std::string("hsvd_b200: ") + hsvd_cu_last_error());
+// One B200 context per thread (the C ABI context is not shared across
+// threads), on the device chosen by hsvd::set_device (default 0).
+struct Holder {
+  hsvd_cu_ctx* c = nullptr;
+  int device = 0;
+  ~Holder() {
+    if (c) hsvd_cu_ctx_destroy(c);
   }
+};
+inline Holder& holder() {
+  thread_local Holder h;
+  return h;
+}
+inline hsvd_cu_ctx* ctx() {
+  Holder& h = holder();
+  if (!h.c && hsvd_cu_ctx_create(h.device, &h.c) != HSVD_CU_OK)
+    throw std::runtime_error(std::string("hsvd_b200: ") + hsvd_cu_last_error());
   return h.c;
 }
 
@@ -191,6 +234,19 @@ inline hsvd_cu_factor_in side(const SvdFactor& f, MergeOrientation o) {
 
 }  // namespace detail
 
+// Selects the CUDA device of this thread's calls (one context per thread and
+// device; the previous context is released).
+inline void set_device(int device) {
+  detail::Holder& h = detail::holder();
+  if (h.c && h.device == device) return;
+  if (h.c) {
+    hsvd_cu_ctx_destroy(h.c);
+    h.c = nullptr;
+  }
+  h.device = device;
+}
+inline int current_device() { return detail::holder().device; }
+
 inline void validate(const MatConfig& cfg) {
   if (cfg.gamma < 0.0 || !std::isfinite(cfg.gamma))
     throw std::invalid_argument("MatConfig: gamma must be finite and >= 0");
@@ -241,6 +297,16 @@ inline SvdFactor full_svd(const DenseMatrix& a) {
   hsvd_cu_result* r = nullptr;
   detail::check(hsvd_cu_full_svd(detail::ctx(), a.data(), a.rows(), a.cols(), a.cols(), &r));
   return detail::take(r);
+}
+
+// kernels.hpp:29 qr_thin -> (Q rows x p, R p x cols), Householder on the device.
+inline std::pair<DenseMatrix, DenseMatrix> qr_thin(const DenseMatrix& a) {
+  if (a.rows() == 0 || a.cols() == 0) throw std::invalid_argument("qr_thin: matrix is empty");
+  const Index p = std::min(a.rows(), a.cols());
+  std::pair<DenseMatrix, DenseMatrix> qr{DenseMatrix(a.rows(), p), DenseMatrix(p, a.cols())};
+  detail::check(hsvd_cu_qr_thin(detail::ctx(), a.data(), a.rows(), a.cols(), a.cols(),
+                                qr.first.data(), qr.second.data()));
+  return qr;
 }
 
 inline SvdFactor merge_pair_qr(const SvdFactor& f1, const SvdFactor& f2, MergeOrientation o,
@@ -304,6 +370,50 @@ inline SvdFactor recover_left_vectors(const DenseMatrix& x, const DenseMatrix& v
   detail::check(hsvd_cu_recover_left_vectors(detail::ctx(), x.data(), HSVD_CU_F64, x.rows(),
                                              x.cols(), x.cols(), HSVD_CU_HOST, v_r.data(),
                                              v_r.cols(), v_r.cols(), HSVD_CU_HOST, &r));
+  return detail::take(r);
+}
+
+namespace detail {
+inline SvdFactor hsvd_raw(const void* x, int dtype, Index m, Index n, Index ld, int where,
+                          const MatConfig& cfg) {
+  if (m == 0 || n == 0) throw std::invalid_argument("hierarchical_svd: matrix is empty");
+  validate(cfg);
+  const hsvd_cu_config c = to_c(cfg);
+  hsvd_cu_result* r = nullptr;
+  check(hsvd_cu_hierarchical_svd(ctx(), x, dtype, m, n, ld, where, &c, &r));
+  return take(r);
+}
+inline SvdFactor recover_raw(const void* x, int dtype, Index m, Index n, Index ld, int where,
+                             const DenseMatrix& v_r) {
+  if (v_r.rows() != n)
+    throw std::invalid_argument("recover_left_vectors: v_r must have x.cols() rows");
+  hsvd_cu_result* r = nullptr;
+  check(hsvd_cu_recover_left_vectors(ctx(), x, dtype, m, n, ld, where, v_r.data(), v_r.cols(),
+                                     v_r.cols(), HSVD_CU_HOST, &r));
+  return take(r);
+}
+}  // namespace detail
+
+// fp32 and device-resident overloads of the drop-in (same contracts).
+inline SvdFactor hierarchical_svd(const DenseMatrixF32& x, const MatConfig& cfg) {
+  return detail::hsvd_raw(x.data(), HSVD_CU_F32, x.rows(), x.cols(), x.cols(), HSVD_CU_HOST, cfg);
+}
+inline SvdFactor hierarchical_svd(const DeviceMatrixView& x, const MatConfig& cfg) {
+  return detail::hsvd_raw(x.data, x.dtype, x.rows, x.cols, x.ld, HSVD_CU_DEVICE, cfg);
+}
+inline SvdFactor recover_left_vectors(const DenseMatrixF32& x, const DenseMatrix& v_r) {
+  return detail::recover_raw(x.data(), HSVD_CU_F32, x.rows(), x.cols(), x.cols(), HSVD_CU_HOST,
+                             v_r);
+}
+inline SvdFactor recover_left_vectors(const DeviceMatrixView& x, const DenseMatrix& v_r) {
+  return detail::recover_raw(x.data, x.dtype, x.rows, x.cols, x.ld, HSVD_CU_DEVICE, v_r);
+}
+inline SvdFactor svd_of_col_slices(const DenseMatrixF32& x_slice, Index c, double gamma,
+                                   std::optional<Index> max_rank = std::nullopt) {
+  hsvd_cu_result* r = nullptr;
+  detail::check(hsvd_cu_svd_of_col_slices(detail::ctx(), x_slice.data(), HSVD_CU_F32,
+                                          x_slice.rows(), x_slice.cols(), x_slice.cols(),
+                                          HSVD_CU_HOST, c, gamma, max_rank ? *max_rank : 0, &r));
   return detail::take(r);
 }
 

@@ -170,6 +170,12 @@ int hsvd_cu_residual_norm(hsvd_cu_ctx* ctx, const void* x, int dtype, int64_t m,
  * Inf (the finiteness check runs on the device). */
 int hsvd_cu_load_hsvd1(hsvd_cu_ctx* ctx, const char* path, int64_t* rows, int64_t* cols,
                        const double** dev_x);
+/* The same loader also accepting the fp32 payload variant:
+ * magic "HSVF1\0", same header, 4-byte little-endian floats (half the file
+ * and device bytes of the fp64 form; config 5 is 17 GB instead of 34 GB).
+ * *dtype receives HSVD_CU_F32 or HSVD_CU_F64; pass it on with dev_x. */
+int hsvd_cu_load_matrix(hsvd_cu_ctx* ctx, const char* path, int64_t* rows, int64_t* cols,
+                        int* dtype, const void** dev_x);
 
 /* hierarchical_svd + recover_left_vectors with V_r kept on the device. */
 int hsvd_cu_rank_k_svd(hsvd_cu_ctx* ctx, const void* x, int dtype, int64_t m, int64_t n,

@@ -12,6 +12,6 @@ from .hsvd import (  # noqa: F401
     rank_k_svd, rank_k_svd_device, reconstruct, recover_left_vectors, retained_count, svd_of_col_slices,
     tree_merge, truncate_factor, validate, LIB_PATH, EXPORTED, ThreadGroup, nccl_unique_id,
     shard_rows, rank_k_svd_sharded, syevx_topk, syevx_topk_batch, block_gram, qr_thin, refine_factors, RefineResult,
-    factor_diff_norm, rank_k_error, residual_norm, load_hsvd1, save_hsvd1, DeviceMatrix,
+    factor_diff_norm, rank_k_error, residual_norm, load_hsvd1, load_matrix, save_hsvd1, DeviceMatrix,
     IoError, FormatError,
 )

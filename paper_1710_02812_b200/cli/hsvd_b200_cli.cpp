@@ -120,15 +120,16 @@ int run_svd(int argc, char** argv) {
     ~CtxGuard() { hsvd_cu_ctx_destroy(c); }
   } cg{ctx};
   int64_t m = 0, n = 0;
-  const double* dx = nullptr;
-  check(hsvd_cu_load_hsvd1(ctx, input.c_str(), &m, &n, &dx));
+  int dt = HSVD_CU_F64;
+  const void* dx = nullptr;  // HSVD1 (fp64) or its fp32 variant HSVF1
+  check(hsvd_cu_load_matrix(ctx, input.c_str(), &m, &n, &dt, &dx));
   const hsvd_cu_config cfg = {gamma, d, c, eps, iters, max_rank};
   check(hsvd_cu_validate(&cfg));
 
   hsvd_cu_result* res = nullptr;
   if (refine) {  // hierarchical_svd, then refine_factors from (V, sigma)
     hsvd_cu_result* right = nullptr;
-    check(hsvd_cu_hierarchical_svd(ctx, dx, HSVD_CU_F64, m, n, n, HSVD_CU_DEVICE, &cfg, &right));
+    check(hsvd_cu_hierarchical_svd(ctx, dx, dt, m, n, n, HSVD_CU_DEVICE, &cfg, &right));
     int64_t r = 0, ur = 0, vr = 0;
     int32_t hu = 0, hv = 0, deg = 0;
     check(hsvd_cu_result_info(right, &r, &hu, &hv, &ur, &vr, &deg));
@@ -138,12 +139,12 @@ int run_svd(int argc, char** argv) {
     hsvd_cu_result_free(right);
     int32_t it = 0, conv = 0;
     double err = 0.0;
-    check(hsvd_cu_refine_factors(ctx, dx, HSVD_CU_F64, m, n, n, HSVD_CU_DEVICE, v.data(), n, r, r,
+    check(hsvd_cu_refine_factors(ctx, dx, dt, m, n, n, HSVD_CU_DEVICE, v.data(), n, r, r,
                                  HSVD_CU_HOST, s.data(), r, eps, iters, &it, &err, &conv, &res));
     std::printf("refined in %d iteration(s), final error %s%s\n", it, num(err, precise).c_str(),
                 conv ? "" : " (not converged)");
   } else {
-    check(hsvd_cu_rank_k_svd(ctx, dx, HSVD_CU_F64, m, n, n, HSVD_CU_DEVICE, &cfg, &res));
+    check(hsvd_cu_rank_k_svd(ctx, dx, dt, m, n, n, HSVD_CU_DEVICE, &cfg, &res));
   }
   int64_t k = 0, ur = 0, vr = 0;
   int32_t hu = 0, hv = 0, deg = 0;

@@ -730,9 +730,11 @@ int hsvd_cu_residual_norm(hsvd_cu_ctx* ctx, const void* x, int dtype, int64_t m,
 }
 
 // ---- HSVD1 loader (matrix_io.cpp:91-113), streamed to the device ---------
+extern "C++" {
 namespace {
 
-__global__ void k_all_finite(const double* __restrict__ x, long long count, int* __restrict__ bad) {
+template <typename T>
+__global__ void k_all_finite(const T* __restrict__ x, long long count, int* __restrict__ bad) {
   int b = 0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
        i += (long long)gridDim.x * blockDim.x)
@@ -740,10 +742,10 @@ __global__ void k_all_finite(const double* __restrict__ x, long long count, int*
   if (__syncthreads_or(b) && threadIdx.x == 0) atomicOr(bad, 1);
 }
 
-}  // namespace
-
-int hsvd_cu_load_hsvd1(hsvd_cu_ctx* ctx, const char* path, int64_t* rows, int64_t* cols,
-                       const double** dev_x) {
+// HSVD1 (fp64 payload, matrix_io.cpp:91-113) and, when allow_f32, its fp32
+// payload variant "HSVF1\0" (same 22-byte header layout, 4-byte elements).
+int load_matrix(hsvd_cu_ctx* ctx, const char* path, bool allow_f32, int64_t* rows, int64_t* cols,
+                int* dtype, const void** dev_x) {
   return guarded([&] {
     if (!ctx || !path || !rows || !cols || !dev_x) throw Error(kInvalid, "null argument");
     const std::string p(path);
@@ -754,8 +756,15 @@ int hsvd_cu_load_hsvd1(hsvd_cu_ctx* ctx, const char* path, int64_t* rows, int64_
     if (std::fread(header, 1, sizeof(header), f) != sizeof(header))
       throw Error(kFormat, p + ": truncated header");
     static const char kMagic[6] = {'H', 'S', 'V', 'D', '1', '\0'};
-    if (std::memcmp(header, kMagic, sizeof(kMagic)) != 0)
-      throw Error(kFormat, p + ": bad magic, not an HSVD1 file");
+    static const char kMagicF32[6] = {'H', 'S', 'V', 'F', '1', '\0'};
+    bool f32 = false;
+    if (std::memcmp(header, kMagic, sizeof(kMagic)) != 0) {
+      if (allow_f32 && std::memcmp(header, kMagicF32, sizeof(kMagicF32)) == 0)
+        f32 = true;
+      else
+        throw Error(kFormat, p + ": bad magic, not an HSVD1 file");
+    }
+    const size_t esize = f32 ? sizeof(float) : sizeof(double);
     auto u64 = [&](int off) {
       std::uint64_t v = 0;
       for (int i = 0; i < 8; ++i) v |= static_cast<std::uint64_t>(header[off + i]) << (8 * i);
@@ -768,7 +777,7 @@ int hsvd_cu_load_hsvd1(hsvd_cu_ctx* ctx, const char* path, int64_t* rows, int64_
       throw Error(kFormat, p + ": implausible dimensions");
     Ctx& cx = ctx->c;
     HSVD_CUDA(cudaSetDevice(cx.device));
-    const size_t count = (size_t)(r * c), bytes = count * sizeof(double);
+    const size_t count = (size_t)(r * c), bytes = count * esize;
     if (ctx->loaded_cap < bytes) {
       if (ctx->loaded) HSVD_CUDA(cudaFree(ctx->loaded));
       ctx->loaded = nullptr;
@@ -809,7 +818,12 @@ int hsvd_cu_load_hsvd1(hsvd_cu_ctx* ctx, const char* path, int64_t* rows, int64_
       int* bad = nullptr;
       HSVD_CUDA(cudaMalloc(&bad, sizeof(int)));
       HSVD_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), cx.stream));
-      k_all_finite<<<4 * cx.num_sms, 256, 0, cx.stream>>>(ctx->loaded, (long long)count, bad);
+      if (f32)
+        k_all_finite<float><<<4 * cx.num_sms, 256, 0, cx.stream>>>(
+            reinterpret_cast<const float*>(ctx->loaded), (long long)count, bad);
+      else
+        k_all_finite<double><<<4 * cx.num_sms, 256, 0, cx.stream>>>(ctx->loaded, (long long)count,
+                                                                    bad);
       int hb = 0;
       HSVD_CUDA(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, cx.stream));
       HSVD_CUDA(cudaStreamSynchronize(cx.stream));
@@ -823,9 +837,27 @@ int hsvd_cu_load_hsvd1(hsvd_cu_ctx* ctx, const char* path, int64_t* rows, int64_
     cleanup();
     *rows = (int64_t)r;
     *cols = (int64_t)c;
+    if (dtype) *dtype = f32 ? HSVD_CU_F32 : HSVD_CU_F64;
     *dev_x = ctx->loaded;
     return HSVD_CU_OK;
   });
+}
+
+}  // namespace
+}  // extern "C++"
+
+int hsvd_cu_load_hsvd1(hsvd_cu_ctx* ctx, const char* path, int64_t* rows, int64_t* cols,
+                       const double** dev_x) {
+  const void* p = nullptr;
+  const int rc = load_matrix(ctx, path, false, rows, cols, nullptr, &p);
+  if (rc == HSVD_CU_OK) *dev_x = static_cast<const double*>(p);
+  return rc;
+}
+
+int hsvd_cu_load_matrix(hsvd_cu_ctx* ctx, const char* path, int64_t* rows, int64_t* cols,
+                        int* dtype, const void** dev_x) {
+  if (!dtype) return fail(HSVD_CU_EINVAL, "null argument");
+  return load_matrix(ctx, path, true, rows, cols, dtype, dev_x);
 }
 
 int hsvd_cu_rank_k_svd(hsvd_cu_ctx* ctx, const void* x, int dtype, int64_t m, int64_t n,

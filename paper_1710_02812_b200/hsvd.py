@@ -91,7 +91,7 @@ EXPORTED = [
     "hsvd_cu_rank_k_svd_sharded", "hsvd_cu_syevx_topk", "hsvd_cu_refine_factors",
     "hsvd_cu_factor_diff_norm", "hsvd_cu_rank_k_error", "hsvd_cu_residual_norm",
     "hsvd_cu_load_hsvd1", "hsvd_cu_syevx_topk_batch", "hsvd_cu_block_gram",
-    "hsvd_cu_qr_thin",
+    "hsvd_cu_qr_thin", "hsvd_cu_load_matrix",
 ]
 
 
@@ -147,6 +147,8 @@ def load_library(path: str = LIB_PATH):
         lib.hsvd_cu_rank_k_svd.argtypes = xargs + [C.POINTER(_Config), pp]
         lib.hsvd_cu_recover_left_vectors.argtypes = xargs + [P, I64, I64, I32, pp]
         lib.hsvd_cu_load_hsvd1.argtypes = [P, C.c_char_p, C.POINTER(I64), C.POINTER(I64), pp]
+        lib.hsvd_cu_load_matrix.argtypes = [P, C.c_char_p, C.POINTER(I64), C.POINTER(I64),
+                                            C.POINTER(C.c_int), pp]
         uv = C.POINTER(_FactorUV)
         lib.hsvd_cu_factor_diff_norm.argtypes = [P, uv, uv, C.POINTER(D)]
         lib.hsvd_cu_rank_k_error.argtypes = [P, uv, uv, I64, C.POINTER(D)]
@@ -503,7 +505,7 @@ def _matrix_arg(x, ctx: Optional["Context"] = None):
     current stream on the context's stream (ctx defaults to the default
     context)."""
     if isinstance(x, DeviceMatrix):
-        return (x.ptr, F64, x.shape[0], x.shape[1], x.shape[1], DEVICE, x)
+        return (x.ptr, x.dtype, x.shape[0], x.shape[1], x.shape[1], DEVICE, x)
     mod = type(x).__module__
     if mod.startswith("torch"):
         if x.dim() != 2:
@@ -639,8 +641,9 @@ class DeviceMatrix:
     """A matrix resident in device memory owned by a context (the last
     load_hsvd1); accepted wherever a matrix is (passed as HSVD_CU_DEVICE)."""
 
-    def __init__(self, ctx: "Context", ptr: int, rows: int, cols: int):
+    def __init__(self, ctx: "Context", ptr: int, rows: int, cols: int, dtype: int = None):
         self.ctx, self.ptr, self.shape = ctx, ptr, (rows, cols)
+        self.dtype = F64 if dtype is None else dtype
 
 
 def load_hsvd1(path: str, ctx: Optional[Context] = None) -> DeviceMatrix:
@@ -654,15 +657,28 @@ def load_hsvd1(path: str, ctx: Optional[Context] = None) -> DeviceMatrix:
     return DeviceMatrix(c, ptr.value, int(r.value), int(k.value))
 
 
-def save_hsvd1(x, path: str) -> None:
-    """matrix_io.cpp:115-127 save_hsvd1 (host writer, for tests and the CLI)."""
-    a = np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+def load_matrix(path: str, ctx: Optional[Context] = None) -> DeviceMatrix:
+    """load_hsvd1 also accepting the fp32 payload variant ("HSVF1\0" magic,
+    same header; SURVEY 8(f) #3): the matrix stays fp32 on the device."""
+    c = _ctx(ctx)
+    r, k, dt = C.c_int64(), C.c_int64(), C.c_int(0)
+    ptr = C.c_void_p()
+    _check(c.lib.hsvd_cu_load_matrix(c.handle, os.fsencode(path), C.byref(r), C.byref(k),
+                                     C.byref(dt), C.byref(ptr)))
+    return DeviceMatrix(c, ptr.value, int(r.value), int(k.value), int(dt.value))
+
+
+def save_hsvd1(x, path: str, dtype: str = "f64") -> None:
+    """matrix_io.cpp:115-127 save_hsvd1 (host writer, for tests and the CLI);
+    dtype="f32" writes the fp32 payload variant (magic "HSVF1\0")."""
+    f32 = dtype == "f32"
+    a = np.ascontiguousarray(np.asarray(x, dtype=np.float32 if f32 else np.float64))
     if a.ndim == 1:
         a = a.reshape(-1, 1)
     with open(path, "wb") as f:
-        f.write(b"HSVD1\0" + int(a.shape[0]).to_bytes(8, "little") +
+        f.write((b"HSVF1\0" if f32 else b"HSVD1\0") + int(a.shape[0]).to_bytes(8, "little") +
                 int(a.shape[1]).to_bytes(8, "little"))
-        f.write(a.tobytes())
+        f.write(a.astype("<f4" if f32 else "<f8").tobytes())
 
 
 # ---- device evaluation of reconstruction errors (SURVEY 8(f) next #2) -----

@@ -100,6 +100,45 @@ int main() {
   const BlockPlan plan = BlockPlan::make(10, 7, 4, 3);
   CHECK(plan.row_slices.size() == 3 && plan.col_slices[2].count == 1);
 
+  // Eigen-style sigma(i) access (hsvd_main.cpp:100 prints sigma(i))
+  CHECK(std::abs(full.sigma(0) - 5.0) < 1e-10 && full.sigma.size() == r);
+
+  // fp32 overloads (the BASELINE dtype) agree with the fp64 path
+  DenseMatrixF32 xf(m, n);
+  for (Index i = 0; i < m; ++i)
+    for (Index j = 0; j < n; ++j) xf(i, j) = (float)x(i, j);
+  const SvdFactor rf = hierarchical_svd(xf, cfg);
+  const SvdFactor ff = recover_left_vectors(xf, *rf.v);
+  CHECK(ff.rank() == r);
+  for (Index t = 0; t < r; ++t) CHECK(std::abs(ff.sigma(t) - (5.0 - t)) < 1e-5);
+
+  // kernels.hpp:29 qr_thin: Q R = A, Q orthonormal, R upper triangular
+  DenseMatrix a(7, 4);
+  for (Index i = 0; i < 7; ++i)
+    for (Index j = 0; j < 4; ++j) a(i, j) = std::sin(1.0 + i * 0.7 + j * 1.3);
+  const auto qr = qr_thin(a);
+  double qerr = 0.0, oerr = 0.0;
+  for (Index i = 0; i < 7; ++i)
+    for (Index j = 0; j < 4; ++j) {
+      double s = 0.0;
+      for (Index t = 0; t < 4; ++t) s += qr.first(i, t) * qr.second(t, j);
+      qerr = std::max(qerr, std::abs(s - a(i, j)));
+    }
+  for (Index i = 0; i < 4; ++i)
+    for (Index j = 0; j < 4; ++j) {
+      double s = 0.0;
+      for (Index t = 0; t < 7; ++t) s += qr.first(t, i) * qr.first(t, j);
+      oerr = std::max(oerr, std::abs(s - (i == j ? 1.0 : 0.0)));
+      if (i > j) CHECK(qr.second(i, j) == 0.0);
+    }
+  CHECK(qerr < 1e-13 && oerr < 1e-13);
+  CHECK(throws<std::invalid_argument>([] { qr_thin(DenseMatrix()); }));
+
+  // device selection (one context per thread and device)
+  set_device(0);
+  CHECK(current_device() == 0);
+  CHECK(hierarchical_svd(x, cfg).rank() == r);
+
   std::printf("cpp api: %d failure(s)\n", failures);
   return failures;
 }

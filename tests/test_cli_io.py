@@ -100,3 +100,39 @@ def test_cli_svd_matches_reference_cli(tmp_path, golden):
     assert rc == 0 and out.splitlines()[0] == "rank 2", err
     rc, _, err = _run("svd", "--input", str(tmp_path / "none.hsvd"))
     assert rc == 2 and "cannot open for reading" in err
+
+
+@pytest.mark.gpu
+def test_fp32_payload_variant(tmp_path):
+    """HSVF1: the fp32 payload variant (half the bytes of HSVD1) loads to an
+    fp32 device matrix and decomposes to the same factors as the fp32 host
+    input; the fp64-only load_hsvd1 keeps the reference's behaviour (bad
+    magic); the CLI reads either form."""
+    import paper_1710_02812_b200 as H
+    rng = np.random.default_rng(32)
+    x = rng.standard_normal((400, 96)).astype(np.float32)
+    p = str(tmp_path / "x32.hsvd")
+    H.save_hsvd1(x, p, dtype="f32")
+    assert os.path.getsize(p) == 22 + 4 * x.size
+    dm = H.load_matrix(p)
+    assert dm.shape == (400, 96) and dm.dtype == H.hsvd.F32
+    cfg = H.MatConfig(gamma=0.0, row_block_rows=100, col_block_cols=48, max_rank=20)
+    a = H.rank_k_svd(dm, cfg)
+    b = H.rank_k_svd(x, cfg)
+    assert np.array_equal(a.sigma, b.sigma)
+    with pytest.raises(H.FormatError, match="bad magic"):
+        H.load_hsvd1(p)
+    d64 = str(tmp_path / "x64.hsvd")
+    H.save_hsvd1(x.astype(np.float64), d64)
+    assert H.load_matrix(d64).dtype == H.hsvd.F64
+    bad = x.copy()
+    bad[5, 5] = np.inf
+    H.save_hsvd1(bad, str(tmp_path / "inf32.hsvd"), dtype="f32")
+    with pytest.raises(H.FormatError, match="NaN or Inf"):
+        H.load_matrix(str(tmp_path / "inf32.hsvd"))
+    rc, out, err = _run("svd", "--input", p, "--gamma", "0", "--row-block", "100",
+                        "--col-block", "48", "--max-rank", "20", "--precise")
+    assert rc == 0, err
+    sig = [float(t) for t in out.splitlines()[1].split()[1:]]
+    assert out.splitlines()[0] == "rank 20"
+    assert np.allclose(sig, a.sigma[:len(sig)], rtol=1e-12, atol=0)
