@@ -950,13 +950,17 @@ void launch_latrd(Ctx& ctx, int R, int count, int cs, size_t smem, const EigDev*
 // Reduction choice.  The two-stage path moves the O(n^3) work onto DMMA
 // GEMMs but its band stages (panel QR, bulge chase, band inverse iteration)
 // run one CTA (or a few) per matrix, so it pays off for large n or for
-// batches that fill the GPU (measured on B200: single matrix, one-stage
-// wins at n = 1024 and 2048, two-stage at 4096; 64 matrices of n = 2048,
-// 2500 or 4096, two-stage wins).  HSVD_TWO_STAGE_MIN_N overrides with a
-// plain size threshold.
+// batches that fill the GPU.  Measured on B200 (round 2, after the chase and
+// Q2 improvements of round 1; profiles/r02_eig_batch*.json, top-kk device
+// time): two-stage wins at n >= 2048 for every batch size -- 1 x 2048: 65 vs
+// 77 ms, 8 x 2048: 67 vs 106, 8 x 2500: 91 vs 216, 2 x 4096: 184 vs 1151 --
+// so the per-rank leaf batches of a multi-GPU run (8 leaves per rank at 8
+// GPUs for configs 2-4) keep the two-stage path; one-stage still wins at
+// n = 1024 and 1536 for small batches (17 vs 28 ms, 41 vs 45 ms).
+// HSVD_TWO_STAGE_MIN_N overrides with a plain size threshold.
 constexpr int kTwoStageMinN = 1024;       // batched
 constexpr int kTwoStageMinBatch = 32;
-constexpr int kTwoStageAlwaysN = 3072;    // any batch size
+constexpr int kTwoStageAlwaysN = 2048;    // any batch size
 bool use_two_stage(int nmax, int count) {
   if (const char* env = std::getenv("HSVD_TWO_STAGE_MIN_N")) return nmax >= std::atoi(env);
   return nmax >= kTwoStageAlwaysN || (nmax >= kTwoStageMinN && count >= kTwoStageMinBatch);

@@ -105,3 +105,30 @@ def test_failing_rank_releases_peers():
     assert not any(t.is_alive() for t in th), "a rank is still blocked"
     assert errs[1] is not None and "must hold rows" in errs[1]
     assert errs[0] is not None and "peer rank failed" in errs[0]
+
+
+def test_world8_cfg2_like_equals_single():
+    """Eight ranks at a config-2-like shape (8x8 grid, k = 100, fp32, the
+    noise-bulk spectrum of config 2): every rank owns one row slice, the row
+    tree crosses ranks at all three levels (pairs (0,1),(2,3).. then
+    (01,23).. then (0123,4567): SPEC.md:271), V_r is broadcast and the U
+    Gram all-reduced.  Equal to the single-context result."""
+    import paper_1710_02812_b200 as H
+    rng = np.random.default_rng(2)
+    m = n = 10000
+    r = 100
+    u = np.linalg.qr(rng.standard_normal((m, r)))[0]
+    v = np.linalg.qr(rng.standard_normal((n, r)))[0]
+    x = ((u * np.arange(1, r + 1) ** -1.5) @ v.T + 1e-3 * rng.standard_normal((m, n))).astype(
+        np.float32)
+    cfg = H.MatConfig(gamma=1e-12, row_block_rows=m // 8, col_block_cols=n // 8, max_rank=100)
+    single = H.rank_k_svd(x, cfg)
+    res = _run_group(H, x, cfg, 8)
+    assert [r[1] for r in res] == [m // 8] * 8
+    u_all = np.vstack([r[2].u for r in res])
+    for _, _, f in res:
+        assert f.rank() == single.rank() == 100
+        assert np.abs(f.sigma - single.sigma).max() <= 1e-11 * single.sigma[0]
+        assert O.largest_principal_angle(single.v, f.v) < 1e-8
+    assert O.largest_principal_angle(single.u, u_all) < 1e-8
+    assert O.orthonormality_defect(u_all) < 1e-8
