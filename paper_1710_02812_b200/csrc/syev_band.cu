@@ -936,10 +936,16 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
   if (const char* env = std::getenv("HSVD_BAND_INVIT")) band_invit = std::atoi(env) != 0;
   if (const char* env = std::getenv("HSVD_BAND_GROUP")) kBandGroup = std::max(1, std::atoi(env));
   size_t lu_slot_max = 0;
+  // all bands contiguous: one L2 persisting window covers them in the chase
+  size_t band_total = 0;
+  for (int g = 0; g < count; ++g) band_total += ((size_t)LDBB * dev[g].n * sizeof(double) + 255) & ~size_t(255);
+  char* band_base = static_cast<char*>(ctx.arena.alloc(band_total));
+  size_t band_off = 0;
   for (int g = 0; g < count; ++g) {
     EigDev& d = dev[g];
     const int n = d.n;
-    d.band = ctx.arena.alloc_n<double>((size_t)LDBB * n);
+    d.band = reinterpret_cast<double*>(band_base + band_off);
+    band_off += ((size_t)LDBB * n * sizeof(double) + 255) & ~size_t(255);
     d.band0 = band_invit ? ctx.arena.alloc_n<double>((size_t)LDBB * n) : nullptr;
     d.Tp = ctx.arena.alloc_n<double>((size_t)ceil_div(n, B2) * B2 * B2);
     d.psum = ctx.arena.alloc_n<double>((size_t)8 * B2 * B2);
@@ -1064,6 +1070,9 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
   int ccs = 1;
   while (ccs < 2 && count * ccs * 2 <= ctx.num_sms) ccs *= 2;  // 4 measured slower
   if (const char* env = std::getenv("HSVD_CHASE_CS")) ccs = std::max(1, std::atoi(env));
+  // (An L2 persisting access-policy window over the contiguous bands was
+  // measured in round 2: no change at config 2, 388 -> 675 ms at config 5,
+  // where the 545 MB of bands exceed the persisting carve-out; not used.)
   if (ccs == 1) {
     k_chase<false><<<count, CHASE_WARPS * 32, 0, ctx.stream>>>(dd, 1);
   } else {
