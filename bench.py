@@ -538,6 +538,7 @@ def run_ours(args, w):
         "tflops_tc": w.flops_tc() / (ms / 1000.0) / 1e12,
         "kernels": [{"name": k, "launches": n, "ms": round(t, 4), "share": round(s, 4)}
                     for k, n, t, s in shares[:12]],
+        "kernels_all": [[k, n, round(t, 4)] for k, n, t, s in shares],
     }
     print(json.dumps(line), flush=True)
     return 0

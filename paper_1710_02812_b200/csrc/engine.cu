@@ -93,6 +93,18 @@ void leaf_gram_tall(Ctx& ctx, DType dt, const std::vector<GemmDesc>& descs) {
   gemm_grouped(ctx, dt, dt, false, true, true, dm);
 }
 
+// Projections of the fp32 input onto fp64 factors (leaf P = X_b Z, V-recovery
+// X_j^T U_j, U-recovery X V_r, refinement X^T U): on the tcgen05 int8 tensor
+// cores through the Ozaki planes (fp64-grade; ozaki_gram.cu) when they fit
+// (N <= 256, K <= 65536), else -- and for fp64 inputs, or HSVD_PROJ=dmma --
+// the DMMA GEMM.
+void project_x(Ctx& ctx, DType xt, bool trans_a, const std::vector<GemmDesc>& descs) {
+  std::vector<GemmDesc> oz, dm;
+  for (const GemmDesc& d : descs) (ozaki_gemm_applicable(xt, trans_a, d) ? oz : dm).push_back(d);
+  ozaki_gemm_batch(ctx, trans_a, oz);
+  gemm_grouped(ctx, xt, DType::F64, trans_a, false, false, dm);
+}
+
 // ---------------------------------------------------------------------------
 // block SVD (leaves): Gram of the smaller side + top-k eigenpairs + projection
 // ---------------------------------------------------------------------------
@@ -189,8 +201,8 @@ std::vector<DFac> block_svd_batch(Ctx& ctx, const XView& x, const std::vector<Bl
   ctx.phase = "leaf.eig";
   eig_topk(ctx, ej);
   ctx.phase = "leaf.proj";
-  gemm_grouped(ctx, x.dt, DType::F64, true, false, false, proj_t);
-  gemm_grouped(ctx, x.dt, DType::F64, false, false, false, proj_w);
+  project_x(ctx, x.dt, true, proj_t);
+  project_x(ctx, x.dt, false, proj_w);
   ctx.phase = "leaf.jacobi";
   jacobi_svd_batch(ctx, jj);
   ctx.phase = "leaf.fin";
@@ -421,7 +433,7 @@ std::vector<DFac> vrecover_batch(Ctx& ctx, const XView& x, const std::vector<Sli
     g3.push_back({m.Bt, m.Z, m.V, n, m.r, n, n, m.kk, m.r, 1.0, 0.0});
   }
   ctx.phase = "vrec.proj";
-  gemm_grouped(ctx, x.dt, DType::F64, false, false, false, g1);
+  project_x(ctx, x.dt, false, g1);
   ctx.phase = "vrec.gram";
   gemm_grouped(ctx, DType::F64, DType::F64, true, false, true, g2);
   ctx.phase = "vrec.eig";
@@ -521,8 +533,7 @@ DFac recover_left_vectors(Ctx& ctx, const XView& x, const double* v_r, long long
   int* d_rd = ctx.arena.alloc_n<int>(2);
   // Y = X V_r : Xt (n x m) transposed
   ctx.phase = "urec.proj";
-  gemm_grouped(ctx, x.dt, DType::F64, true, false, false,
-               {{x.X, v_r, Y, x.ld, ldv, m, m, r, n, 1.0, 0.0}});
+  project_x(ctx, x.dt, true, {{x.X, v_r, Y, x.ld, ldv, m, m, r, n, 1.0, 0.0}});
   if (kk == r && small_svd_jacobi(m, r)) {  // kernels.cpp:28: full_svd(Y), r <= 32
     ctx.phase = "urec.jacobi";
     std::vector<JacJob> jj{{Y, 1, 1, m, r, nullptr, nullptr, 0, 0, nullptr, m, nullptr, Yh, m, Z,
@@ -614,8 +625,7 @@ DFac refine_factors(Ctx& ctx, const XView& x, const double* v_hat, long long ldv
     double* Zp = ctx.arena.alloc_n<double>((size_t)p * kk);
     int* d_rd = ctx.arena.alloc_n<int>(2);
     ctx.phase = "refine.proj";  // B^T = X^T U_outer (n x p): Xt is n x m, ld x.ld
-    gemm_grouped(ctx, x.dt, DType::F64, false, false, false,
-                 {{x.X, Uo, Bt, x.ld, L.ld, n, n, p, m, 1.0, 0.0}});
+    project_x(ctx, x.dt, false, {{x.X, Uo, Bt, x.ld, L.ld, n, n, p, m, 1.0, 0.0}});
     if (kk == p && small_svd_jacobi(n, p)) {  // kernels.cpp:28: full_svd(U^T X), p <= 32
       ctx.phase = "refine.jacobi";
       std::vector<JacJob> jj{{Bt, 1, 1, n, p, nullptr, nullptr, 0, 0, nullptr, n, nullptr, P, n,

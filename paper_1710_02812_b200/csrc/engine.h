@@ -80,6 +80,10 @@ struct HsvdConfig {
 // tcgen05 int8 Ozaki path, fp64 on the DMMA SYRK (engine.cu).
 void leaf_gram_tall(Ctx& ctx, DType dt, const std::vector<GemmDesc>& descs);
 
+// op(A) B projections of the fp32/fp64 input onto fp64 factors (tcgen05
+// Ozaki GEMM when applicable, else DMMA): engine.cu.
+void project_x(Ctx& ctx, DType xt, bool trans_a, const std::vector<GemmDesc>& descs);
+
 // Exact thin SVD of each block, truncated (hierarchy.cpp:57: truncate_factor
 // (full_svd(block))).  keep_both: also return the other side in B2.
 std::vector<DFac> block_svd_batch(Ctx& ctx, const XView& x, const std::vector<Block>& blocks,

@@ -205,7 +205,7 @@ DFac rank_k_svd_sharded(Ctx& ctx, Comm& comm, const XView& xl, long long m_total
   int* d_rd = ctx.arena.alloc_n<int>(2);
   ctx.phase = "urec.proj";
   if (ml > 0) {
-    gemm_grouped(ctx, xl.dt, DType::F64, true, false, false, {{xl.X, vr, Y, xl.ld, n, ml, ml, r, n, 1.0, 0.0}});
+    project_x(ctx, xl.dt, true, {{xl.X, vr, Y, xl.ld, n, ml, ml, r, n, 1.0, 0.0}});
     ctx.phase = "urec.gram";
     gemm_grouped(ctx, DType::F64, DType::F64, true, false, true, {{Y, Y, H, ml, ml, r, r, r, ml, 1.0, 0.0}});
   } else {

@@ -18,4 +18,13 @@ bool ozaki_gram_applicable(DType dt, const GemmDesc& d);
 // c, K = d).
 void ozaki_gram_batch(Ctx& ctx, const std::vector<GemmDesc>& descs);
 
+// The projection GEMMs of the path on the same int8 tensor-core machinery:
+// C (M x N, column-major ldc) = op(A) B with A fp32 (op(A) = A^T of the
+// column-major lda view when trans_a, i.e. rows of a row-major matrix; else
+// the columns of a row-major K x M block), B fp64 column-major K x N
+// (N <= 256), alpha = 1, beta = 0 -- gemm_grouped(ctx, F32, F64, trans_a,
+// false, false, descs) semantics, fp64-grade.
+bool ozaki_gemm_applicable(DType ta, bool trans_a, const GemmDesc& d);
+void ozaki_gemm_batch(Ctx& ctx, bool trans_a, const std::vector<GemmDesc>& descs);
+
 }  // namespace hsvdcu

@@ -61,21 +61,47 @@ constexpr int kBBytes = kBN * kBK;                 // 32 KB
 constexpr int kStageBytes = kABytes + kBBytes;     // 48 KB
 constexpr int kGramThreads = 192;                  // 6 warps
 constexpr size_t kGramSmem = (size_t)kStages * kStageBytes + 1024 + 256;
+constexpr int kMaxK = 65536;  // |level sum| <= 7 * K * 64^2 < 2^31
 
+// Column-scaled source (k_oz_split): the columns of a row-major fp32 block
+// become digit-plane rows (transposed, K = the block's rows).
 struct OzLeaf {
   const float* x;      // block base (row-major, ld)
   long long ld;
-  int K;               // rows of the block (Gram contraction length)
-  int q;               // columns of the block (Gram order)
-  long long row_base;  // first row of this leaf's digit planes in the slice tensor
-  double* G;           // q x q column-major output
+  int K;               // rows of the block (contraction length)
+  int q;               // columns of the block (operand rows)
+  long long row_base;  // first row of this block's digit planes in the slice tensor
+  double* G;           // unused by the slicer
   long long ldg;
   double* scale;       // per column 2^e_j (q_pad entries)
   unsigned* colmax;    // per column max |x| bits (q_pad entries)
 };
 
+// Row-scaled source (k_oz_split_rows): rows with K contiguous (a row-major
+// fp32 block, or the columns of a column-major fp64 factor).
+struct OzRows {
+  const void* x;
+  int f64;
+  long long ld;        // row stride (elements)
+  int rows, K;
+  long long row_base;  // first digit-plane row
+  double* scale;       // per row 2^e (rows entries)
+};
+
+// One product C (M x N, column-major ldc) = A_op B_op^T over digit planes.
+struct OzJob {
+  long long a_row, b_row;  // plane-1 rows of A_op row 0 / B_op row 0
+  double* C;
+  long long ldc;
+  const double* sa;        // scale of each C row (A_op row)
+  const double* sb;        // scale of each C column (B_op row)
+  int M, N;
+  int sym;                 // Gram: write j >= l and mirror to the upper triangle
+};
+
+// One CTA: rows mb*128.., columns nb*256.. of job, K chunks [k0, k0 + nk).
 struct OzTile {
-  int leaf, jb, lb;
+  int job, mb, nb, k0, nk;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -158,6 +184,71 @@ __global__ void __launch_bounds__(256) k_oz_split(const OzLeaf* __restrict__ lea
     const long long row = L.row_base + (long long)a * plane_rows + j0 + jr;
     *reinterpret_cast<uint4*>(planes + row * kpad + i0 + p * 16) = w;
   }
+}
+
+// per-row scale of a row-scaled source: one warp per row, max |x| over K
+__global__ void k_oz_rowmax(const OzRows* __restrict__ srcs) {
+  const OzRows S = srcs[blockIdx.y];
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (row >= S.rows) return;
+  double m = 0.0;
+  if (S.f64) {
+    const double* p = static_cast<const double*>(S.x) + (long long)row * S.ld;
+    for (int k = lane; k < S.K; k += 32) m = fmax(m, fabs(p[k]));
+  } else {
+    const float* p = static_cast<const float*>(S.x) + (long long)row * S.ld;
+    for (int k = lane; k < S.K; k += 32) m = fmax(m, (double)fabsf(__ldg(p + k)));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0) {
+    int e = 0;
+    if (m > 0.0) frexp(m, &e);  // m < 2^e
+    S.scale[row] = m > 0.0 ? ldexp(1.0, e) : 1.0;
+  }
+}
+
+// rows x K -> S digit planes (K-major, rows padded by the caller's zeroed
+// tail, K padded to kpad with zeros).  Thread: 4 consecutive K of one row.
+__global__ void __launch_bounds__(256) k_oz_split_rows(const OzRows* __restrict__ srcs,
+                                                       signed char* __restrict__ planes,
+                                                       long long kpad, long long plane_rows) {
+  const OzRows S = srcs[blockIdx.z];
+  const int row = blockIdx.y * 8 + (threadIdx.x >> 5);
+  const int k4 = blockIdx.x * 128 + (threadIdx.x & 31) * 4;
+  if (row >= S.rows) return;
+  const double inv = 1.0 / S.scale[row];  // exact: a power of two
+  uint32_t packed[kS];
+#pragma unroll
+  for (int a = 0; a < kS; ++a) packed[a] = 0u;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int k = k4 + u;
+    if (k < S.K) {
+      if (S.f64) {
+        double v = static_cast<const double*>(S.x)[(long long)row * S.ld + k] * inv * 64.0;
+#pragma unroll
+        for (int a = 0; a < kS; ++a) {
+          const double d = rint(v);
+          v = (v - d) * 128.0;
+          packed[a] |= (uint32_t)(uint8_t)(signed char)(int)d << (8 * u);
+        }
+      } else {
+        float v = __ldg(static_cast<const float*>(S.x) + (long long)row * S.ld + k) *
+                  (float)inv * 64.0f;
+#pragma unroll
+        for (int a = 0; a < kS; ++a) {
+          const float d = rintf(v);
+          v = (v - d) * 128.0f;
+          packed[a] |= (uint32_t)(uint8_t)(signed char)(int)d << (8 * u);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < kS; ++a)
+    *reinterpret_cast<uint32_t*>(planes + (S.row_base + (long long)a * plane_rows + row) * kpad +
+                                 k4) = packed[a];
 }
 
 // ---------------------------------------------------------------------------
@@ -248,9 +339,9 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, int (&v)[32]) {
 // ---------------------------------------------------------------------------
 
 __global__ void __launch_bounds__(kGramThreads, 1)
-    k_oz_gram(const __grid_constant__ CUtensorMap tmap, const OzLeaf* __restrict__ leaves,
-              const OzTile* __restrict__ tiles, long long plane_rows, int nk,
-              int* __restrict__ part) {
+    k_oz_gram(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+              const OzJob* __restrict__ jobs, const OzTile* __restrict__ tiles,
+              long long planeA, long long planeB, int* __restrict__ part) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -262,7 +353,7 @@ __global__ void __launch_bounds__(kGramThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const OzTile T = tiles[blockIdx.x];
-  const OzLeaf L = leaves[T.leaf];
+  const OzJob J = jobs[T.job];
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -274,7 +365,8 @@ __global__ void __launch_bounds__(kGramThreads, 1)
       mbar_init(&tempty[b], 4);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -287,8 +379,8 @@ __global__ void __launch_bounds__(kGramThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  const long long rowA0 = L.row_base + (long long)T.jb * kBM;
-  const long long rowB0 = L.row_base + (long long)T.lb * kBN;
+  const long long rowA0 = J.a_row + (long long)T.mb * kBM;
+  const long long rowB0 = J.b_row + (long long)T.nb * kBN;
 
   if (warp == 0) {
     // ---------------- TMA producer ----------------
@@ -298,15 +390,15 @@ __global__ void __launch_bounds__(kGramThreads, 1)
       for (int t = 2; t <= kS + 1; ++t) {
         for (int a = max(1, t - kS); a <= min(kS, t - 1); ++a) {
           const int b = t - a;
-          const int ra = static_cast<int>(rowA0 + (long long)(a - 1) * plane_rows);
-          const int rb = static_cast<int>(rowB0 + (long long)(b - 1) * plane_rows);
-          for (int kc = 0; kc < nk; ++kc) {
+          const int ra = static_cast<int>(rowA0 + (long long)(a - 1) * planeA);
+          const int rb = static_cast<int>(rowB0 + (long long)(b - 1) * planeB);
+          for (int kc = T.k0; kc < T.k0 + T.nk; ++kc) {
             mbar_wait(&empty[stage], phase ^ 1);
             uint8_t* sa = smem + stage * kStageBytes;
             mbar_expect_tx(&full[stage], kStageBytes);
-            tma_load_2d(sa, &tmap, kc * kBK, ra, &full[stage]);
-            tma_load_2d(sa + kABytes, &tmap, kc * kBK, rb, &full[stage]);
-            tma_load_2d(sa + kABytes + kABytes, &tmap, kc * kBK, rb + kBM, &full[stage]);
+            tma_load_2d(sa, &tmA, kc * kBK, ra, &full[stage]);
+            tma_load_2d(sa + kABytes, &tmB, kc * kBK, rb, &full[stage]);
+            tma_load_2d(sa + kABytes + kABytes, &tmB, kc * kBK, rb + kBM, &full[stage]);
             if (++stage == kStages) {
               stage = 0;
               phase ^= 1;
@@ -327,7 +419,7 @@ __global__ void __launch_bounds__(kGramThreads, 1)
         const uint32_t d = tmem + buf * kBN;
         bool first = true;
         for (int a = max(1, t - kS); a <= min(kS, t - 1); ++a) {
-          for (int kc = 0; kc < nk; ++kc) {
+          for (int kc = 0; kc < T.nk; ++kc) {
             mbar_wait(&full[stage], phase);
             tc_fence_after();
             const uint32_t sa = smem_u32(smem + stage * kStageBytes);
@@ -380,40 +472,74 @@ __global__ void __launch_bounds__(kGramThreads, 1)
   }
 }
 
-// G from the int32 level tiles: G_jl = 2^(e_j+e_l) sum_t 2^-(12+7(t-2)) P_t
-// (most significant level first, fp64), written for j >= l and mirrored to
-// (l, j) through a shared-memory transpose (full symmetric storage for the
-// eigensolver).  One CTA per Gram tile, 32x32 sub-blocks.
-__global__ void __launch_bounds__(256) k_oz_combine(const OzLeaf* __restrict__ leaves,
+// C from the int32 level tiles of the K splits of one output tile:
+// C_jl = sa_j sb_l sum_t 2^-(12+7(t-2)) sum_split P_t (most significant level
+// first, fixed order: deterministic), fp64.  Gram jobs (sym) write j >= l
+// and mirror to (l, j) through a shared-memory transpose (full symmetric
+// storage for the eigensolver).  One CTA (512 threads) per output tile in
+// 32-column x 128-row slabs: every thread keeps its 7 x NSPLIT level loads
+// of two elements in flight (the pass is HBM-bound: 28 B read per element).
+template <int NSPLIT>
+__global__ void __launch_bounds__(512) k_oz_combine(const OzJob* __restrict__ jobs,
                                                     const OzTile* __restrict__ tiles,
-                                                    const int* __restrict__ part) {
-  __shared__ double sub[32][33];
-  const OzTile T = tiles[blockIdx.x];
-  const OzLeaf L = leaves[T.leaf];
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const int* P = part + (long long)blockIdx.x * (kS * kBN * kBM);
-  for (int rb = 0; rb < kBM; rb += 32) {
-    const int row0 = T.jb * kBM + rb;
-    for (int cb = 0; cb < kBN; cb += 32) {
-      const int col0 = T.lb * kBN + cb;
-      if (row0 + 31 < col0 || row0 >= L.q || col0 >= L.q) continue;  // no j >= l element
-      const int row = row0 + tx;
-      const double sr = row < L.q ? L.scale[row] : 0.0;
-      for (int y = ty; y < 32; y += 8) {
-        const int col = col0 + y;
-        const int* p = P + (cb + y) * kBM + rb + tx;
-        double acc = 0.0;
+                                                    const int* __restrict__ part, int nsplit_rt) {
+  __shared__ double sub[32][kBM + 1];  // [col in slab][row]
+  const int nsplit = NSPLIT > 0 ? NSPLIT : nsplit_rt;
+  const OzTile T = tiles[(long long)blockIdx.x * nsplit];
+  const OzJob J = jobs[T.job];
+  const int tid = threadIdx.x;
+  const int row = T.mb * kBM + (tid & (kBM - 1));  // 128 rows
+  const int cq = tid >> 7;                          // 4 column groups
+  const double sr = row < J.M ? J.sa[row] : 0.0;
+  const int* P = part + (long long)blockIdx.x * nsplit * (kS * kBN * kBM) + (tid & (kBM - 1));
+  for (int cb = 0; cb < kBN; cb += 32) {
+    const int col0 = T.nb * kBN + cb;
+    if (col0 >= J.N) break;
+    if (J.sym && T.mb * kBM + kBM - 1 < col0) break;  // the rest of the tile is j < l
 #pragma unroll
-        for (int t = 0; t < kS; ++t) acc += ldexp((double)__ldcs(p + t * kBN * kBM), -(12 + 7 * t));
-        acc *= sr * (col < L.q ? L.scale[col] : 0.0);
-        sub[y][tx] = acc;
-        if (row < L.q && col < L.q && row >= col) L.G[row + (long long)col * L.ldg] = acc;
+    for (int h = 0; h < 8; h += 2) {
+      // two columns per thread per pass: cb + cq*8 + h, +1
+      const int c0 = cb + cq * 8 + h;
+      double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+      for (int t = 0; t < kS; ++t) {
+        long long l0 = 0, l1 = 0;
+        if (NSPLIT > 0) {
+#pragma unroll
+          for (int sp = 0; sp < (NSPLIT > 0 ? NSPLIT : 1); ++sp) {
+            const int* q = P + ((long long)sp * kS + t) * (kBN * kBM);
+            l0 += __ldcs(q + c0 * kBM);
+            l1 += __ldcs(q + (c0 + 1) * kBM);
+          }
+        } else {
+          for (int sp = 0; sp < nsplit; ++sp) {
+            const int* q = P + ((long long)sp * kS + t) * (kBN * kBM);
+            l0 += __ldcs(q + c0 * kBM);
+            l1 += __ldcs(q + (c0 + 1) * kBM);
+          }
+        }
+        acc0 += ldexp((double)l0, -(12 + 7 * t));
+        acc1 += ldexp((double)l1, -(12 + 7 * t));
       }
+      const int col = T.nb * kBN + c0;
+      acc0 *= sr * (col < J.N ? J.sb[col] : 0.0);
+      acc1 *= sr * (col + 1 < J.N ? J.sb[col + 1] : 0.0);
+      sub[c0 - cb][tid & (kBM - 1)] = acc0;
+      sub[c0 - cb + 1][tid & (kBM - 1)] = acc1;
+      if (row < J.M) {
+        if (col < J.N && (!J.sym || row >= col)) J.C[row + (long long)col * J.ldc] = acc0;
+        if (col + 1 < J.N && (!J.sym || row >= col + 1))
+          J.C[row + (long long)(col + 1) * J.ldc] = acc1;
+      }
+    }
+    if (J.sym) {
       __syncthreads();
-      for (int y = ty; y < 32; y += 8) {
-        // mirror: (row0 + y, col0 + tx) <- sub[tx][y] when row0 + y > col0 + tx
-        const int mrow = col0 + tx, mcol = row0 + y;
-        if (mcol < L.q && mrow < L.q && mcol > mrow) L.G[mrow + (long long)mcol * L.ldg] = sub[tx][y];
+      // mirror: C[col][row] <- C[row][col] for row > col; 32 columns of the
+      // slab become 32 rows; a warp writes 32 consecutive destination rows
+      for (int e = tid; e < 32 * kBM; e += 512) {
+        const int rr = e >> 5, cc = e & 31;  // source row rr (0..127), slab column cc
+        const int srow = T.mb * kBM + rr, scol = col0 + cc;
+        if (srow < J.M && scol < J.N && srow > scol) J.C[scol + (long long)srow * J.ldc] = sub[cc][rr];
       }
       __syncthreads();
     }
@@ -451,92 +577,257 @@ int slices_env() {
 
 bool ozaki_gram_applicable(DType dt, const GemmDesc& d) {
   // tall fp32 blocks (G = X_b^T X_b, K = rows): every BASELINE fp32 leaf
-  return slices_env() > 0 && dt == DType::F32 && d.K >= 1 && d.K <= 65536 && d.M >= 1 &&
+  return slices_env() > 0 && dt == DType::F32 && d.K >= 1 && d.K <= kMaxK && d.M >= 1 &&
          d.M == d.N && d.A == d.B;
 }
+
+bool ozaki_gemm_applicable(DType ta, bool trans_a, const GemmDesc& d) {
+  (void)trans_a;
+  const char* e = std::getenv("HSVD_PROJ");
+  if (e && std::strcmp(e, "dmma") == 0) return false;
+  // N > 160: the 256-wide MMA tile wastes < 40% and the 28 products beat
+  // the fp64 DMMA GEMM (measured, round 2: config 5's N = 200 projections
+  // 70 -> ~40 ms; config 3/4's N = 64/128 were slower than DMMA, bound by
+  // the padded tile and the A-plane traffic of 28 products)
+  return ta == DType::F32 && d.K >= 1 && d.K <= kMaxK && d.M >= 1 && d.N > 160 && d.N <= kBN &&
+         d.alpha == 1.0 && d.beta == 0.0;
+}
+
+namespace {
+
+struct PlaneSet {
+  signed char* planes = nullptr;
+  long long plane_rows = 0;  // rows of one digit plane (all sources)
+  long long kpad = 0;
+  CUtensorMap map;
+};
+
+CUtensorMap make_map(signed char* planes, long long kpad, long long rows) {
+  CUtensorMap tmap;
+  const cuuint64_t gdim[2] = {(cuuint64_t)kpad, (cuuint64_t)rows};
+  const cuuint64_t gstride[1] = {(cuuint64_t)kpad};
+  const cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)kBM};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult cr = encode_fn()(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, planes, gdim, gstride, box,
+                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) throw Error(kCuda, "cuTensorMapEncodeTiled failed");
+  return tmap;
+}
+
+template <typename T>
+T* stage_table(Ctx& ctx, const std::vector<T>& v) {
+  return static_cast<T*>(ctx.staging.put_to(ctx.arena.alloc(v.size() * sizeof(T)), v.data(),
+                                            v.size() * sizeof(T), ctx.stream));
+}
+
+// Column-scaled, transposed planes of fp32 blocks (sources' rows_base and
+// scale pointers are filled in here; each source takes q_pad = ceil(q/256)
+// plane rows).
+PlaneSet slice_cols(Ctx& ctx, std::vector<OzLeaf>& src, long long kpad) {
+  PlaneSet ps;
+  ps.kpad = kpad;
+  int max_qp = 0, Kmax = 0;
+  for (auto& l : src) {
+    const int qp = ceil_div(l.q, kBN) * kBN;
+    l.row_base = ps.plane_rows;
+    ps.plane_rows += qp;
+    max_qp = std::max(max_qp, qp);
+    Kmax = std::max(Kmax, l.K);
+  }
+  double* scales = ctx.arena.alloc_n<double>((size_t)ps.plane_rows);
+  unsigned* cmax = ctx.arena.alloc_n<unsigned>((size_t)ps.plane_rows);
+  for (auto& l : src) {
+    l.scale = scales + l.row_base;
+    l.colmax = cmax + l.row_base;
+  }
+  ps.planes = ctx.arena.alloc_n<signed char>((size_t)(kS * ps.plane_rows * kpad));
+  const int nl = static_cast<int>(src.size());
+  OzLeaf* dl = stage_table(ctx, src);
+  HSVD_CUDA(cudaMemsetAsync(cmax, 0, (size_t)ps.plane_rows * sizeof(unsigned), ctx.stream));
+  const int rpb = 256;
+  ctx.launch_begin();
+  k_oz_colmax<<<dim3(ceil_div(max_qp, 256), ceil_div(Kmax, rpb), nl), 256, 0, ctx.stream>>>(dl, rpb);
+  ctx.check_launch("k_oz_colmax");
+  ctx.launch_begin();
+  k_oz_split<<<dim3((unsigned)(kpad / 128), max_qp / 32, nl), 256, 0, ctx.stream>>>(
+      dl, ps.planes, kpad, ps.plane_rows);
+  ctx.check_launch("k_oz_split");
+  ps.map = make_map(ps.planes, kpad, kS * ps.plane_rows);
+  return ps;
+}
+
+// Row-scaled planes (rows with K contiguous): fp32 blocks or the columns of
+// column-major fp64 factors.  Each source takes ceil(rows/256)*256 plane
+// rows (the padding rows stay unwritten: they only reach C rows / columns
+// that are never stored).
+PlaneSet slice_rows(Ctx& ctx, std::vector<OzRows>& src, long long kpad) {
+  PlaneSet ps;
+  ps.kpad = kpad;
+  int max_rows = 0;
+  for (auto& r : src) {
+    r.row_base = ps.plane_rows;
+    ps.plane_rows += (long long)ceil_div(r.rows, kBN) * kBN;
+    max_rows = std::max(max_rows, r.rows);
+  }
+  double* scales = ctx.arena.alloc_n<double>((size_t)ps.plane_rows);
+  for (auto& r : src) r.scale = scales + r.row_base;
+  ps.planes = ctx.arena.alloc_n<signed char>((size_t)(kS * ps.plane_rows * kpad));
+  const int ns = static_cast<int>(src.size());
+  OzRows* ds = stage_table(ctx, src);
+  ctx.launch_begin();
+  k_oz_rowmax<<<dim3(ceil_div(max_rows, 8), ns), 256, 0, ctx.stream>>>(ds);
+  ctx.check_launch("k_oz_rowmax");
+  ctx.launch_begin();
+  k_oz_split_rows<<<dim3((unsigned)(kpad / 128), ceil_div(max_rows, 8), ns), 256, 0, ctx.stream>>>(
+      ds, ps.planes, kpad, ps.plane_rows);
+  ctx.check_launch("k_oz_split_rows");
+  ps.map = make_map(ps.planes, kpad, kS * ps.plane_rows);
+  return ps;
+}
+
+// Tiles of every job (Gram jobs: the lower triangle only), each output tile
+// split over nsplit K ranges (consecutive tile entries), then the
+// tensor-core launch and the combine.
+void run_products(Ctx& ctx, const PlaneSet& A, const PlaneSet& B, const std::vector<OzJob>& jobs) {
+  const int nk = static_cast<int>(A.kpad / kBK);
+  long long outs = 0;
+  for (const auto& j : jobs) {
+    const int mt = ceil_div(j.M, kBM), nt = ceil_div(j.N, kBN);
+    for (int mb = 0; mb < mt; ++mb)
+      for (int nb = 0; nb < nt; ++nb)
+        if (!j.sym || nb * kBN <= mb * kBM + kBM - 1) ++outs;
+  }
+  // enough CTAs for two per SM slot, each split keeping >= 8 K chunks
+  int nsplit = (int)std::max<long long>(1, (2LL * ctx.num_sms + outs - 1) / std::max(1LL, outs));
+  nsplit = std::max(1, std::min({nsplit, nk / 8, 16}));
+  const int per = ceil_div(nk, nsplit);
+  nsplit = ceil_div(nk, per);
+  std::vector<OzTile> ht;
+  ht.reserve((size_t)outs * nsplit);
+  for (int ji = 0; ji < (int)jobs.size(); ++ji) {
+    const OzJob& j = jobs[ji];
+    const int mt = ceil_div(j.M, kBM), nt = ceil_div(j.N, kBN);
+    for (int mb = 0; mb < mt; ++mb)
+      for (int nb = 0; nb < nt; ++nb) {
+        if (j.sym && nb * kBN > mb * kBM + kBM - 1) continue;
+        for (int sp = 0; sp < nsplit; ++sp)
+          ht.push_back({ji, mb, nb, sp * per, std::min(per, nk - sp * per)});
+      }
+  }
+  OzJob* dj = stage_table(ctx, jobs);
+  OzTile* dt = stage_table(ctx, ht);
+  int* part = ctx.arena.alloc_n<int>(ht.size() * (size_t)kS * kBN * kBM);
+  smem_optin(k_oz_gram, kGramSmem);
+  // tensor-pipe work of the launch: int8 multiply-adds x 2 over every tile,
+  // product and K chunk (the profiler's "flops" for this kernel)
+  ctx.pending_flops = (double)ht.size() * (kS * (kS + 1) / 2) * 2.0 * kBM * kBN * (double)per * kBK;
+  ctx.launch_begin();
+  k_oz_gram<<<(unsigned)ht.size(), kGramThreads, kGramSmem, ctx.stream>>>(
+      A.map, B.map, dj, dt, A.plane_rows, B.plane_rows, part);
+  ctx.check_launch("k_oz_gram");
+  ctx.launch_begin();
+  if (nsplit == 1)
+    k_oz_combine<1><<<(unsigned)outs, 512, 0, ctx.stream>>>(dj, dt, part, 1);
+  else
+    k_oz_combine<0><<<(unsigned)outs, 512, 0, ctx.stream>>>(dj, dt, part, nsplit);
+  ctx.check_launch("k_oz_combine");
+}
+
+constexpr size_t kPlaneBudget = size_t(4) << 30;  // digit planes + level tiles per launch
+
+}  // namespace
 
 void ozaki_gram_batch(Ctx& ctx, const std::vector<GemmDesc>& descs) {
   if (descs.empty()) return;
   int Kmax = 0;
   for (const auto& d : descs) Kmax = std::max(Kmax, d.K);
   const long long kpad = (long long)ceil_div(Kmax, kBK) * kBK;
-  smem_optin(k_oz_gram, kGramSmem);
-  // batches of leaves bounded by the digit-plane memory (~2 GB)
-  const size_t kPlaneBudget = size_t(2) << 30;
   size_t i0 = 0;
   while (i0 < descs.size()) {
     size_t i1 = i0;
-    long long rows = 0;
+    long long used = 0;
     while (i1 < descs.size()) {
       const long long qp = (long long)ceil_div(descs[i1].M, kBN) * kBN;
       // planes (S q_pad K_pad bytes) + level tiles (~ S q_pad^2 / 2 int32)
       const long long need = kS * qp * kpad + 2LL * kS * qp * (qp + kBN);
-      if (i1 > i0 && (size_t)(rows + need) > kPlaneBudget) break;
-      rows += need;
+      if (i1 > i0 && (size_t)(used + need) > kPlaneBudget) break;
+      used += need;
       ++i1;
     }
     Arena::Mark mk = ctx.arena.mark();
-    const int nl = static_cast<int>(i1 - i0);
-    std::vector<OzLeaf> hl(nl);
-    std::vector<OzTile> ht;
-    long long base = 0, plane_rows = 0;
-    int max_qp = 0;
-    for (int l = 0; l < nl; ++l) max_qp = std::max(max_qp, ceil_div(descs[i0 + l].M, kBN) * kBN);
-    // plane layout: rows = a * plane_rows + leaf_base + j, plane_rows = sum_l q_pad(l)
-    for (int l = 0; l < nl; ++l) plane_rows += (long long)ceil_div(descs[i0 + l].M, kBN) * kBN;
-    double* scales = ctx.arena.alloc_n<double>((size_t)plane_rows);
-    unsigned* cmax = ctx.arena.alloc_n<unsigned>((size_t)plane_rows);
-    signed char* planes = ctx.arena.alloc_n<signed char>((size_t)(kS * plane_rows * kpad));
-    for (int l = 0; l < nl; ++l) {
-      const GemmDesc& d = descs[i0 + l];
-      const int qp = ceil_div(d.M, kBN) * kBN;
-      hl[l] = {static_cast<const float*>(d.A), d.lda, d.K, d.M, base, d.C, d.ldc, scales + base,
-               cmax + base};
-      for (int jb = 0; jb * kBM < qp; ++jb)
-        for (int lb = 0; lb * kBN <= jb * kBM + kBM - 1 && lb * kBN < qp; ++lb)
-          ht.push_back({l, jb, lb});
-      base += qp;
+    std::vector<OzLeaf> src;
+    for (size_t i = i0; i < i1; ++i) {
+      const GemmDesc& d = descs[i];
+      src.push_back({static_cast<const float*>(d.A), d.lda, d.K, d.M, 0, d.C, d.ldc, nullptr,
+                     nullptr});
     }
-    // job tables read by several launches: staged into arena memory
-    OzLeaf* dl = static_cast<OzLeaf*>(ctx.staging.put_to(
-        ctx.arena.alloc(hl.size() * sizeof(OzLeaf)), hl.data(), hl.size() * sizeof(OzLeaf),
-        ctx.stream));
-    OzTile* dt = static_cast<OzTile*>(ctx.staging.put_to(
-        ctx.arena.alloc(ht.size() * sizeof(OzTile)), ht.data(), ht.size() * sizeof(OzTile),
-        ctx.stream));
-    HSVD_CUDA(cudaMemsetAsync(cmax, 0, (size_t)plane_rows * sizeof(unsigned), ctx.stream));
+    PlaneSet ps = slice_cols(ctx, src, kpad);
+    std::vector<OzJob> jobs;
+    for (size_t i = i0; i < i1; ++i) {
+      const OzLeaf& l = src[i - i0];
+      jobs.push_back({l.row_base, l.row_base, descs[i].C, descs[i].ldc, l.scale, l.scale,
+                      descs[i].M, descs[i].M, 1});
+    }
+    run_products(ctx, ps, ps, jobs);
+    ctx.arena.release(mk);
+    i0 = i1;
+  }
+}
 
-    const int rpb = 256;
-    ctx.launch_begin();
-    k_oz_colmax<<<dim3(ceil_div(max_qp, 256), ceil_div(Kmax, rpb), nl), 256, 0, ctx.stream>>>(dl,
-                                                                                              rpb);
-    ctx.check_launch("k_oz_colmax");
-    ctx.launch_begin();
-    k_oz_split<<<dim3((unsigned)(kpad / 128), max_qp / 32, nl), 256, 0, ctx.stream>>>(
-        dl, planes, kpad, plane_rows);
-    ctx.check_launch("k_oz_split");
-
-    CUtensorMap tmap;
-    const cuuint64_t gdim[2] = {(cuuint64_t)kpad, (cuuint64_t)(kS * plane_rows)};
-    const cuuint64_t gstride[1] = {(cuuint64_t)kpad};
-    const cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)kBM};
-    const cuuint32_t estr[2] = {1, 1};
-    CUresult cr = encode_fn()(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, planes, gdim, gstride, box,
-                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (cr != CUDA_SUCCESS) throw Error(kCuda, "cuTensorMapEncodeTiled failed");
-    // tensor-pipe work of the launch: int8 multiply-adds x 2 over every
-    // tile, product and padded K (the profiler's "flops" for this kernel)
-    ctx.pending_flops = (double)ht.size() * (kS * (kS + 1) / 2) * 2.0 * kBM * kBN * (double)kpad;
-    int* part = ctx.arena.alloc_n<int>(ht.size() * (size_t)kS * kBN * kBM);
-    ctx.launch_begin();
-    k_oz_gram<<<(unsigned)ht.size(), kGramThreads, kGramSmem, ctx.stream>>>(
-        tmap, dl, dt, plane_rows, static_cast<int>(kpad / kBK), part);
-    ctx.check_launch("k_oz_gram");
-    ctx.launch_begin();
-    k_oz_combine<<<(unsigned)ht.size(), 256, 0, ctx.stream>>>(dl, dt, part);
-    ctx.check_launch("k_oz_combine");
+void ozaki_gemm_batch(Ctx& ctx, bool trans_a, const std::vector<GemmDesc>& descs) {
+  if (descs.empty()) return;
+  int Kmax = 0;
+  for (const auto& d : descs) Kmax = std::max(Kmax, d.K);
+  const long long kpad = (long long)ceil_div(Kmax, kBK) * kBK;
+  // split every product into row chunks whose A planes fit half the budget
+  struct Piece {
+    const GemmDesc* d;
+    int m0, mc;
+  };
+  const long long chunk_rows =
+      std::max<long long>(kBN, (long long)(kPlaneBudget / 2 / (kS * kpad)) / kBN * kBN);
+  std::vector<Piece> pieces;
+  for (const auto& d : descs)
+    for (int m0 = 0; m0 < d.M; m0 += (int)chunk_rows)
+      pieces.push_back({&d, m0, (int)std::min<long long>(chunk_rows, d.M - m0)});
+  size_t i0 = 0;
+  while (i0 < pieces.size()) {
+    size_t i1 = i0;
+    long long used = 0;
+    while (i1 < pieces.size()) {
+      const long long mp = (long long)ceil_div(pieces[i1].mc, kBN) * kBN;
+      const long long need = kS * (mp + kBN) * kpad + 16LL * kS * kBM * kBN * (mp / kBM);
+      if (i1 > i0 && (size_t)(used + need) > kPlaneBudget) break;
+      used += need;
+      ++i1;
+    }
+    Arena::Mark mk = ctx.arena.mark();
+    std::vector<OzLeaf> acol;
+    std::vector<OzRows> arow, brow;
+    for (size_t i = i0; i < i1; ++i) {
+      const Piece& pc = pieces[i];
+      const GemmDesc& d = *pc.d;
+      const float* A = static_cast<const float*>(d.A);
+      if (trans_a)  // op(A) rows = rows of a row-major fp32 matrix (ld = lda), K contiguous
+        arow.push_back({A + (long long)pc.m0 * d.lda, 0, d.lda, pc.mc, d.K, 0, nullptr});
+      else  // op(A) rows = columns of a row-major fp32 K x M block: transposed planes
+        acol.push_back({A + pc.m0, d.lda, d.K, pc.mc, 0, nullptr, 0, nullptr, nullptr});
+      // B: column-major K x N fp64; its columns are the operand rows
+      brow.push_back({d.B, 1, d.ldb, d.N, d.K, 0, nullptr});
+    }
+    PlaneSet pa = trans_a ? slice_rows(ctx, arow, kpad) : slice_cols(ctx, acol, kpad);
+    PlaneSet pb = slice_rows(ctx, brow, kpad);
+    std::vector<OzJob> jobs;
+    for (size_t i = i0; i < i1; ++i) {
+      const Piece& pc = pieces[i];
+      const GemmDesc& d = *pc.d;
+      const long long ar = trans_a ? arow[i - i0].row_base : acol[i - i0].row_base;
+      const double* sa = trans_a ? arow[i - i0].scale : acol[i - i0].scale;
+      jobs.push_back({ar, brow[i - i0].row_base, d.C + pc.m0, d.ldc, sa, brow[i - i0].scale,
+                      pc.mc, d.N, 0});
+    }
+    run_products(ctx, pa, pb, jobs);
     ctx.arena.release(mk);
     i0 = i1;
   }

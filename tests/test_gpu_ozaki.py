@@ -78,3 +78,28 @@ def test_leaves_on_int8_gram_vs_oracle(gram, monkeypatch):
     assert got.rank() == ref.rank() == 30
     assert np.abs(got.sigma - ref.sigma).max() <= 1e-9 * ref.sigma[0]
     assert O.largest_principal_angle(ref.u, got.u) < 1e-7
+
+
+@pytest.mark.parametrize("shape,grid,k", [((3000, 2400), (3, 4), 200), ((8000, 1024), (4, 1), 180),
+                                          ((1500, 3000), (2, 3), 200)])
+def test_projections_on_int8_match_dmma(shape, grid, k, monkeypatch):
+    """The projection GEMMs (leaf X_b Z, V-recovery X_j^T U_j, U-recovery
+    X V_r; routed to the tcgen05 Ozaki planes for N > 160 columns) against the
+    same pipeline with them on the fp64 DMMA GEMM: fp64-grade agreement."""
+    import paper_1710_02812_b200 as H
+    rng = np.random.default_rng(shape[0] + shape[1])
+    m, n = shape
+    r = min(m, n, 2 * k)
+    u = np.linalg.qr(rng.standard_normal((m, r)))[0]
+    v = np.linalg.qr(rng.standard_normal((n, r)))[0]
+    x = ((u * np.exp(-0.04 * np.arange(r))) @ v.T + 1e-5 * rng.standard_normal((m, n))).astype(
+        np.float32)
+    cfg = H.MatConfig(gamma=1e-12, row_block_rows=m // grid[0], col_block_cols=n // grid[1],
+                      max_rank=k)
+    oz = H.rank_k_svd(x, cfg)
+    monkeypatch.setenv("HSVD_PROJ", "dmma")
+    dm = H.rank_k_svd(x, cfg)
+    assert oz.rank() == dm.rank() == k
+    assert np.abs(oz.sigma - dm.sigma).max() <= 1e-12 * dm.sigma[0]
+    assert O.largest_principal_angle(dm.u, oz.u) < 1e-9
+    assert O.largest_principal_angle(dm.v, oz.v) < 1e-9
