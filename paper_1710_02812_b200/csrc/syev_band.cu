@@ -2,7 +2,7 @@
 // B2 by cluster panel QR + delayed DMMA trailing updates, band ->
 // tridiagonal by pipelined Householder bulge chasing, eigenvectors by
 // inverse iteration on the tridiagonal pushed through the chase reflectors
-// (k_q2_apply) or, when forced, by inverse iteration on the band itself;
+// (k_q2_tbuild + k_q2_wy, blocked on DMMA) or, when forced, by inverse iteration on the band itself;
 // then back through the stage-1 reflectors (syev.cu back_transform).
 #include "syev_impl.cuh"
 
@@ -257,17 +257,8 @@ __device__ __forceinline__ double band_ld(const double* p) {
   return CG ? __ldcg(p) : *p;
 }
 
-// Steps of sweep s (k with r0 = s+1+32k <= n-2) and the steps of all sweeps
-// before it: the compact sweep-major index of the stored chase reflectors.
+// Steps of sweep s (k with r0 = s+1+32k <= n-2).
 __device__ __forceinline__ int sweep_steps(int n, int s) { return (n - 3 - s) / B2 + 1; }
-__device__ __forceinline__ long long floor_sum(long long A) {  // sum_{a=0}^{A} floor(a/B2)
-  if (A < 0) return 0;
-  const long long q = (A + 1) / B2, r = (A + 1) % B2;
-  return B2 * q * (q - 1) / 2 + r * q;
-}
-__device__ __forceinline__ long long steps_before(int n, int s) {
-  return s + floor_sum(n - 3) - floor_sum(n - 3 - s);
-}
 
 // carry: x and the left block of this step are the rows-after block the
 // same warp updated in its previous step (its column 0 and columns 1..31),
@@ -317,8 +308,8 @@ __device__ __forceinline__ bool chase_step(double* bb, int c, int r0, int L, int
   const double scal = 1.0 / (alpha - beta);
   const double v = lane == 0 ? 1.0 : (lx ? x * scal : 0.0);
   vs[lane] = v;
-  if (rout) {  // kept for the eigenvector back-transform (k_q2_apply)
-    __stcs(rout + lane, v);  // streaming: read once by k_q2_apply, keep L2 for the band
+  if (rout) {  // kept for the eigenvector back-transform (k_q2_wy)
+    __stcs(rout + lane, v);  // streaming: read later by k_q2_tbuild / k_q2_wy, keep L2 for the band
     if (lane == 0) __stcs(rout + B2, tau);
   }
   if (lx) *px = lane == 0 ? beta : 0.0;
@@ -489,7 +480,7 @@ __global__ void __launch_bounds__(CHASE_WARPS * 32, 1) k_chase(const EigDev* __r
       const int c = k == 0 ? s : s + 1 + (k - 1) * B2;
       const int nl = r0 - c - 1;                // left-block columns (0 or B2-1)
       const int na = min(n, r0 + 2 * B2) - r1;  // rows after R
-      double* rout = J.refl ? J.refl + (steps_before(n, s) + k) * (B2 + 1) : nullptr;
+      double* rout = J.refl ? J.refl + (refl_off(n, k) + s) * RS : nullptr;
       const bool last = r0 + B2 > n - 2;  // the loop's own continuation test
       const bool ok =
           (L == B2 && nl == B2 - 1)
@@ -500,7 +491,7 @@ __global__ void __launch_bounds__(CHASE_WARPS * 32, 1) k_chase(const EigDev* __r
       if (!ok) {  // no bulge left in this sweep: its remaining reflectors are I
         if (J.refl && lane == 0)
           for (int k2 = k; k2 < sweep_steps(n, s); ++k2)
-            J.refl[(steps_before(n, s) + k2) * (B2 + 1) + B2] = 0.0;
+            J.refl[(refl_off(n, k2) + s) * RS + B2] = 0.0;
         break;
       }
       __syncwarp();  // every lane's band stores before lane 0's release
@@ -523,101 +514,310 @@ __global__ void __launch_bounds__(CHASE_WARPS * 32, 1) k_chase(const EigDev* __r
 }
 
 // Eigenvectors of the band matrix from those of its tridiagonal: Z <- Q2 Z
-// with Q2 the product of the chase reflectors in chase order, applied in
-// reverse (LAPACK dsbtrd's Q, applied as dormtr would).  Every reflector
-// re-reads and rewrites its 32 rows of Z, so the rows must live on chip: one
-// CTA per NC eigenvectors keeps its n x NC slice of Z in shared memory for
-// the whole pass (row-major; lane = column x row group, rows interleaved so
-// a warp's accesses are conflict-free).  The reflectors of one sweep touch
-// disjoint 32-row blocks: the CTA's Q2_WARPS warps share a sweep's blocks and
-// synchronise once per sweep, with the next sweep's reflectors staged into
-// shared memory by cp.async while the current one is applied.
-constexpr int Q2_WARPS = 16;  // measured on B200 (cfg2 leaves): 8 -> 25.1 ms, 16 -> 21.9, 32 -> 23.5
+// with Q2 the product of the chase reflectors in chase order (LAPACK
+// dsbtrd's Q, applied as dormtr would), blocked for the DMMA tensor path
+// (tools/proto/q2_wy.py is the numpy model; it checks the order below
+// against the reflector-by-reflector application).
+//
+// Group a = sweeps QG*a-1 .. QG*a+QG-2; block (k, a) = H(s0,k) ... H(s0+7,k)
+// = I - V T V^T, V the 39 x 8 parallelogram of the group's step-k reflectors
+// on rows QG*a + B2*k .. +39 (reflector j at offset j), T upper (dlarft 'F').
+// The sweeps of one step touch disjoint rows, and H(s,k) overlaps H(s',k')
+// (s < s') only for k' in {k, k-1}, so a pass over a super-group of QSG
+// groups may go down the rows: for k ascending, the groups' blocks in
+// descending order; super-groups are applied last first.
+//
+// k_q2_tbuild: T of every block (one warp per block), stored as the DMMA
+// B fragment of T^T; also clears v of identity reflectors (tau = 0, left
+// unset by the chase) so every value the apply reads is finite.
+//
+// k_q2_wy: one consumer warp per 8 eigenvector columns keeps the super-
+// group's 96-row window of Z^T in DMMA accumulator registers (lane: column
+// lane/4, rows 2(lane%4)+{0,1} of each 8-row tile) for the whole downward
+// pass: per block W^T = Z_w^T V (10 DMMA, the k index permuted so the
+// window's accumulator registers serve directly as A fragments), W2^T = W^T
+// T^T (2), Z_w^T -= W2^T V^T (10); no shuffles, no shared-memory traffic on
+// Z.  Each pass step stores the 32 rows the super-group no longer touches
+// and loads 32 new ones (prefetched one step ahead); a lane only ever reads
+// its own earlier stores, so warps never synchronise on Z.  A producer warp
+// streams the blocks (V: one contiguous run of the step-major reflector
+// storage, T: 512 B) into a ring of shared-memory stages with
+// cp.async.bulk + mbarrier transaction counts; the consumers release a
+// stage with one arrive per warp.
+constexpr int QSG = 8;                  // groups per super-group pass (window 96 rows)
+constexpr int QW = 4;                   // consumer warps per CTA (8 columns each)
+constexpr int QDEPTH = 16;              // ring stages (one WY block each)
+constexpr int QV_BYTES = QG * RS * 8;   // 2176
+constexpr int QT_BYTES = 64 * 8;        // 512
+constexpr int QSTAGE = QV_BYTES + QT_BYTES;
+constexpr int QWIN = (QSG * QG + B2) / 8;  // window tiles (12)
+static_assert(QSTAGE % 16 == 0 && QV_BYTES % 16 == 0, "bulk copies need 16-byte multiples");
+static_assert(B2 == 32 && QG == 8, "k_q2_wy's fragment maps assume 32-row reflectors, 8 per block");
+constexpr size_t kQ2Smem = 256 + (size_t)QDEPTH * QSTAGE;
 
-template <int NC>
-__global__ void __launch_bounds__(Q2_WARPS * 32) k_q2_apply(const EigDev* __restrict__ jobs) {
-  constexpr int G = 32 / NC;       // row groups per warp
-  constexpr int RPL = B2 / G;      // rows per lane
+constexpr int TB_WARPS = 8;
+
+__global__ void __launch_bounds__(TB_WARPS * 32) k_q2_tbuild(const EigDev* __restrict__ jobs) {
+  const EigDev J = jobs[blockIdx.y];
+  const int n = J.n;
+  if (n < 3 || !J.refl) return;
+  const int K = chase_steps(n);
+  const long long total = tblk_off(n, K);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ double vs[TB_WARPS][QG][B2 + QG];  // zero tail for the shifted dots
+  __shared__ double Ss[TB_WARPS][QG][QG];
+  __shared__ double tw[TB_WARPS][QG];
+  __shared__ double Tm[TB_WARPS][QG][QG];
+  for (long long idx = (long long)blockIdx.x * TB_WARPS + warp; idx < total;
+       idx += (long long)gridDim.x * TB_WARPS) {
+    int lo = 0, hi = K - 1;  // step of the block: last k with tblk_off(n, k) <= idx
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (tblk_off(n, mid) <= idx) lo = mid;
+      else hi = mid - 1;
+    }
+    const int k = lo, a = (int)(idx - tblk_off(n, k));
+    const int smax = n - 3 - B2 * k;
+    double* rk = J.refl + refl_off(n, k) * RS;
+#pragma unroll
+    for (int j = 0; j < QG; ++j) {
+      const int s = QG * a - 1 + j;
+      const bool valid = s >= 0 && s <= smax;
+      double* r = rk + (long long)s * RS;
+      const double tau = valid ? r[B2] : 0.0;
+      double v = valid ? r[lane] : 0.0;
+      if (valid && tau == 0.0) {
+        r[lane] = 0.0;
+        v = 0.0;
+      }
+      vs[warp][j][lane] = v;
+      if (lane < QG) vs[warp][j][B2 + lane] = 0.0;
+      if (lane == 0) tw[warp][j] = tau;
+    }
+    __syncwarp();
+    if (lane < QG * (QG - 1) / 2) {  // S[j][jp] = v_j^T v_jp over the window, j < jp
+      int p = lane, j = 0;
+      while (p >= QG - 1 - j) {
+        p -= QG - 1 - j;
+        ++j;
+      }
+      const int jp = j + 1 + p, d = jp - j;
+      double s0 = 0.0, s1 = 0.0;
+      for (int t = 0; t + 1 < B2; t += 2) {
+        s0 += vs[warp][j][t + d] * vs[warp][jp][t];
+        s1 += vs[warp][j][t + 1 + d] * vs[warp][jp][t + 1];
+      }
+      Ss[warp][j][jp] = s0 + s1;
+    }
+    __syncwarp();
+    if (lane < QG) {  // row i of T: T[i][j] = -tau_j sum_{l=i}^{j-1} T[i][l] S[l][j]
+      const int i = lane;
+      double tr[QG];
+#pragma unroll
+      for (int j = 0; j < QG; ++j) {
+        double t = 0.0;
+        if (j == i) {
+          t = tw[warp][j];
+        } else if (j > i) {
+          double acc = 0.0;
+#pragma unroll
+          for (int l = 0; l < j; ++l)
+            if (l >= i) acc += tr[l] * Ss[warp][l][j];
+          t = -tw[warp][j] * acc;
+        }
+        tr[j] = t;
+      }
+#pragma unroll
+      for (int j = 0; j < QG; ++j) Tm[warp][i][j] = tr[j];
+    }
+    __syncwarp();
+    // B fragment of T^T for k_q2_wy: entry 2*lane + kt = T[lane/4][2(lane%4) + kt]
+    double2 out;
+    out.x = Tm[warp][lane >> 2][2 * (lane & 3)];
+    out.y = Tm[warp][lane >> 2][2 * (lane & 3) + 1];
+    reinterpret_cast<double2*>(J.q2T + idx * 64)[lane] = out;
+    __syncwarp();
+  }
+}
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void q2_mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void q2_dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__((QW + 1) * 32, 3) k_q2_wy(const EigDev* __restrict__ jobs) {
   const EigDev J = jobs[blockIdx.y];
   const int n = J.n, kk = J.kk;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nt = blockDim.x;
-  const int c0 = blockIdx.x * NC;
-  if (c0 >= kk || n < 3) return;
-  const int nc = min(NC, kk - c0);
-  const int kmax = sweep_steps(n, 0);
-  extern __shared__ __align__(16) double q2sm[];
-  double* Zs = q2sm;                              // [n][NC]
-  double* rbuf = q2sm + (size_t)n * NC;           // [2][kmax][B2 + 1]
-  for (int e = tid; e < n * NC; e += nt) {
-    const int r = e % n, q = e / n;
-    Zs[r * NC + q] = q < nc ? J.Z[r + (long long)(c0 + q) * J.ldz] : 0.0;
-  }
-  const double* R = J.refl;
-  auto stage = [&](int s, int buf) {
-    const double* src = R + steps_before(n, s) * (B2 + 1);
-    double* dst = rbuf + (size_t)buf * kmax * (B2 + 1);
-    const int cnt = sweep_steps(n, s) * (B2 + 1);
-    for (int e = tid; e < cnt; e += nt) {
-      const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst + e));
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src + e));
+  const int c_cta = blockIdx.x * QW * 8;
+  if (n < 3 || c_cta >= kk) return;
+  const int nwork = min(QW, (kk - c_cta + 7) / 8);  // consumer warps with columns
+  extern __shared__ __align__(128) unsigned char q2s[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(q2s);
+  uint64_t* empty = full + QDEPTH;
+  unsigned char* stages = q2s + 256;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // stale stage slots (sweeps outside a block) must hold finite values: T
+  // zeroes their rows and columns, and 0 * finite = 0
+  for (int e = tid; e < QDEPTH * QSTAGE / 8; e += blockDim.x)
+    reinterpret_cast<double*>(stages)[e] = 0.0;
+  if (tid == 0) {
+    for (int i = 0; i < QDEPTH; ++i) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(full + i)), "r"(1));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(empty + i)), "r"(nwork));
     }
-  };
-  stage(n - 3, 0);
-  asm volatile("cp.async.commit_group;\n");
-  const int q = lane % NC, g = lane / NC;  // column, row group
-  int it = 0;
-  for (int s = n - 3; s >= 0; --s, ++it) {
-    const int sb = it & 1;
-    if (s > 0) stage(s - 1, sb ^ 1);
-    asm volatile("cp.async.commit_group;\n");
-    asm volatile("cp.async.wait_group 1;\n");
-    __syncthreads();
-    const double* rb = rbuf + (size_t)sb * kmax * (B2 + 1);
-    const int K = sweep_steps(n, s);
-    for (int k = warp; k < K; k += Q2_WARPS) {
-      const double* rv = rb + k * (B2 + 1);
-      const double tau = rv[B2];
-      if (tau == 0.0) continue;
-      const int r0 = s + 1 + k * B2, L = min(B2, n - r0);
-      double z[RPL], v[RPL];
-#pragma unroll
-      for (int j = 0; j < RPL; ++j) {
-        const int i = g + G * j;  // row of the block
-        v[j] = rv[i];
-        z[j] = i < L ? Zs[(r0 + i) * NC + q] : 0.0;
-      }
-      double dot = 0.0;
-#pragma unroll
-      for (int j = 0; j < RPL; ++j) dot += v[j] * z[j];
-#pragma unroll
-      for (int o = NC; o < 32; o <<= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-      dot *= tau;
-#pragma unroll
-      for (int j = 0; j < RPL; ++j) {
-        const int i = g + G * j;
-        if (i < L) Zs[(r0 + i) * NC + q] = z[j] - dot * v[j];
-      }
-    }
-    __syncthreads();  // next sweep: rows overlap, and this buffer is restaged
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  asm volatile("cp.async.wait_group 0;\n");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
-  for (int e = tid; e < n * NC; e += nt) {
-    const int r = e % n, qq = e / n;
-    if (qq < nc) J.Z[r + (long long)(c0 + qq) * J.ldz] = Zs[r * NC + qq];
+  if (warp > nwork) return;
+
+  const int A0 = tgroups0(n);
+  const int nsg = (A0 + QSG - 1) / QSG;
+  if (warp == 0) {  // producer
+    if (lane != 0) return;
+    int it = 0;
+    for (int b = nsg - 1; b >= 0; --b) {
+      const int slo = max(0, QSG * QG * b - 1);
+      const int kend = (n - 3 - slo) / B2;
+      for (int k = 0; k <= kend; ++k) {
+        const int Ak = A0 - (B2 / QG) * k;
+        const double* rk = J.refl + refl_off(n, k) * RS;
+        const double* tk = J.q2T + tblk_off(n, k) * 64;
+        for (int g = QSG - 1; g >= 0; --g) {
+          const int a = b * QSG + g;
+          if (a >= Ak) continue;
+          const int slot = it % QDEPTH;
+          if (it >= QDEPTH) q2_mbar_wait(empty + slot, ((it / QDEPTH) & 1) ^ 1);
+          const int jlo = a == 0 ? 1 : 0;
+          const int sfirst = QG * a - 1 + jlo;
+          const int slast = min(QG * a + QG - 2, n - 3 - B2 * k);
+          const uint32_t vbytes = (uint32_t)(slast - sfirst + 1) * RS * 8;
+          unsigned char* st = stages + (size_t)slot * QSTAGE;
+          const uint32_t fb = smem_addr(full + slot);
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb),
+                       "r"(vbytes + QT_BYTES)
+                       : "memory");
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  smem_addr(st + jlo * RS * 8)),
+              "l"(rk + (long long)sfirst * RS), "r"(vbytes), "r"(fb)
+              : "memory");
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  smem_addr(st + QV_BYTES)),
+              "l"(tk + (long long)a * 64), "r"((uint32_t)QT_BYTES), "r"(fb)
+              : "memory");
+          ++it;
+        }
+      }
+    }
+    return;
   }
-}
 
-// Columns per CTA: as many as fit shared memory with the reflector buffers.
-int q2_cols(int n) {
-  const size_t rb = (size_t)2 * ((n - 3) / B2 + 1) * (B2 + 1) * sizeof(double);
-  for (int nc : {8, 4, 2})
-    if ((size_t)n * nc * sizeof(double) + rb <= 220 * 1024) return nc;
-  return 0;
-}
-
-size_t q2_smem(int n, int nc) {
-  return (size_t)n * nc * sizeof(double) + (size_t)2 * ((n - 3) / B2 + 1) * (B2 + 1) * sizeof(double);
+  // consumer warp: columns c_cta + 8*(warp-1) + 0..7
+  const int q = lane & 3, j1 = lane >> 2;
+  const int col = c_cta + 8 * (warp - 1) + j1;
+  const bool cok = col < kk;
+  double* Zc = J.Z + (long long)(cok ? col : 0) * J.ldz;
+  auto zload = [&](int row0, double (&t)[2]) {
+    const int r = row0 + 2 * q;
+    t[0] = (cok && r < n) ? Zc[r] : 0.0;
+    t[1] = (cok && r + 1 < n) ? Zc[r + 1] : 0.0;
+  };
+  auto zstore = [&](int row0, const double (&t)[2]) {
+    const int r = row0 + 2 * q;
+    if (cok && r < n) Zc[r] = t[0];
+    if (cok && r + 1 < n) Zc[r + 1] = t[1];
+  };
+  int it = 0;
+  double z[QWIN][2], zn[4][2];
+  for (int b = nsg - 1; b >= 0; --b) {
+    const int slo = max(0, QSG * QG * b - 1);
+    const int kend = (n - 3 - slo) / B2;
+    int base = QSG * QG * b;  // window rows base .. base + 95 (group g: base + 8g ..)
+#pragma unroll
+    for (int t = 0; t < QWIN; ++t) zload(base + 8 * t, z[t]);
+    for (int k = 0; k <= kend; ++k) {
+      const bool more = k < kend;
+      if (more) {
+#pragma unroll
+        for (int t = 0; t < 4; ++t) zload(base + 8 * (QWIN + t), zn[t]);
+      }
+      const int Ak = A0 - (B2 / QG) * k;
+#pragma unroll
+      for (int g = QSG - 1; g >= 0; --g) {
+        if (b * QSG + g >= Ak) continue;
+        const int slot = it % QDEPTH;
+        q2_mbar_wait(full + slot, (it / QDEPTH) & 1);
+        const double* sv = reinterpret_cast<const double*>(stages + (size_t)slot * QSTAGE);
+        const double2 tf = reinterpret_cast<const double2*>(sv + QV_BYTES / 8)[lane];
+        // W^T = Z_w^T V: k-step kt covers window rows 8(kt/2) + 2q + (kt&1)
+        double w0[2] = {0.0, 0.0}, w1[2] = {0.0, 0.0};
+#pragma unroll
+        for (int kt = 0; kt < 10; ++kt) {
+          const int e = 8 * (kt >> 1) + 2 * q + (kt & 1) - j1;
+          const double bv = (e >= 0 && e < B2) ? sv[j1 * RS + e] : 0.0;
+          if (kt & 1) q2_dmma(w1, z[g + (kt >> 1)][1], bv);
+          else q2_dmma(w0, z[g + (kt >> 1)][0], bv);
+        }
+        // V^T fragments of the update, read before the stage is released
+        double vb[5][2];
+#pragma unroll
+        for (int nt = 0; nt < 5; ++nt)
+#pragma unroll
+          for (int kt = 0; kt < 2; ++kt) {
+            const int j3 = 2 * q + kt, e = 8 * nt + j1 - j3;
+            vb[nt][kt] = (e >= 0 && e < B2) ? sv[j3 * RS + e] : 0.0;
+          }
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(empty + slot)) : "memory");
+        ++it;
+        // W2^T = W^T T^T (A fragments = W's accumulator registers, k = 2q + kt)
+        double u[2] = {0.0, 0.0};
+        q2_dmma(u, w0[0] + w1[0], tf.x);
+        q2_dmma(u, w0[1] + w1[1], tf.y);
+        // Z_w^T -= W2^T V^T
+#pragma unroll
+        for (int nt = 0; nt < 5; ++nt) {
+          q2_dmma(z[g + nt], -u[0], vb[nt][0]);
+          q2_dmma(z[g + nt], -u[1], vb[nt][1]);
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) zstore(base + 8 * t, z[t]);
+      if (more) {
+#pragma unroll
+        for (int t = 0; t < QWIN - 4; ++t) {
+          z[t][0] = z[t + 4][0];
+          z[t][1] = z[t + 4][1];
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          z[QWIN - 4 + t][0] = zn[t][0];
+          z[QWIN - 4 + t][1] = zn[t][1];
+        }
+        base += B2;
+      } else {
+#pragma unroll
+        for (int t = 4; t < QWIN; ++t) zstore(base + 8 * t, z[t]);
+      }
+    }
+  }
 }
 
 // Eigenvectors of the band matrix (band0, bandwidth B2) by inverse
@@ -958,10 +1158,10 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
     d.shifts = ctx.arena.alloc_n<double>(d.kk);
     d.cstarts = ctx.arena.alloc_n<int>(d.kk);
     d.vals_only = band_invit ? 1 : 2;
-    if (!band_invit) {
-      long long steps = 0;  // chase reflectors of all sweeps
-      for (int s2 = 0; s2 <= n - 3; ++s2) steps += (n - 3 - s2) / B2 + 1;
-      d.refl = ctx.arena.alloc_n<double>((size_t)std::max(1LL, steps) * (B2 + 1));
+    if (!band_invit) {  // chase reflectors of all sweeps + the T factors of their WY blocks
+      const int K = chase_steps(n);
+      d.refl = ctx.arena.alloc_n<double>((size_t)std::max(1LL, refl_off(n, K)) * RS);
+      d.q2T = ctx.arena.alloc_n<double>((size_t)std::max(1LL, tblk_off(n, K)) * 64);
     }
     HSVD_CUDA(cudaMemsetAsync(d.band, 0, (size_t)LDBB * n * sizeof(double), ctx.stream));
     lu_slot_max = std::max(lu_slot_max, (size_t)n * (2 * B2 + 1 + B2 + 3));
@@ -971,8 +1171,6 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
   // capped at 8 GB
   int cpm = std::max(1, std::min(ceil_div(3 * ctx.num_sms, count), ceil_div(kkmax, INV_WARPS)));
   while (cpm > 1 && lu_slot_max * sizeof(double) * INV_WARPS * cpm * count > (size_t(8) << 30)) --cpm;
-  const int q2nc = std::max(1, q2_cols(nmax));
-  const int q2x = ceil_div(kkmax, q2nc);
   if (band_invit) {
     double* lu = ctx.arena.alloc_n<double>(lu_slot_max * INV_WARPS * cpm * count);
     for (int g = 0; g < count; ++g) {  // indexed by blockIdx.x in the kernel
@@ -1096,18 +1294,21 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
   if (!band_invit) {
     launch_band_mgs(ctx, dd, count);  // clusters of the tridiagonal's vectors
     ctx.launch_begin();
-    const size_t q2smem = q2_smem(nmax, q2nc);
-    if (q2nc == 8) {
-      smem_optin(k_q2_apply<8>, q2smem);
-      k_q2_apply<8><<<dim3(q2x, count), Q2_WARPS * 32, q2smem, ctx.stream>>>(dd);
-    } else if (q2nc == 4) {
-      smem_optin(k_q2_apply<4>, q2smem);
-      k_q2_apply<4><<<dim3(q2x, count), Q2_WARPS * 32, q2smem, ctx.stream>>>(dd);
-    } else {
-      smem_optin(k_q2_apply<2>, q2smem);
-      k_q2_apply<2><<<dim3(q2x, count), Q2_WARPS * 32, q2smem, ctx.stream>>>(dd);
+    {
+      const long long tmax = tblk_off(nmax, chase_steps(nmax));
+      const int tbx = std::max(1, std::min(ceil_div(tmax, TB_WARPS), ceil_div(8 * ctx.num_sms, count)));
+      k_q2_tbuild<<<dim3(tbx, count), TB_WARPS * 32, 0, ctx.stream>>>(dd);
+      ctx.check_launch("k_q2_tbuild");
     }
-    ctx.check_launch("k_q2_apply");
+    ctx.launch_begin();
+    {  // algorithmic flops: 4 * 32 * kk per stored reflector
+      double fl = 0.0;
+      for (const EigDev& e : dev) fl += 4.0 * B2 * e.kk * (double)refl_off(e.n, chase_steps(e.n));
+      ctx.pending_flops = fl;
+    }
+    smem_optin(k_q2_wy, kQ2Smem);
+    k_q2_wy<<<dim3(ceil_div(kkmax, QW * 8), count), (QW + 1) * 32, kQ2Smem, ctx.stream>>>(dd);
+    ctx.check_launch("k_q2_wy");
   } else {
     const size_t smem =
         ((size_t)INV_WARPS * ((B2 + 1) * (2 * B2 + 1) + INV_RING) + 64) * sizeof(double);

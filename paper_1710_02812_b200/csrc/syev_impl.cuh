@@ -65,7 +65,8 @@ struct EigDev {
   double* Mb;        // B2 x B2
   double* Z1;        // (2*B2*group) x B2: pending-update products
   double* lu;        // per-warp band LU workspace (cpm * INV_WARPS slots per matrix)
-  double* refl;      // chase reflectors: (steps) x 33 (v[0..31], tau), sweep-major
+  double* refl;      // chase reflectors, step-major: (refl_off(n, k) + s) * RS (v[0..31], tau, pad)
+  double* q2T;       // WY T factors of the Q2 blocks, step-major: (tblk_off(n, k) + a) * 64
   long long lu_slot;  // doubles per slot
 };
 
@@ -81,6 +82,22 @@ __device__ __forceinline__ unsigned hash32(unsigned x) {
   x *= 0x846ca68bU;
   x ^= x >> 16;
   return x;
+}
+
+// Chase reflector storage (two-stage path).  Sweep s, step k acts on rows
+// s+1+B2*k .. s+B2+B2*k; step k exists for sweeps 0 .. n-3-B2*k, so the
+// reflectors are stored step-major (the WY blocks of k_q2_wy are runs of
+// consecutive sweeps at one step: one contiguous bulk copy each).
+constexpr int RS = 34;  // doubles per stored reflector: v[0..31], tau, pad (272 B, 16-byte multiple)
+constexpr int QG = 8;   // sweeps per WY block of the Q2 back-transform (group a: sweeps QG*a-1 ..)
+__host__ __device__ __forceinline__ int chase_steps(int n) { return n < 3 ? 0 : (n - 3) / B2 + 1; }
+__host__ __device__ __forceinline__ long long refl_off(int n, int k) {  // first entry of step k
+  return (long long)k * (n - 2) - (long long)(B2 / 2) * k * (k - 1);
+}
+// groups with a sweep at step k: A_k = A_0 - (B2/QG) k
+__host__ __device__ __forceinline__ int tgroups0(int n) { return (n - 2) / QG + 1; }
+__host__ __device__ __forceinline__ long long tblk_off(int n, int k) {
+  return (long long)k * tgroups0(n) - (long long)(B2 / QG / 2) * k * (k - 1);
 }
 
 // element (i, j), i >= j, of the lower band storage (two-stage path)

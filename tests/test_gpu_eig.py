@@ -85,9 +85,10 @@ def test_chase_cs1_forced(monkeypatch):
     _check_batch(a, lam, z, kk)
 
 
-def test_n4096_q2_apply_four_columns():
-    """n = 4096, kk = 200: config 5's leaf eigenproblem (two-stage by size,
-    Q2 back-transform with 4 eigenvector columns per CTA, k_q2_apply<4>)."""
+def test_n4096_q2_wy():
+    """n = 4096, kk = 200: config 5's leaf eigenproblem (two-stage by size;
+    blocked Q2 back-transform k_q2_tbuild + k_q2_wy with a partial last CTA:
+    200 columns = 6 CTAs of 32 + one warp of 8)."""
     import paper_1710_02812_b200 as H
     n, kk, count = 4096, 200, 2
     rng = np.random.default_rng(4096)
