@@ -264,11 +264,37 @@ __device__ __forceinline__ int sweep_steps(int n, int s) { return (n - 3 - s) / 
 // same warp updated in its previous step (its column 0 and columns 1..31),
 // still in registers (x, yl); last: no further step in this sweep, so the
 // updated rows-after block is stored instead of being carried.
+// The step's R and rows-after blocks are read from pf, the warp's shared-
+// memory copy of band columns r0..r0+31 (all LDBB diagonals), fetched by
+// cp.async while the previous step ran; once both blocks are in registers
+// the copy of the next step's columns is issued (nnext of them, 0: none).
+// Step k starts once sweep s-1 has finished its steps 0..k+2.  Step k+1's
+// columns are written by this sweep's step k+1 and by sweep s-1's steps
+// <= k+3 -- the last of which touches one element this sweep reads, the
+// rows-after block's corner (r0+63, r0+31) of step k+1 (s-1's step k+3
+// stores its x column there).  So the copy is issued during step k with
+// s-1's steps <= k+2 done, and the corner is read from global memory at the
+// start of step k+1 instead (tools/probes/chase_check.py: without it the
+// 2- and 4-CTA cluster chase, whose sweeps run closest together, goes wrong).
+template <bool CG>
+__device__ __forceinline__ void chase_fetch(double* pf, const double* src, int ncols, int lane) {
+  const int chunks = ncols * (LDBB / 2);  // 16-byte chunks
+  for (int e = lane; e < chunks; e += 32) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(pf + 2 * e));
+    if (CG)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src + 2 * e) : "memory");
+    else
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src + 2 * e) : "memory");
+  }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+
 template <bool FULL, bool CG>
 __device__ __forceinline__ bool chase_step(double* bb, int c, int r0, int L, int nl, int na,
                                            int lane, double* vs, double* ws, double* rout,
                                            bool carry, bool last, double& x,
-                                           double (&yl)[B2 - 1]) {
+                                           double (&yl)[B2 - 1], const double* pf, int nnext,
+                                           double corner) {
   constexpr long long LD = LDBB;
   const bool lx = lane < L;
   double* px = bb + (r0 + lane - c) + (long long)c * LD;
@@ -287,9 +313,9 @@ __device__ __forceinline__ bool chase_step(double* bb, int c, int r0, int L, int
       yl[l] = (lx && (FULL || l < nl)) ? band_ld<CG>(pyl + l * (LD - 1)) : 0.0;
   }
 #pragma unroll
-  for (int j = 0; j < B2; ++j) {
-    const double* pa = lane >= j ? pa1 + j * (LD - 1) : pa2 + j;
-    ar[j] = (lx && (FULL || j < L)) ? band_ld<CG>(pa) : 0.0;
+  for (int j = 0; j < B2; ++j) {  // (r0+lane, r0+j): column j, diagonal lane-j (or transposed)
+    const double* pa = lane >= j ? pf + j * LD + (lane - j) : pf + lane * LD + (j - lane);
+    ar[j] = (lx && (FULL || j < L)) ? *pa : 0.0;
   }
   const double xn2 = warp_sum(lane >= 1 ? x * x : 0.0);
   const double alpha = __shfl_sync(0xffffffffu, x, 0);
@@ -343,8 +369,10 @@ __device__ __forceinline__ bool chase_step(double* bb, int c, int r0, int L, int
   // rows-after block, loaded once the left block is done (fewer live
   // registers through the butterfly); the R update hides its latency
 #pragma unroll
-  for (int j = 0; j < B2; ++j) ya[j] = (ly && (FULL || j < L)) ? band_ld<CG>(pya + j * (LD - 1)) : 0.0;
-  __syncwarp();
+  for (int j = 0; j < B2; ++j) ya[j] = (ly && (FULL || j < L)) ? pf[j * LD + (L + lane - j)] : 0.0;
+  if (lane == B2 - 1) ya[B2 - 1] = corner;
+  __syncwarp();  // every lane's reads of pf done: refill it with the next step's columns
+  if (nnext > 0) chase_fetch<CG>(const_cast<double*>(pf), bb + (long long)(r0 + B2) * LD, nnext, lane);
   // R x R: two-sided (symmetric, lower storage); p = tau R v
   // (vs, ws: 16-byte aligned per-warp rows, read as double2 broadcasts)
   const double2* vs2 = reinterpret_cast<const double2*>(vs);
@@ -421,6 +449,8 @@ __global__ void __launch_bounds__(CHASE_WARPS * 32, 1) k_chase(const EigDev* __r
   __shared__ unsigned long long prog[CHASE_WARPS];
   __shared__ __align__(16) double vsh[CHASE_WARPS][B2];
   __shared__ __align__(16) double wsh[CHASE_WARPS][B2];
+  extern __shared__ __align__(16) double chase_pf[];  // [CHASE_WARPS][B2 * LDBB]
+  double* pf = chase_pf + (size_t)warp * B2 * LDBB;
   if (tid < CHASE_WARPS) prog[tid] = prog_encode(crank * CHASE_WARPS + tid - W, kSweepDone);
   cg::cluster_group cluster = cg::this_cluster();
   if (CL) cluster.sync();
@@ -482,12 +512,20 @@ __global__ void __launch_bounds__(CHASE_WARPS * 32, 1) k_chase(const EigDev* __r
       const int na = min(n, r0 + 2 * B2) - r1;  // rows after R
       double* rout = J.refl ? J.refl + (refl_off(n, k) + s) * RS : nullptr;
       const bool last = r0 + B2 > n - 2;  // the loop's own continuation test
+      if (k == 0) chase_fetch<CL>(pf, bb + (long long)r0 * LDBB, min(B2, n - r0), lane);
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      __syncwarp();
+      const int nnext = last ? 0 : min(B2, n - (r0 + B2));
+      // rows-after corner (r0+63, r0+31), possibly newer than the prefetched copy
+      const double corner = (lane == B2 - 1 && na == B2 && r0 + B2 <= n)
+                                ? band_ld<CL>(&band_at(bb, r0 + 2 * B2 - 1, r0 + B2 - 1))
+                                : 0.0;
       const bool ok =
           (L == B2 && nl == B2 - 1)
               ? chase_step<true, CL>(bb, c, r0, L, nl, na, lane, vsh[warp], wsh[warp], rout,
-                                     k > 0, last, cx, cyl)
+                                     k > 0, last, cx, cyl, pf, nnext, corner)
               : chase_step<false, CL>(bb, c, r0, L, nl, na, lane, vsh[warp], wsh[warp], rout,
-                                      k > 0, last, cx, cyl);
+                                      k > 0, last, cx, cyl, pf, nnext, corner);
       if (!ok) {  // no bulge left in this sweep: its remaining reflectors are I
         if (J.refl && lane == 0)
           for (int k2 = k; k2 < sweep_steps(n, s); ++k2)
@@ -497,6 +535,7 @@ __global__ void __launch_bounds__(CHASE_WARPS * 32, 1) k_chase(const EigDev* __r
       __syncwarp();  // every lane's band stores before lane 0's release
       publish(prog_encode(s, (unsigned)(k + 1)));
     }
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");  // a prefetch of a step that did not run
     __syncwarp();
     publish(prog_encode(s, kSweepDone));
   }
@@ -1271,13 +1310,16 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
   // (An L2 persisting access-policy window over the contiguous bands was
   // measured in round 2: no change at config 2, 388 -> 675 ms at config 5,
   // where the 545 MB of bands exceed the persisting carve-out; not used.)
+  const size_t chase_smem = (size_t)CHASE_WARPS * B2 * LDBB * sizeof(double);
   if (ccs == 1) {
-    k_chase<false><<<count, CHASE_WARPS * 32, 0, ctx.stream>>>(dd, 1);
+    smem_optin(k_chase<false>, chase_smem);
+    k_chase<false><<<count, CHASE_WARPS * 32, chase_smem, ctx.stream>>>(dd, 1);
   } else {
+    smem_optin(k_chase<true>, chase_smem);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(count * ccs);
     cfg.blockDim = dim3(CHASE_WARPS * 32);
-    cfg.dynamicSmemBytes = 0;
+    cfg.dynamicSmemBytes = chase_smem;
     cfg.stream = ctx.stream;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;

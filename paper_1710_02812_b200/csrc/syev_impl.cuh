@@ -28,7 +28,7 @@ constexpr int TRD_QMAX = 8;  // rows per thread when n > 1024 (n <= 8192)
 constexpr int EIG_THREADS = 512;
 constexpr int NB = 32;       // reflectors per compact-WY block
 constexpr int B2 = 32;       // bandwidth of the two-stage reduction
-constexpr int LDBB = 2 * B2 + 1;  // band storage: diagonals 0..2*B2 (chase fill)
+constexpr int LDBB = 2 * B2 + 2;  // band storage: diagonals 0..2*B2 (chase fill) + pad (16-byte columns)
 constexpr int kBandInvitMinN = 1 << 30;  // band inverse iteration: only when forced
 constexpr int kBandGroupDefault = 4;  // panels per delayed trailing update (two-stage stage 1)
 constexpr int INV_WARPS = 4;      // warps (= LU workspace slots) per band inverse iteration CTA

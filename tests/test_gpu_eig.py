@@ -98,3 +98,20 @@ def test_n4096_q2_wy():
         a[g] = x.T @ x
     lam, z = H.syevx_topk_batch(a, kk)
     _check_batch(a, lam, z, kk, tol_lam=1e-11, tol_res=1e-10)
+
+
+@pytest.mark.parametrize("cs", ["1", "2", "4"])
+def test_chase_cluster_sizes_repeat(cs, monkeypatch):
+    """The bulge chase with its sweeps on 1, 2 or 4 CTAs (2 and 4: the
+    sweeps run closest together, so a dependency the step-ahead band copy
+    missed shows up there first); three runs, each against LAPACK."""
+    import paper_1710_02812_b200 as H
+    monkeypatch.setenv("HSVD_TWO_STAGE_MIN_N", "1")
+    monkeypatch.setenv("HSVD_CHASE_CS", cs)
+    n, kk = 1100, 64
+    a = _gram(n, 77, 6.0)
+    w = np.linalg.eigvalsh(a)[::-1][:kk]
+    for _ in range(3):
+        lam, z = H.syevx_topk(a, kk)
+        assert np.abs(lam - w).max() <= 1e-12 * w[0]
+        assert np.abs(a @ z - z * lam).max() <= 1e-11 * w[0]
