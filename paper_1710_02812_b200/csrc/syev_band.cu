@@ -268,13 +268,13 @@ __device__ __forceinline__ int sweep_steps(int n, int s) { return (n - 3 - s) / 
 // memory copy of band columns r0..r0+31 (all LDBB diagonals), fetched by
 // cp.async while the previous step ran; once both blocks are in registers
 // the copy of the next step's columns is issued (nnext of them, 0: none).
-// Step k starts once sweep s-1 has finished its steps 0..k+2.  Step k+1's
-// columns are written by this sweep's step k+1 and by sweep s-1's steps
-// <= k+3 -- the last of which touches one element this sweep reads, the
-// rows-after block's corner (r0+63, r0+31) of step k+1 (s-1's step k+3
-// stores its x column there).  So the copy is issued during step k with
-// s-1's steps <= k+2 done, and the corner is read from global memory at the
-// start of step k+1 instead (tools/probes/chase_check.py: without it the
+// Step k starts once sweep s-1 has finished its steps 0..k+1 and stored the
+// beta of its step k+2.  Step k+1's columns are written by this sweep's step
+// k+1 and by sweep s-1's steps <= k+3 -- the last of which touches one
+// element this sweep reads, the rows-after block's corner (r0+63, r0+31) of
+// step k+1 (s-1's step k+3 stores its beta there).  So the copy is issued
+// during step k once s-1's step k+2 is complete, and the corner is read from
+// global memory at the start of step k+1 instead (tools/probes/chase_check.py: without it the
 // 2- and 4-CTA cluster chase, whose sweeps run closest together, goes wrong).
 template <bool CG>
 __device__ __forceinline__ void chase_fetch(double* pf, const double* src, int ncols, int lane) {
@@ -289,12 +289,12 @@ __device__ __forceinline__ void chase_fetch(double* pf, const double* src, int n
   asm volatile("cp.async.commit_group;\n" ::: "memory");
 }
 
-template <bool FULL, bool CG>
+template <bool FULL, bool CG, class PubBeta, class WaitPf>
 __device__ __forceinline__ bool chase_step(double* bb, int c, int r0, int L, int nl, int na,
                                            int lane, double* vs, double* ws, double* rout,
                                            bool carry, bool last, double& x,
                                            double (&yl)[B2 - 1], const double* pf, int nnext,
-                                           double corner) {
+                                           double corner, PubBeta&& pub_beta, WaitPf&& wait_pf) {
   constexpr long long LD = LDBB;
   const bool lx = lane < L;
   double* px = bb + (r0 + lane - c) + (long long)c * LD;
@@ -339,6 +339,7 @@ __device__ __forceinline__ bool chase_step(double* bb, int c, int r0, int L, int
     if (lane == 0) __stcs(rout + B2, tau);
   }
   if (lx) *px = lane == 0 ? beta : 0.0;
+  pub_beta();  // the successor sweep's next step needs only this element of the step
   // left block: d_l = sum_i v_i y_il by a transposing butterfly (lane l
   // ends with d_l), then y_il -= tau v_i d_l
   {
@@ -372,7 +373,10 @@ __device__ __forceinline__ bool chase_step(double* bb, int c, int r0, int L, int
   for (int j = 0; j < B2; ++j) ya[j] = (ly && (FULL || j < L)) ? pf[j * LD + (L + lane - j)] : 0.0;
   if (lane == B2 - 1) ya[B2 - 1] = corner;
   __syncwarp();  // every lane's reads of pf done: refill it with the next step's columns
-  if (nnext > 0) chase_fetch<CG>(const_cast<double*>(pf), bb + (long long)(r0 + B2) * LD, nnext, lane);
+  if (nnext > 0) {
+    wait_pf();  // the next step's columns: sweep s-1's step k+2 complete
+    chase_fetch<CG>(const_cast<double*>(pf), bb + (long long)(r0 + B2) * LD, nnext, lane);
+  }
   // R x R: two-sided (symmetric, lower storage); p = tau R v
   // (vs, ws: 16-byte aligned per-warp rows, read as double2 broadcasts)
   const double2* vs2 = reinterpret_cast<const double2*>(vs);
@@ -416,6 +420,9 @@ __device__ __forceinline__ bool chase_step(double* bb, int c, int r0, int L, int
       if (ly && (FULL || j < L)) pya[j * (LD - 1)] = ya[j] - y * a.x;
       if (ly && (FULL || j + 1 < L)) pya[(j + 1) * (LD - 1)] = ya[j + 1] - y * a.y;
     }
+    x = 0.0;  // nothing is carried out of a sweep's last step (frees the registers)
+#pragma unroll
+    for (int j = 0; j < B2 - 1; ++j) yl[j] = 0.0;
   } else {  // the next step's x and left block (stored by that step)
     const double2 a0 = vs2[0];
     x = ya[0] - y * a0.x;
@@ -473,40 +480,43 @@ __global__ void __launch_bounds__(CHASE_WARPS * 32, 1) k_chase(const EigDev* __r
   unsigned long long seen = 0;  // last acquired progress of sweep s-1's warp
   const int nsweeps = n - 2;
   for (int s = gw; s < nsweeps; s += W) {
+    // progress of sweep s-1 in half steps: 2k+1 once its step k stored the
+    // new subdiagonal element (beta), 2k+2 once step k is complete
+    auto wait_pred = [&](unsigned need) {
+      if (s == 0) return;
+      auto ahead = [&](unsigned long long pv) {
+        const int vs = (int)(pv >> 32) - 1;
+        const unsigned st = (unsigned)(pv & 0xffffffffu);
+        return vs > s - 1 || (vs == s - 1 && st >= need);
+      };
+      // progress only grows: a value already acquired that suffices needs
+      // no new (remote) poll
+      if (ahead(seen)) return;
+      while (true) {
+        unsigned long long pv;
+        if (CL)
+          asm volatile("ld.acquire.cluster.u64 %0, [%1];\n" : "=l"(pv) : "l"(pprog) : "memory");
+        else
+          pv = *pprog;
+        if (ahead(pv)) {
+          seen = pv;
+          break;
+        }
+        __nanosleep(64);
+      }
+      if (!CL) __threadfence_block();
+    };
     double cx, cyl[B2 - 1];  // x and left block, carried between consecutive steps
     for (int k = 0;; ++k) {
       const int r0 = s + 1 + k * B2;
       if (r0 >= n) break;
       const int r1 = min(n, r0 + B2), L = r1 - r0;
       if (L < 2) break;
-      if (s > 0) {  // wait for sweep s-1 to be 3 steps ahead (or done)
-        const unsigned need = (unsigned)(k + 3);
-        auto ahead = [&](unsigned long long pv) {
-          const int vs = (int)(pv >> 32) - 1;
-          const unsigned st = (unsigned)(pv & 0xffffffffu);
-          return vs > s - 1 || (vs == s - 1 && st >= need);
-        };
-        // progress only grows: a value already acquired that suffices needs
-        // no new (remote) poll
-        if (!ahead(seen)) {
-          while (true) {
-            unsigned long long pv;
-            if (CL)
-              asm volatile("ld.acquire.cluster.u64 %0, [%1];\n"
-                           : "=l"(pv)
-                           : "l"(pprog)
-                           : "memory");
-            else
-              pv = *pprog;
-            if (ahead(pv)) {
-              seen = pv;
-              break;
-            }
-            __nanosleep(100);
-          }
-          if (!CL) __threadfence_block();
-        }
-      }
+      // step k of sweep s touches sweep s-1's work only through its steps
+      // <= k+1 and the beta of its step k+2 (the rows-after corner, read
+      // fresh below); the step-ahead copy issued inside the step waits for
+      // s-1's step k+2 to be complete
+      wait_pred((unsigned)(2 * k + 5));
       const int c = k == 0 ? s : s + 1 + (k - 1) * B2;
       const int nl = r0 - c - 1;                // left-block columns (0 or B2-1)
       const int na = min(n, r0 + 2 * B2) - r1;  // rows after R
@@ -520,12 +530,14 @@ __global__ void __launch_bounds__(CHASE_WARPS * 32, 1) k_chase(const EigDev* __r
       const double corner = (lane == B2 - 1 && na == B2 && r0 + B2 <= n)
                                 ? band_ld<CL>(&band_at(bb, r0 + 2 * B2 - 1, r0 + B2 - 1))
                                 : 0.0;
+      auto pub_beta = [&]() { publish(prog_encode(s, (unsigned)(2 * k + 1))); };
+      auto wait_pf = [&]() { wait_pred((unsigned)(2 * k + 6)); };
       const bool ok =
           (L == B2 && nl == B2 - 1)
               ? chase_step<true, CL>(bb, c, r0, L, nl, na, lane, vsh[warp], wsh[warp], rout,
-                                     k > 0, last, cx, cyl, pf, nnext, corner)
+                                     k > 0, last, cx, cyl, pf, nnext, corner, pub_beta, wait_pf)
               : chase_step<false, CL>(bb, c, r0, L, nl, na, lane, vsh[warp], wsh[warp], rout,
-                                      k > 0, last, cx, cyl, pf, nnext, corner);
+                                      k > 0, last, cx, cyl, pf, nnext, corner, pub_beta, wait_pf);
       if (!ok) {  // no bulge left in this sweep: its remaining reflectors are I
         if (J.refl && lane == 0)
           for (int k2 = k; k2 < sweep_steps(n, s); ++k2)
@@ -533,7 +545,7 @@ __global__ void __launch_bounds__(CHASE_WARPS * 32, 1) k_chase(const EigDev* __r
         break;
       }
       __syncwarp();  // every lane's band stores before lane 0's release
-      publish(prog_encode(s, (unsigned)(k + 1)));
+      publish(prog_encode(s, (unsigned)(2 * k + 2)));
     }
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");  // a prefetch of a step that did not run
     __syncwarp();
