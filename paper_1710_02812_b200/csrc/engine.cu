@@ -206,11 +206,15 @@ std::vector<DFac> block_svd_batch(Ctx& ctx, const XView& x, const std::vector<Bl
   ctx.phase = "leaf.jacobi";
   jacobi_svd_batch(ctx, jj);
   ctx.phase = "leaf.fin";
+  // the projected side is written (and its null directions completed) for
+  // the retained columns only, unless the caller keeps it whole (full_svd:
+  // write_all / keep_both); a wide block's factor basis is the gathered
+  // eigenvector side, whose permutation covers all kk columns
   std::vector<FinJob> fj;
   for (int b = 0; b < nb; ++b) {
     Tmp& m = t[b];
     fj.push_back({m.P, m.s, m.s, m.kk, gamma, cap, m.Bp, m.s, m.sig, m.perm, d_rd + b,
-                  d_rd + nb + b, (write_all || !m.tall || keep_both) ? 1 : 0});
+                  d_rd + nb + b, (write_all || keep_both) ? 1 : 0});
   }
   finalize(ctx, fj);
   // the eigenvector side, permuted to the sigma order

@@ -453,13 +453,15 @@ __global__ void __launch_bounds__(EIG_THREADS) k_steig(const EigDev* __restrict_
   const int tid = threadIdx.x, nt = blockDim.x;
   const int lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
   extern __shared__ double sm[];
-  double* dd = sm;
+  // the tridiagonal and the per-eigenvalue arrays live in shared memory, or
+  // (large n or kk) in global scratch (3n + 3kk doubles)
+  double* dd = J.trig ? J.trig : sm;
   double* ee = dd + n;
   double* e2 = ee + n;
   double* lam = e2 + n;
   double* shift = lam + kk;
   double* dots = shift + kk;
-  double* red = dots + kk;
+  double* red = J.trig ? sm : dots + kk;
   int* cstart = reinterpret_cast<int*>(red + 32);
 
   double lo_g = 1e308, hi_g = -1e308, ee2max = 0.0;
@@ -728,7 +730,7 @@ __global__ void __launch_bounds__(EIG_THREADS) k_steig(const EigDev* __restrict_
   // iterates -> Z (column-major), R rows at a time through shared memory
   // (the tridiagonal's dd, ee, e2 are dead: 3n doubles)
   {
-    double* stage = sm;
+    double* stage = dd;
     const int R = max(1, min(n, 3 * n / kk));
     for (int r0 = 0; r0 < n; r0 += R) {
       const int rows = min(R, n - r0);
@@ -876,6 +878,21 @@ __device__ void cluster_gs(double* Z, long long ldz, int n, int cs, int ce, doub
       __syncthreads();
     }
   }
+}
+
+// One panel of a large cluster (k_gs_panel): its vectors orthonormalised
+// among themselves after the GEMM projections against the cluster's earlier
+// panels (launch_band_mgs).
+struct GsPanel {
+  double* Z;
+  long long ldz;
+  int n, q, np;
+};
+
+__global__ void __launch_bounds__(256) k_gs_panel(const GsPanel* __restrict__ pan) {
+  const GsPanel P = pan[blockIdx.x];
+  __shared__ double sm[GS_SMEM_DOUBLES];
+  cluster_gs(P.Z, P.ldz, P.n, P.q, P.q + P.np, sm);
 }
 
 __global__ void __launch_bounds__(256) k_band_mgs(const EigDev* __restrict__ jobs) {
@@ -1036,19 +1053,105 @@ const EigDev* upload_jobs(Ctx& ctx, const std::vector<EigDev>& dev) {
       ctx.staging.put_to(ctx.arena.alloc(bytes), dev.data(), bytes, ctx.stream));
 }
 
+constexpr size_t kSteigSmemMax = 220 * 1024;
+size_t steig_smem(int nmax, int kkmax, bool global_tri) {
+  return ((global_tri ? 0 : 3 * (size_t)nmax + 3 * (size_t)kkmax) + 32) * sizeof(double) +
+         (size_t)std::max(kkmax, EIG_THREADS) * sizeof(int) + 64;
+}
+bool steig_global_tri(int nmax, int kkmax) { return steig_smem(nmax, kkmax, false) > kSteigSmemMax; }
+
 void launch_steig(Ctx& ctx, const EigDev* dd, int count, int nmax, int kkmax) {
-    const size_t smem = (3 * (size_t)nmax + 3 * (size_t)kkmax + 32) * sizeof(double) +
-                        (size_t)std::max(kkmax, EIG_THREADS) * sizeof(int) + 64;
+    const size_t smem = steig_smem(nmax, kkmax, steig_global_tri(nmax, kkmax));
     smem_optin(k_steig, smem);
     ctx.launch_begin();
     k_steig<<<count, EIG_THREADS, smem, ctx.stream>>>(dd);
     ctx.check_launch("k_steig");
 }
 
-void launch_band_mgs(Ctx& ctx, const EigDev* dd, int count) {
+// Clusters of at least kBigCluster vectors (many eigenpairs requested, e.g.
+// the whole spectrum of a block under the default MatConfig, where dstein's
+// 1e-3 |T| rule groups most of them) would cost one CTA O(n c^2) in
+// k_band_mgs; they are orthonormalised instead by block classical
+// Gram-Schmidt twice over panels of GS_PW vectors, the projections against
+// the cluster's earlier panels as grouped DMMA GEMMs across the GPU and each
+// panel's own vectors by k_gs_panel.  The cluster starts are read back to
+// plan that (one small device->host copy, only when kk >= kBigCluster); big
+// clusters are then marked as singletons for k_band_mgs.
+constexpr int kBigCluster = 192;
+constexpr int GS_PW = 64;
+
+void launch_band_mgs(Ctx& ctx, const EigDev* dd, const std::vector<EigDev>& dev) {
+  const int count = static_cast<int>(dev.size());
+  struct Big {
+    int g, cs, ce;
+    double* W;
+  };
+  std::vector<Big> big;
+  int kkmax = 0;
+  for (const EigDev& e : dev) kkmax = std::max(kkmax, e.kk);
+  if (kkmax >= kBigCluster) {
+    std::vector<size_t> off(count + 1, 0);
+    for (int g = 0; g < count; ++g) off[g + 1] = off[g] + dev[g].kk;
+    int* h = ctx.pinned_ints(off[count]);
+    for (int g = 0; g < count; ++g)
+      HSVD_CUDA(cudaMemcpyAsync(h + off[g], dev[g].cstarts, dev[g].kk * sizeof(int),
+                                cudaMemcpyDeviceToHost, ctx.stream));
+    HSVD_CUDA(cudaStreamSynchronize(ctx.stream));
+    std::vector<int> hc(h, h + off[count]);
+    for (int g = 0; g < count; ++g) {
+      const int kk = dev[g].kk;
+      int* c = hc.data() + off[g];
+      bool changed = false;
+      for (int cs = 0; cs < kk;) {
+        int ce = cs + 1;
+        while (ce < kk && c[ce] == cs) ++ce;
+        if (ce - cs >= kBigCluster) {
+          big.push_back({g, cs, ce, ctx.arena.alloc_n<double>((size_t)(ce - cs) * GS_PW)});
+          for (int i = cs; i < ce; ++i) c[i] = i;  // singletons for k_band_mgs
+          changed = true;
+        }
+        cs = ce;
+      }
+      if (changed)
+        ctx.staging.put_to(dev[g].cstarts, c, kk * sizeof(int), ctx.stream);
+    }
+  }
   ctx.launch_begin();
   k_band_mgs<<<count, 256, 0, ctx.stream>>>(dd);
   ctx.check_launch("k_band_mgs");
+  if (big.empty()) return;
+  int npan = 0;
+  for (const Big& b : big) npan = std::max(npan, ceil_div(b.ce - b.cs, GS_PW));
+  std::vector<GemmDesc> d1, d2;
+  std::vector<GsPanel> pans;
+  for (int j = 0; j < npan; ++j) {
+    d1.clear();
+    d2.clear();
+    pans.clear();
+    for (const Big& b : big) {
+      const int q = b.cs + j * GS_PW;
+      if (q >= b.ce) continue;
+      const EigDev& e = dev[b.g];
+      const int np = std::min(GS_PW, b.ce - q), M = q - b.cs;
+      double* Zp = e.Z + (long long)q * e.ldz;
+      const double* Zc = e.Z + (long long)b.cs * e.ldz;
+      if (M > 0) {
+        d1.push_back({Zc, Zp, b.W, e.ldz, e.ldz, M, M, np, e.n, 1.0, 0.0});    // W = Zc^T Zp
+        d2.push_back({Zc, b.W, Zp, e.ldz, M, e.ldz, e.n, np, M, -1.0, 1.0});  // Zp -= Zc W
+      }
+      pans.push_back({e.Z, e.ldz, e.n, q, np});
+    }
+    for (int rep = 0; rep < 2 && !d1.empty(); ++rep) {
+      gemm_grouped(ctx, DType::F64, DType::F64, true, false, false, d1);
+      gemm_grouped(ctx, DType::F64, DType::F64, false, false, false, d2);
+    }
+    const size_t bytes = pans.size() * sizeof(GsPanel);
+    const GsPanel* dp = static_cast<const GsPanel*>(
+        ctx.staging.put_to(ctx.arena.alloc(bytes), pans.data(), bytes, ctx.stream));
+    ctx.launch_begin();
+    k_gs_panel<<<(unsigned)pans.size(), 256, 0, ctx.stream>>>(dp);
+    ctx.check_launch("k_gs_panel");
+  }
 }
 
 }  // namespace syev_impl
@@ -1068,7 +1171,6 @@ void eig_topk(Ctx& ctx, const std::vector<EigJob>& jobs_in) {
   for (int g = 0; g < count; ++g) {
     const EigJob& j = jobs[g];
     if (j.kk > j.n) throw Error(kInvalid, "eig_topk: kk > n");
-    if (j.n > 6144) throw Error(kInvalid, "eig_topk: n > 6144 not supported");
     EigDev& d = dev[g];
     d.A = j.A;
     d.lda = j.lda;
@@ -1093,6 +1195,9 @@ void eig_topk(Ctx& ctx, const std::vector<EigJob>& jobs_in) {
     nmax = std::max(nmax, j.n);
     kkmax = std::max(kkmax, j.kk);
   }
+  if (steig_global_tri(nmax, kkmax))  // k_steig's tridiagonal in global memory
+    for (int g = 0; g < count; ++g)
+      dev[g].trig = ctx.arena.alloc_n<double>((size_t)3 * dev[g].n + 3 * (size_t)dev[g].kk);
   const EigDev* dd = upload_jobs(ctx, dev);
 
   if (use_two_stage(nmax, count)) {
@@ -1144,7 +1249,7 @@ void eig_topk(Ctx& ctx, const std::vector<EigJob>& jobs_in) {
   {
     launch_steig(ctx, dd, count, nmax, kkmax);
     if (!inline_gs) {
-      launch_band_mgs(ctx, dd, count);
+      launch_band_mgs(ctx, dd, dev);
     }
   }
   // 3. back-transform Z <- Q Z (blocks applied last to first)

@@ -16,6 +16,7 @@ namespace {
 
 // Panel j0: copy the diagonal block to the band, Householder QR of the
 // panel below the band (R -> band, explicit V in place and in VW/WV), T.
+template <bool GP>
 __global__ void __launch_bounds__(512, 1) k_panel_qr(const EigDev* __restrict__ jobs, int j0,
                                                      int CS, int vcol) {
   // One matrix per cluster of CS CTAs; CTA c keeps rows [c*mc, (c+1)*mc) of
@@ -39,8 +40,10 @@ __global__ void __launch_bounds__(512, 1) k_panel_qr(const EigDev* __restrict__ 
   const int lo = min(m, crank * mc), hi = min(m, lo + mc), ml = hi - lo;
   const int ldp = mc + 1;
   extern __shared__ double psm[];
-  double* Pl = psm;                          // [B2][ldp]
-  double* dbuf = Pl + (size_t)B2 * ldp;      // [2][CS][2][B2] per-column exchange
+  // GP: the panel does not fit the cluster's shared memory (very large n)
+  // and lives in global scratch instead (L2-resident; same algorithm)
+  double* Pl = GP ? J.pscr + (size_t)crank * B2 * ldp : psm;  // [B2][ldp]
+  double* dbuf = GP ? psm : Pl + (size_t)B2 * ldp;          // [2][CS][2][B2] per-column exchange
   __shared__ double beta_s[B2], tau_s[B2];
   __shared__ double S[B2][B2 + 1], T[B2][B2 + 1];
   cluster.sync();  // peers' shared memory is live before any DSMEM write
@@ -187,12 +190,15 @@ size_t panel_smem(int mc, int cs) {
   return ((size_t)B2 * (mc + 1) + (size_t)4 * cs * B2) * sizeof(double);
 }
 
+bool panel_global(int mmax) { return panel_smem((mmax + 7) / 8, 8) > kPanelSmemMax; }
+
 void launch_panel_qr(Ctx& ctx, int count, int mmax, const EigDev* dd, int j0, int vcol) {
   int cs = 1;
   while (cs < 8 && panel_smem((mmax + cs - 1) / cs, cs) > kPanelSmemMax) cs *= 2;
-  const size_t smem = panel_smem((mmax + cs - 1) / cs, cs);
-  if (smem > kPanelSmemMax) throw Error(kInvalid, "k_panel_qr: n too large");
-  smem_optin(k_panel_qr, smem);
+  const bool gp = panel_smem((mmax + cs - 1) / cs, cs) > kPanelSmemMax;
+  const size_t smem = gp ? (size_t)4 * cs * B2 * sizeof(double) : panel_smem((mmax + cs - 1) / cs, cs);
+  auto kern = gp ? k_panel_qr<true> : k_panel_qr<false>;
+  smem_optin(kern, smem);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(count * cs);
   cfg.blockDim = dim3(512);
@@ -206,7 +212,7 @@ void launch_panel_qr(Ctx& ctx, int count, int mmax, const EigDev* dd, int j0, in
   cfg.attrs = at;
   cfg.numAttrs = 1;
   ctx.launch_begin();
-  HSVD_CUDA(cudaLaunchKernelEx(&cfg, k_panel_qr, dd, j0, cs, vcol));
+  HSVD_CUDA(cudaLaunchKernelEx(&cfg, kern, dd, j0, cs, vcol));
   ctx.check_launch("k_panel_qr");
 }
 
@@ -1199,6 +1205,7 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
     band_off += ((size_t)LDBB * n * sizeof(double) + 255) & ~size_t(255);
     d.band0 = band_invit ? ctx.arena.alloc_n<double>((size_t)LDBB * n) : nullptr;
     d.Tp = ctx.arena.alloc_n<double>((size_t)ceil_div(n, B2) * B2 * B2);
+    d.pscr = panel_global(nmax) ? ctx.arena.alloc_n<double>((size_t)B2 * (n + 16)) : nullptr;
     d.psum = ctx.arena.alloc_n<double>((size_t)8 * B2 * B2);
     d.VW = ctx.arena.alloc_n<double>((size_t)n * 2 * B2 * kBandGroup);
     d.WV = ctx.arena.alloc_n<double>((size_t)n * 2 * B2 * kBandGroup);
@@ -1346,7 +1353,7 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
   launch_steig(ctx, dd, count, nmax, kkmax);
   // eigenvectors of the band matrix
   if (!band_invit) {
-    launch_band_mgs(ctx, dd, count);  // clusters of the tridiagonal's vectors
+    launch_band_mgs(ctx, dd, dev);  // clusters of the tridiagonal's vectors
     ctx.launch_begin();
     {
       const long long tmax = tblk_off(nmax, chase_steps(nmax));
@@ -1370,7 +1377,7 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
     ctx.launch_begin();
     k_band_invit<<<dim3(cpm, count), INV_WARPS * 32, smem, ctx.stream>>>(dd);
     ctx.check_launch("k_band_invit");
-    launch_band_mgs(ctx, dd, count);
+    launch_band_mgs(ctx, dd, dev);
   }
   // back through the stage-1 reflectors
   SubPhase sp3(ctx, "back");

@@ -65,6 +65,8 @@ struct EigDev {
   double* Mb;        // B2 x B2
   double* Z1;        // (2*B2*group) x B2: pending-update products
   double* lu;        // per-warp band LU workspace (cpm * INV_WARPS slots per matrix)
+  double* trig;      // k_steig's d, e, e^2 in global memory (n too large for shared memory), or null
+  double* pscr;      // k_panel_qr's panel in global memory (n too large for shared memory), or null
   double* refl;      // chase reflectors, step-major: (refl_off(n, k) + s) * RS (v[0..31], tau, pad)
   double* q2T;       // WY T factors of the Q2 blocks, step-major: (tblk_off(n, k) + a) * 64
   long long lu_slot;  // doubles per slot
@@ -111,7 +113,7 @@ const EigDev* upload_jobs(Ctx& ctx, const std::vector<EigDev>& dev);
 // k_steig: top-kk eigenvalues of the tridiagonal (d, e) + vectors or shifts
 void launch_steig(Ctx& ctx, const EigDev* dd, int count, int nmax, int kkmax);
 // k_band_mgs: orthonormalise the vectors of every eigenvalue cluster in Z
-void launch_band_mgs(Ctx& ctx, const EigDev* dd, int count);
+void launch_band_mgs(Ctx& ctx, const EigDev* dd, const std::vector<EigDev>& dev);
 // Z <- Q Z through the reflectors stored in A (unit at row j + off)
 void back_transform(Ctx& ctx, const std::vector<EigJob>& jobs, const std::vector<EigDev>& dev,
                     const EigDev* dd, int nmax, int off);
