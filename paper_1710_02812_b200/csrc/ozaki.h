@@ -27,4 +27,13 @@ void ozaki_gram_batch(Ctx& ctx, const std::vector<GemmDesc>& descs);
 bool ozaki_gemm_applicable(DType ta, bool trans_a, const GemmDesc& d);
 void ozaki_gemm_batch(Ctx& ctx, bool trans_a, const std::vector<GemmDesc>& descs);
 
+// Stage-1 trailing update of the two-stage eigensolver (ozaki_syr2k.cu):
+// C (M x M, column-major ldc, full symmetric storage) -= VW WV^T for
+// descriptors {VW + r0, WV + r0, A22, ld, ld, lda, m, m, K, -1, 1} of
+// syev_band.cu, VW = [V_1 W_1 ...] (K = 64 x panels <= 256) and WV its
+// panel-swapped copy (only VW is read).  Opt-in: HSVD_SYR2K=ozaki (measured
+// slower than the DMMA SYR2K; see ozaki_syr2k.cu).
+bool ozaki_syr2k_applicable(const GemmDesc& d);
+void ozaki_syr2k_batch(Ctx& ctx, const std::vector<GemmDesc>& descs);
+
 }  // namespace hsvdcu

@@ -5,6 +5,7 @@
 // (k_q2_tbuild + k_q2_wy, blocked on DMMA) or, when forced, by inverse iteration on the band itself;
 // then back through the stage-1 reflectors (syev.cu back_transform).
 #include "syev_impl.cuh"
+#include "ozaki.h"
 
 namespace hsvdcu {
 namespace syev_impl {
@@ -1312,7 +1313,10 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
     }
     if (!g6.empty()) {
       SubPhase s2k(ctx, "band.syr2k");
-      gemm_grouped(ctx, DType::F64, DType::F64, false, true, true, g6);
+      std::vector<GemmDesc> oz, dm;  // tcgen05 int8 Ozaki update, else the DMMA SYR2K
+      for (const GemmDesc& g : g6) (ozaki_syr2k_applicable(g) ? oz : dm).push_back(g);
+      ozaki_syr2k_batch(ctx, oz);
+      gemm_grouped(ctx, DType::F64, DType::F64, false, true, true, dm);
     }
   }
   if (band_invit)  // the band before the chase, for the band inverse iteration

@@ -115,3 +115,15 @@ def test_chase_cluster_sizes_repeat(cs, monkeypatch):
         lam, z = H.syevx_topk(a, kk)
         assert np.abs(lam - w).max() <= 1e-12 * w[0]
         assert np.abs(a @ z - z * lam).max() <= 1e-11 * w[0]
+
+
+def test_two_stage_ozaki_syr2k_opt_in(monkeypatch):
+    """The opt-in tcgen05 int8 Ozaki trailing update (HSVD_SYR2K=ozaki,
+    ozaki_syr2k.cu) in the two-stage reduction, against LAPACK."""
+    import paper_1710_02812_b200 as H
+    monkeypatch.setenv("HSVD_TWO_STAGE_MIN_N", "1")
+    monkeypatch.setenv("HSVD_SYR2K", "ozaki")
+    n, kk, count = 1100, 64, 3
+    a = np.stack([_gram(n, 3000 + g, 6.0) for g in range(count)])
+    lam, z = H.syevx_topk_batch(a, kk)
+    _check_batch(a, lam, z, kk)
