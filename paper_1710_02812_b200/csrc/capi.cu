@@ -98,14 +98,35 @@ DType dtype_of(int dt) {
 // already issued (x_wait_chunk blocks only until a chunk is issued).
 class PageableStager final : public HostStager {
  public:
+  // Pageable host input: every 64 MB chunk is copied into one of the
+  // context's pinned slots by a persistent pool of host threads (created once
+  // per call: spawning threads per chunk cost ~10% of the copy), then DMAed
+  // on the copy stream while the pool fills the next slot.
   PageableStager(Ctx& c, char* dst, const char* src, int64_t row_bytes, int64_t src_pitch,
                  std::vector<int64_t> ends, std::vector<cudaEvent_t> evs)
       : c_(c), dst_(dst), src_(src), row_bytes_(row_bytes), pitch_(src_pitch),
         ends_(std::move(ends)), evs_(std::move(evs)) {
+    const unsigned hw = std::thread::hardware_concurrency();
+    // leave a core to the caller's thread (it keeps launching the compute)
+    nt_ = std::max<size_t>(1, std::min<size_t>(16, hw > 2 ? hw - 2 : 1));
+    for (size_t w = 1; w < nt_; ++w) {
+      try {
+        pool_.emplace_back([this, w] { worker(w); });
+      } catch (...) {
+        nt_ = w;  // fewer workers
+        break;
+      }
+    }
     th_ = std::thread([this] { run(); });
   }
   ~PageableStager() override {
     if (th_.joinable()) th_.join();
+    {
+      std::lock_guard<std::mutex> lk(pm_);
+      quit_ = true;
+    }
+    pcv_.notify_all();
+    for (auto& t : pool_) t.join();
   }
   void wait_issued(size_t i) override {
     std::unique_lock<std::mutex> lk(mu_);
@@ -114,39 +135,59 @@ class PageableStager final : public HostStager {
   }
 
  private:
+  // rows [a, b) of the current chunk (pinned slot pin_, first row r0_)
+  void piece(size_t w) {
+    const int64_t per = (rows_ + (int64_t)nt_ - 1) / (int64_t)nt_;
+    const int64_t a = std::min(rows_, (int64_t)w * per), b = std::min(rows_, a + per);
+    if (pitch_ == row_bytes_) {
+      if (b > a)
+        std::memcpy(pin_ + a * row_bytes_, src_ + (r0_ + a) * pitch_, (size_t)((b - a) * row_bytes_));
+    } else {
+      for (int64_t r = a; r < b; ++r)
+        std::memcpy(pin_ + r * row_bytes_, src_ + (r0_ + r) * pitch_, (size_t)row_bytes_);
+    }
+  }
+  void worker(size_t w) {
+    uint64_t seen = 0;
+    while (true) {
+      {
+        std::unique_lock<std::mutex> lk(pm_);
+        pcv_.wait(lk, [&] { return quit_ || gen_ != seen; });
+        if (quit_) return;
+        seen = gen_;
+      }
+      piece(w);
+      {
+        std::lock_guard<std::mutex> lk(pm_);
+        ++done_;
+      }
+      pcv_.notify_all();
+    }
+  }
   void run() {
     try {
       HSVD_CUDA(cudaSetDevice(c_.device));
       cudaStream_t cs = c_.get_copy_stream();
-      const unsigned hw = std::thread::hardware_concurrency();
-      const size_t nt = std::max(1u, std::min(8u, hw == 0 ? 1u : hw));
       int64_t r0 = 0;
       for (size_t i = 0; i < ends_.size(); ++i) {
         const int slot = static_cast<int>(i % Ctx::kH2dSlots);
         HSVD_CUDA(cudaEventSynchronize(c_.h2d_ev[slot]));  // slot's previous DMA done
-        char* pin = static_cast<char*>(c_.h2d_pin[slot]);
         const int64_t rows = ends_[i] - r0;
-        const int64_t per = (rows + (int64_t)nt - 1) / (int64_t)nt;
-        auto piece = [&](int64_t a, int64_t b) {
-          if (pitch_ == row_bytes_) {
-            std::memcpy(pin + a * row_bytes_, src_ + (r0 + a) * pitch_, (size_t)((b - a) * row_bytes_));
-          } else {
-            for (int64_t r = a; r < b; ++r)
-              std::memcpy(pin + r * row_bytes_, src_ + (r0 + r) * pitch_, (size_t)row_bytes_);
-          }
-        };
-        std::vector<std::thread> th;
-        for (int64_t a = per; a < rows; a += per) {
-          const int64_t b = std::min(rows, a + per);
-          try {
-            th.emplace_back(piece, a, b);
-          } catch (...) {
-            piece(a, b);
-          }
+        {
+          std::lock_guard<std::mutex> lk(pm_);
+          pin_ = static_cast<char*>(c_.h2d_pin[slot]);
+          r0_ = r0;
+          rows_ = rows;
+          done_ = 0;
+          ++gen_;
         }
-        piece(0, std::min(rows, per));
-        for (auto& t : th) t.join();
-        HSVD_CUDA(cudaMemcpyAsync(dst_ + r0 * row_bytes_, pin, (size_t)(rows * row_bytes_),
+        pcv_.notify_all();
+        piece(0);
+        {
+          std::unique_lock<std::mutex> lk(pm_);
+          pcv_.wait(lk, [&] { return done_ + 1 >= nt_; });
+        }
+        HSVD_CUDA(cudaMemcpyAsync(dst_ + r0 * row_bytes_, c_.h2d_pin[slot], (size_t)(rows * row_bytes_),
                                   cudaMemcpyHostToDevice, cs));
         HSVD_CUDA(cudaEventRecord(c_.h2d_ev[slot], cs));
         HSVD_CUDA(cudaEventRecord(evs_[i], cs));
@@ -176,6 +217,16 @@ class PageableStager final : public HostStager {
   size_t issued_ = 0;
   bool failed_ = false;
   std::string why_;
+  // copy pool
+  std::vector<std::thread> pool_;
+  size_t nt_ = 1;
+  std::mutex pm_;
+  std::condition_variable pcv_;
+  uint64_t gen_ = 0;
+  size_t done_ = 0;
+  bool quit_ = false;
+  char* pin_ = nullptr;
+  int64_t r0_ = 0, rows_ = 0;
 };
 
 bool is_pageable(const void* p) {
