@@ -383,6 +383,11 @@ void gemm_grouped(Ctx& ctx, DType ta, DType tb, bool trans_a, bool trans_b, bool
     maxK = std::max(maxK, d.K);
   }
   if (live.empty()) return;
+  if (ta == DType::F64 && tb == DType::F64 && !trans_a && !trans_b && !syrk &&
+      gemm_sk_applicable(live, ctx.num_sms)) {
+    gemm_sk(ctx, live);
+    return;
+  }
   const int count = static_cast<int>(live.size());
   if (count > 65535) throw Error(kInvalid, "gemm_grouped: too many groups");
   const bool skinny = !syrk && maxN <= 32;

@@ -32,4 +32,10 @@ enum : int {
 void gemm_grouped(Ctx& ctx, DType ta, DType tb, bool trans_a, bool trans_b, bool syrk,
                   const std::vector<GemmDesc>& descs, int flags = 0);
 
+// Skinny fp64 GEMM (N <= 32, no transposes) fed by cp.async.bulk (gemm_sk.cu);
+// gemm_grouped routes to it when the operands allow 16-byte bulk copies and
+// the grid is large enough without split-K (HSVD_GEMM_SK=0 disables).
+bool gemm_sk_applicable(const std::vector<GemmDesc>& descs, int num_sms);
+void gemm_sk(Ctx& ctx, const std::vector<GemmDesc>& descs);
+
 }  // namespace hsvdcu
