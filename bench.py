@@ -328,10 +328,13 @@ def ozaki_roofline(prof, steps, torch, dev):
 
 
 def kernel_families(prof):
-    """{kernel name: (launches, ms, flops)} summed over phases."""
+    """{kernel name: (launches, ms, flops)} summed over phases (the grouped
+    DMMA GEMM and its bulk-copy-fed skinny variant form one family)."""
     fam = {}
     for key, (cnt, ms, fl) in prof.items():
         k = key.rsplit(":", 1)[-1]
+        if k == "k_gemm_sk":
+            k = "k_gemm"
         c0, m0, f0 = fam.get(k, (0, 0.0, 0.0))
         fam[k] = (c0 + cnt, m0 + ms, f0 + fl)
     return fam
@@ -363,7 +366,8 @@ def roofline(prof, steps, w, hbm_peak, fp64_peak):
     if name == "k_gemm" and fl > 0:
         peak = fp64_peak()
         achieved = fl / (ms / 1000.0) / 1e12
-        return {"kernel": "k_gemm (all launches)", "bound": "tensor", "achieved": achieved,
+        return {"kernel": "k_gemm + k_gemm_sk (all DMMA GEMM launches)", "bound": "tensor",
+                "achieved": achieved,
                 "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                 "traffic": traffic, "traffic_unit": "bytes per launch",
                 "peak_source": "fp64 cuBLAS DGEMM 8192^3 measured in this run",
