@@ -80,6 +80,7 @@ int guarded(F&& f) {
 void begin(hsvd_cu_ctx* ctx) {
   if (!ctx) throw Error(kInvalid, "null context");
   HSVD_CUDA(cudaSetDevice(ctx->c.device));
+  ctx->c.nvtx_close();
   ctx->c.arena.reset();
   ++ctx->generation;
 }

@@ -15,6 +15,8 @@
 #include <utility>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "common.cuh"
 
 namespace hsvdcu {
@@ -300,7 +302,22 @@ struct Ctx {
     HSVD_CUDA(cudaEventCreate(&e));
     return e;
   }
+  // NVTX: one range per phase ("leaf.gram", "leaf.eig", "merge.eig", ...),
+  // opened lazily at the phase's first launch and closed at the next phase
+  // or the next API call (header-only NVTX3: a no-op without a tool)
+  const char* nvtx_open = nullptr;
+  void nvtx_phase() {
+    if (phase == nvtx_open) return;
+    if (nvtx_open) nvtxRangePop();
+    nvtxRangePushA(phase && *phase ? phase : "hsvd");
+    nvtx_open = phase;
+  }
+  void nvtx_close() {
+    if (nvtx_open) nvtxRangePop();
+    nvtx_open = nullptr;
+  }
   void launch_begin() {
+    nvtx_phase();
     if (!profiling) return;
     pending = get_event();
     HSVD_CUDA(cudaEventRecord(pending, stream));

@@ -444,6 +444,14 @@ __device__ __forceinline__ bool chase_step(double* bb, int c, int r0, int L, int
   return true;
 }
 
+// (Measured, round 2: an L2 evict_last policy on every band store and
+// step-ahead copy -- createpolicy + st.global.L2::cache_hint, reflectors
+// evict-first -- cut config 2's chase DRAM writes from 13.8 to 3.6 GB (2.1x
+// the 1.7 GB reflector payload) but cost 5% at config 2 (39.1 -> 41.2 ms,
+// extra register spills) and 14% at config 5 (294 -> 334 ms, where the
+// 566 MB of bands cannot stay in L2 anyway); the chase is bound by step
+// latency, not DRAM, so the hints are not used.)
+//
 // The sweeps of one matrix run on a cluster of CS CTAs (CS * CHASE_WARPS
 // warps; sweep s on global warp s mod (CS * CHASE_WARPS)).  Progress flags
 // live in each CTA's shared memory and are polled through DSMEM; with CS > 1
