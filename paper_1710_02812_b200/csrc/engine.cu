@@ -196,7 +196,9 @@ std::vector<DFac> block_svd_batch(Ctx& ctx, const XView& x, const std::vector<Bl
       gemm_grouped(ctx, x.dt, x.dt, true, false, true, gw);
       prev = c.row_end;
     }
-    x_wait_rows(ctx, x);  // everything after reads any row
+    long long row_end = 0;  // everything after reads any row of these blocks
+    for (const Block& bl : blocks) row_end = std::max<long long>(row_end, bl.r0 + bl.d);
+    x_wait_rows(ctx, x, row_end);
   }
   ctx.phase = "leaf.eig";
   eig_topk(ctx, ej);
@@ -480,6 +482,12 @@ DFac svd_of_col_slices(Ctx& ctx, const XView& x, long long c, double gamma, int 
   std::vector<DFac> leaves = block_svd_batch(ctx, x, blocks, gamma, cap, false, false);
   return tree_merge_many(ctx, {leaves}, gamma, cap, nullptr).front();
 }
+
+// (Measured, round 2: running the leaves in two halves by row slices when
+// the input arrives from the host, so the first half's eigensolver overlaps
+// the second half's transfer, did not pay at config 5 -- e2e 2414 -> 2442 ms
+// pinned: the second half's Grams, which overlapped the transfer before,
+// then run alone.)
 
 DFac hierarchical_svd(Ctx& ctx, const XView& x, const HsvdConfig& cfg) {
   auto rows = partition(x.m, cfg.d);
