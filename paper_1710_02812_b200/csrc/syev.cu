@@ -446,8 +446,35 @@ __device__ __forceinline__ int sturm_count_less(const double* dd, const double* 
   return cnt;
 }
 
+// The same count with q_{i-1}^-1 from the hardware reciprocal seed refined
+// by Newton steps instead of the IEEE division sequence: each operation
+// still carries a relative error of a few ulps, which is all the backward
+// stability of the Sturm count needs (Kahan; dstebz's analysis).
+__device__ __forceinline__ double fast_rcp(double q) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
+  double e = fma(-q, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-q, r, 1.0);
+  r = fma(r, e, r);
+  return r;
+}
+__device__ __forceinline__ int sturm_count_less_rcp(const double* dd, const double* e2, int n,
+                                                    double x, double pivmin) {
+  double q = dd[0] - x;
+  if (fabs(q) < pivmin) q = -pivmin;
+  int cnt = q < 0.0;
+  for (int i = 1; i < n; ++i) {
+    q = (dd[i] - x) - e2[i - 1] * fast_rcp(q);
+    if (fabs(q) < pivmin) q = -pivmin;
+    cnt += q < 0.0;
+  }
+  return cnt;
+}
 
-__global__ void __launch_bounds__(EIG_THREADS) k_steig(const EigDev* __restrict__ jobs) {
+
+__global__ void __launch_bounds__(EIG_THREADS) k_steig(const EigDev* __restrict__ jobs, int pforce,
+                                                       int flags) {
   const EigDev J = jobs[blockIdx.x];
   const int n = J.n, kk = J.kk;
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -500,7 +527,15 @@ __global__ void __launch_bounds__(EIG_THREADS) k_steig(const EigDev* __restrict_
   // eigenvalue (P = 1 is bisection), so the sequential Sturm counts per
   // eigenvalue drop from ~52 to ~52 / log2(P + 1)
   {
-    const int P = max(1, nt / kk);
+    const int P = max(1, pforce > 0 ? min(pforce, nt / kk) : nt / kk);
+    const bool rcpc = flags & 1;
+    // flags & 2: dstebz's criterion with ABSTOL <= 0 -- converged once the
+    // bracket is below max(ulp |T|, 2 ulp |lambda|) -- instead of relative
+    // accuracy for every eigenvalue (experiment only, see launch_steig)
+    const double atol = (flags & 2) ? eps * tnorm : 0.0;
+    auto count = [&](double x) {
+      return rcpc ? sturm_count_less_rcp(dd, e2, n, x, pivmin) : sturm_count_less(dd, e2, n, x, pivmin);
+    };
     double* blo = dots;  // [kk] bracket (the dots scratch is free here)
     double* bhi = shift;
     int* cnt = reinterpret_cast<int*>(cstart);  // [kk * P] (cstart is set later)
@@ -514,11 +549,11 @@ __global__ void __launch_bounds__(EIG_THREADS) k_steig(const EigDev* __restrict_
         const int idx = n - 1 - t;
         double lo = blo[t], hi = bhi[t];
         for (int it = 0; it < 256; ++it) {
-          const double tol = 2.0 * eps * fmax(fabs(lo), fabs(hi)) + 4.0 * pivmin;
+          const double tol = fmax(atol, 2.0 * eps * fmax(fabs(lo), fabs(hi))) + 4.0 * pivmin;
           if (hi - lo <= tol) break;
           const double mid = 0.5 * (lo + hi);
           if (mid <= lo || mid >= hi) break;
-          if (sturm_count_less(dd, e2, n, mid, pivmin) > idx) hi = mid;
+          if (count(mid) > idx) hi = mid;
           else lo = mid;
         }
         lam[t] = 0.5 * (lo + hi);
@@ -531,10 +566,10 @@ __global__ void __launch_bounds__(EIG_THREADS) k_steig(const EigDev* __restrict_
         double x = 0.0;
         if (mine) {
           const double lo = blo[t], hi = bhi[t];
-          const double tol = 2.0 * eps * fmax(fabs(lo), fabs(hi)) + 4.0 * pivmin;
+          const double tol = fmax(atol, 2.0 * eps * fmax(fabs(lo), fabs(hi))) + 4.0 * pivmin;
           x = lo + (hi - lo) * (double)(g + 1) / (double)(P + 1);
           active = hi - lo > tol && x > lo && x < hi;
-          cnt[t * P + g] = active ? sturm_count_less(dd, e2, n, x, pivmin) : -1;
+          cnt[t * P + g] = active ? count(x) : -1;
         }
         if (!__syncthreads_or(active)) break;
         if (mine && g == 0) {
@@ -598,6 +633,7 @@ __global__ void __launch_bounds__(EIG_THREADS) k_steig(const EigDev* __restrict_
     return;
   }
   const double tiny = eps * tnorm;
+  const bool rcpi = flags & 4;  // the solves' divisions through fast_rcp too
   // The iterates and pivots live in the scratch J.piv in row-major [n][kk]
   // layout: thread t walks its vector row by row, so a warp's accesses to
   // one row are coalesced.  They stream through registers IC rows at a time,
@@ -636,7 +672,7 @@ __global__ void __launch_bounds__(EIG_THREADS) k_steig(const EigDev* __restrict_
         for (int j = 0; j < IC; ++j) {
           const int r = r0 + j;
           if (r < n) {
-            const double l = ee[r - 1] / D;
+            const double l = rcpi ? ee[r - 1] * fast_rcp(D) : ee[r - 1] / D;
             D = guard_pivot(dd[r] - s - l * ee[r - 1], tiny);
             cd[j] = D;
             y = cz[j] - l * y;
@@ -675,7 +711,7 @@ __global__ void __launch_bounds__(EIG_THREADS) k_steig(const EigDev* __restrict_
         for (int j = 0; j < IC; ++j) {
           const int r = r0 - j;
           if (r >= 0) {
-            zr = (cz[j] - ee[r] * zr) / cd[j];
+            zr = rcpi ? (cz[j] - ee[r] * zr) * fast_rcp(cd[j]) : (cz[j] - ee[r] * zr) / cd[j];
             cz[j] = zr;
             nrm2 += zr * zr;
           }
@@ -1064,7 +1100,18 @@ void launch_steig(Ctx& ctx, const EigDev* dd, int count, int nmax, int kkmax) {
     const size_t smem = steig_smem(nmax, kkmax, steig_global_tri(nmax, kkmax));
     smem_optin(k_steig, smem);
     ctx.launch_begin();
-    k_steig<<<count, EIG_THREADS, smem, ctx.stream>>>(dd);
+    // flags: 1 Sturm counts through fast_rcp, 4 the inverse-iteration solves
+    // through fast_rcp (measured round 2: config 5 k_steig 49.5 + 19.7 ->
+    // 34.0 + 13.3 ms with 1; P = 1 bisection instead of the 2-point
+    // multisection was slower: 62.8 + 25.6 ms).  2, dstebz's absolute
+    // tolerance ulp |T| (30.0 + 11.1 ms), is not used: the retained tail of a
+    // leaf can hold eigenvalues ~1e-14 |T| whose shifts then lose the digits
+    // inverse iteration needs to separate them (config-5 stand-in: sigma off
+    // by 1.5e-3 against the oracle).
+    int pforce = 0, flags = 5;
+    if (const char* e = std::getenv("HSVD_STEIG_P")) pforce = std::atoi(e);
+    if (const char* e = std::getenv("HSVD_STEIG_FLAGS")) flags = std::atoi(e);
+    k_steig<<<count, EIG_THREADS, smem, ctx.stream>>>(dd, pforce, flags);
     ctx.check_launch("k_steig");
 }
 
