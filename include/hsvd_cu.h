@@ -92,8 +92,9 @@ int64_t hsvd_cu_launch_count(const hsvd_cu_ctx* ctx);
 int64_t hsvd_cu_arena_bytes(const hsvd_cu_ctx* ctx);
 int hsvd_cu_synchronize(hsvd_cu_ctx* ctx);
 /* Per-launch CUDA-event timing of this library's kernels (for benchmarks).
- * report: "phase[/sub]:kernel\tlaunches\ttotal_ms\tflops\n" lines since the
- * last report (flops: algorithmic flops of the GEMM launches, else 0);
+ * report: "phase[/sub]:kernel\tlaunches\ttotal_ms\tflops\tbytes\n" lines
+ * since the last report (flops: algorithmic flops of the GEMM launches, else
+ * 0; bytes: algorithmic HBM bytes of the factor-streaming launches, else 0);
  * returns the bytes needed (including the NUL), or -1 on error. */
 int hsvd_cu_profile(hsvd_cu_ctx* ctx, int enable);
 int64_t hsvd_cu_profile_report(hsvd_cu_ctx* ctx, char* buf, int64_t len);

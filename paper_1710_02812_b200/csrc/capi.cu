@@ -548,7 +548,7 @@ int64_t hsvd_cu_profile_report(hsvd_cu_ctx* ctx, char* buf, int64_t len) {
     HSVD_CUDA(cudaStreamSynchronize(c.stream));
     std::vector<std::string> order;
     std::vector<std::pair<long long, double>> agg;
-    std::vector<double> fl;
+    std::vector<double> fl, by;
     for (auto& r : c.prof) {
       float ms = 0.f;
       HSVD_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
@@ -558,10 +558,12 @@ int64_t hsvd_cu_profile_report(hsvd_cu_ctx* ctx, char* buf, int64_t len) {
         order.push_back(r.name);
         agg.push_back({0, 0.0});
         fl.push_back(0.0);
+        by.push_back(0.0);
       }
       agg[i].first += 1;
       agg[i].second += ms;
       fl[i] += r.flops;
+      by[i] += r.bytes;
     }
     if (buf && len > 0) {  // a sizing query (buf == NULL) keeps the records
       for (auto& r : c.prof) {
@@ -572,7 +574,7 @@ int64_t hsvd_cu_profile_report(hsvd_cu_ctx* ctx, char* buf, int64_t len) {
     }
     for (size_t i = 0; i < order.size(); ++i)
       out += order[i] + "\t" + std::to_string(agg[i].first) + "\t" + std::to_string(agg[i].second) +
-             "\t" + std::to_string(fl[i]) + "\n";
+             "\t" + std::to_string(fl[i]) + "\t" + std::to_string(by[i]) + "\n";
     return HSVD_CU_OK;
   });
   if (rc != HSVD_CU_OK) return -1;

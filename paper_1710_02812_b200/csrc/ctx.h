@@ -86,6 +86,12 @@ class Arena {
     for (auto& c : chunks_) u += c.size;
     return u;
   }
+  void swap(Arena& o) {
+    chunks_.swap(o.chunks_);
+    std::swap(cur_, o.cur_);
+    std::swap(off_, o.off_);
+    std::swap(peak_, o.peak_);
+  }
   void free_all() {
     for (auto& c : chunks_) cudaFree(c.ptr);
     chunks_.clear();
@@ -138,6 +144,8 @@ class Staging {
     if (b > size_) throw Error(kInvalid, "staging ring too small");
     if (off_ + b > size_) {
       HSVD_CUDA(cudaStreamSynchronize(s));  // all earlier copies consumed
+      for (cudaStream_t o : other_)
+        if (o && o != s) HSVD_CUDA(cudaStreamSynchronize(o));
       off_ = 0;
     }
     char* h = static_cast<char*>(host_) + off_;
@@ -151,7 +159,15 @@ class Staging {
     return d;
   }
 
+  // the two streams whose launches read the ring once a side stream exists
+  // (Ctx::side_begin): a wrap waits for both
+  void also_sync(cudaStream_t a, cudaStream_t b) {
+    other_[0] = a;
+    other_[1] = b;
+  }
+
  private:
+  cudaStream_t other_[2] = {nullptr, nullptr};
   void* host_ = nullptr;
   void* host_dev_ = nullptr;  // device address of host_
   void* dev_ = nullptr;
@@ -255,7 +271,50 @@ struct Ctx {
     }
     return chunk_ev[i];
   }
+  // Side compute stream: independent launches of one call (the back-
+  // transform's T factors, the chase's WY blocks) run there while the
+  // latency-bound kernels of the main stream leave SMs idle.  side_begin()
+  // makes the side stream wait for everything queued on the main stream so
+  // far and routes the following launches to it; side_end() routes back;
+  // side_join() makes the main stream wait for the side stream.  The arena's
+  // mark/release reuse is ordered by ONE stream, so the side launches take
+  // their workspaces from an arena of their own (stack discipline per scope;
+  // the side stream is in-order, so reuse across scopes is safe too).
+  // Results the main stream reads after the join must be allocated outside.
+  Arena side_arena;
+  Arena::Mark side_mark{};
+  cudaStream_t side_stream = nullptr, main_saved = nullptr;
+  cudaEvent_t side_ev[2] = {nullptr, nullptr};
+  void side_begin() {
+    if (!side_stream) {
+      HSVD_CUDA(cudaStreamCreateWithFlags(&side_stream, cudaStreamNonBlocking));
+      for (auto& e : side_ev) HSVD_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    staging.also_sync(stream, side_stream);
+    HSVD_CUDA(cudaEventRecord(side_ev[0], stream));
+    HSVD_CUDA(cudaStreamWaitEvent(side_stream, side_ev[0], 0));
+    main_saved = stream;
+    stream = side_stream;
+    arena.swap(side_arena);
+    side_mark = arena.mark();
+  }
+  void side_end() {
+    arena.release(side_mark);
+    arena.swap(side_arena);
+    stream = main_saved;
+    main_saved = nullptr;
+  }
+  void side_join() {
+    if (!side_stream) return;
+    HSVD_CUDA(cudaEventRecord(side_ev[1], side_stream));
+    HSVD_CUDA(cudaStreamWaitEvent(stream, side_ev[1], 0));
+  }
   ~Ctx() {
+    if (side_stream) {
+      cudaStreamSynchronize(side_stream);
+      cudaStreamDestroy(side_stream);
+      for (auto e : side_ev) cudaEventDestroy(e);
+    }
     for (auto e : chunk_ev) cudaEventDestroy(e);
     if (copy_stream) {
       cudaStreamSynchronize(copy_stream);
@@ -283,8 +342,10 @@ struct Ctx {
     std::string name;
     cudaEvent_t a, b;
     double flops;  // algorithmic flops of the launch (GEMMs), else 0
+    double bytes;  // algorithmic HBM bytes of the launch (factor streaming kernels), else 0
   };
   double pending_flops = 0.0;
+  double pending_bytes = 0.0;
   bool profiling = false;
   const char* phase = "";
   const char* sub = nullptr;  // optional sub-phase inside a phase (profile key phase/sub)
@@ -340,10 +401,11 @@ struct Ctx {
       cudaEvent_t b = get_event();
       HSVD_CUDA(cudaEventRecord(b, stream));
       prof.push_back({std::string(phase) + (sub ? std::string("/") + sub : std::string()) + ":" + what,
-                      pending, b, pending_flops});
+                      pending, b, pending_flops, pending_bytes});
       pending = nullptr;
     }
     pending_flops = 0.0;
+    pending_bytes = 0.0;
   }
 };
 
@@ -352,6 +414,13 @@ struct PhaseScope {
   const char* prev;
   PhaseScope(Ctx& ctx, const char* p) : c(ctx), prev(ctx.phase) { c.phase = p; }
   ~PhaseScope() { c.phase = prev; }
+};
+
+// Routes the launches of a scope to the side stream (exception-safe).
+struct SideScope {
+  Ctx& c;
+  explicit SideScope(Ctx& ctx) : c(ctx) { c.side_begin(); }
+  ~SideScope() { c.side_end(); }
 };
 
 struct SubPhase {

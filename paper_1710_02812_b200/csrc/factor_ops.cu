@@ -360,6 +360,9 @@ int grid_for(long long elems) {
 void finalize(Ctx& ctx, const std::vector<FinJob>& jobs) {
   if (jobs.empty()) return;
   int pmax = 0, chmax = 1, smax = 1;
+  // algorithmic HBM bytes (profile): the norms read P once; the gather reads
+  // and writes the written columns (min(p, cap), all p with write_all)
+  double norm_bytes = 0.0, gather_bytes = 0.0;
   std::vector<FinDev> dev(jobs.size());
   for (size_t i = 0; i < jobs.size(); ++i) {
     FinDev& f = dev[i];
@@ -372,10 +375,13 @@ void finalize(Ctx& ctx, const std::vector<FinJob>& jobs) {
     pmax = std::max(pmax, f.j.p);
     chmax = std::max(chmax, f.nchunk);
     smax = std::max(smax, f.j.s);
+    if (!f.j.norms2) norm_bytes += 8.0 * f.j.s * f.j.p;
+    gather_bytes += 16.0 * f.j.s * ((f.j.write_all || f.j.cap <= 0) ? f.j.p : std::min(f.j.p, f.j.cap));
   }
   const FinDev* dd = stage(ctx, dev);
   const unsigned nj = (unsigned)dev.size();
   ctx.launch_begin();
+  ctx.pending_bytes = norm_bytes;
   k_colnorm_part<<<dim3(chmax, pmax, nj), 256, 0, ctx.stream>>>(dd);
   ctx.check_launch("k_colnorm_part");
   const size_t smem = 2 * (size_t)pmax * sizeof(double) + (size_t)pmax * sizeof(int) + 64;
@@ -385,6 +391,7 @@ void finalize(Ctx& ctx, const std::vector<FinJob>& jobs) {
   ctx.check_launch("k_finalize");
   const int gx = std::min(ceil_div(smax, 256 * 4), 64);
   ctx.launch_begin();
+  ctx.pending_bytes = gather_bytes;
   k_scale_gather<<<dim3(gx, pmax, nj), 256, 0, ctx.stream>>>(dd);
   ctx.check_launch("k_scale_gather");
   const size_t smem2 = ((size_t)pmax + 32) * sizeof(double) + (size_t)pmax * sizeof(int) + 64;
@@ -406,8 +413,13 @@ void scale_sym(Ctx& ctx, const std::vector<ScaleSymJob>& jobs) {
 void scale_rows(Ctx& ctx, const std::vector<ScaleRowsJob>& jobs) {
   if (jobs.empty()) return;
   long long mx = 0;
-  for (auto& j : jobs) mx = std::max(mx, (long long)j.rows * j.cols);
+  double bytes = 0.0;
+  for (auto& j : jobs) {
+    mx = std::max(mx, (long long)j.rows * j.cols);
+    bytes += 16.0 * j.rows * j.cols;
+  }
   ctx.launch_begin();
+  ctx.pending_bytes = bytes;
   k_scale_rows<<<dim3(grid_for(mx), (unsigned)jobs.size()), 256, 0, ctx.stream>>>(stage(ctx, jobs));
   ctx.check_launch("k_scale_rows");
 }
@@ -415,8 +427,13 @@ void scale_rows(Ctx& ctx, const std::vector<ScaleRowsJob>& jobs) {
 void gather_cols(Ctx& ctx, const std::vector<GatherJob>& jobs) {
   if (jobs.empty()) return;
   long long mx = 0;
-  for (auto& j : jobs) mx = std::max(mx, (long long)j.rows * j.cols);
+  double bytes = 0.0;
+  for (auto& j : jobs) {
+    mx = std::max(mx, (long long)j.rows * j.cols);
+    bytes += 16.0 * j.rows * j.cols;
+  }
   ctx.launch_begin();
+  ctx.pending_bytes = bytes;
   k_gather<<<dim3(grid_for(mx), (unsigned)jobs.size()), 256, 0, ctx.stream>>>(stage(ctx, jobs));
   ctx.check_launch("k_gather");
 }

@@ -545,10 +545,16 @@ PlaneSet slice_cols(Ctx& ctx, std::vector<OzLeaf>& src, long long kpad) {
   OzLeaf* dl = stage_table(ctx, src);
   HSVD_CUDA(cudaMemsetAsync(cmax, 0, (size_t)ps.plane_rows * sizeof(unsigned), ctx.stream));
   const int rpb = 256;
+  // algorithmic HBM bytes (profile): the max pass reads the fp32 block once;
+  // the split reads it again and writes kS int8 digit planes
+  double elems = 0.0;
+  for (const auto& l : src) elems += (double)l.K * l.q;
   ctx.launch_begin();
+  ctx.pending_bytes = 4.0 * elems;
   k_oz_colmax<<<dim3(ceil_div(max_qp, 256), ceil_div(Kmax, rpb), nl), 256, 0, ctx.stream>>>(dl, rpb);
   ctx.check_launch("k_oz_colmax");
   ctx.launch_begin();
+  ctx.pending_bytes = (4.0 + kS) * elems;
   k_oz_split<<<dim3((unsigned)(kpad / 128), max_qp / 32, nl), 256, 0, ctx.stream>>>(
       dl, ps.planes, kpad, ps.plane_rows);
   ctx.check_launch("k_oz_split");
@@ -574,10 +580,17 @@ PlaneSet slice_rows(Ctx& ctx, std::vector<OzRows>& src, long long kpad) {
   ps.planes = ctx.arena.alloc_n<signed char>((size_t)(kS * ps.plane_rows * kpad));
   const int ns = static_cast<int>(src.size());
   OzRows* ds = stage_table(ctx, src);
+  double in_bytes = 0.0, elems = 0.0;  // algorithmic HBM bytes, as in slice_cols
+  for (const auto& r : src) {
+    in_bytes += (r.f64 ? 8.0 : 4.0) * r.rows * r.K;
+    elems += (double)r.rows * r.K;
+  }
   ctx.launch_begin();
+  ctx.pending_bytes = in_bytes;
   k_oz_rowmax<<<dim3(ceil_div(max_rows, 8), ns), 256, 0, ctx.stream>>>(ds);
   ctx.check_launch("k_oz_rowmax");
   ctx.launch_begin();
+  ctx.pending_bytes = in_bytes + kS * elems;
   k_oz_split_rows<<<dim3((unsigned)(kpad / 128), ceil_div(max_rows, 8), ns), 256, 0, ctx.stream>>>(
       ds, ps.planes, kpad, ps.plane_rows);
   ctx.check_launch("k_oz_split_rows");

@@ -1023,8 +1023,10 @@ bool use_two_stage(int nmax, int count) {
 
 // Z <- Q Z with Q = H_0 H_1 ... (reflector of column j: unit at row j + off,
 // stored in A column j), in compact-WY blocks of NBT reflectors.
-void back_transform(Ctx& ctx, const std::vector<EigJob>& jobs, const std::vector<EigDev>& dev,
-                    const EigDev* dd, int nmax, int off) {
+// The reflector-only part of the back-transform (explicit V, S = V^T V and
+// the T factors of the WY blocks): independent of the eigenvectors, so the
+// two-stage driver runs it on the side stream under the bulge chase.
+void back_prepare(Ctx& ctx, const std::vector<EigDev>& dev, const EigDev* dd, int nmax, int off) {
   const int count = static_cast<int>(dev.size());
   if (nmax <= off + 1) return;
   const long long nn = (long long)nmax * nmax;
@@ -1050,6 +1052,14 @@ void back_transform(Ctx& ctx, const std::vector<EigJob>& jobs, const std::vector
   ctx.launch_begin();
   k_build_t<<<dim3(nblk_max, count), NBT, tsm, ctx.stream>>>(dd, off);
   ctx.check_launch("k_build_t");
+}
+
+// Z <- Q Z through the WY blocks prepared by back_prepare (last block first).
+void back_apply(Ctx& ctx, const std::vector<EigJob>& jobs, const std::vector<EigDev>& dev,
+                int nmax, int off) {
+  const int count = static_cast<int>(dev.size());
+  if (nmax <= off + 1) return;
+  const int nblk_max = ceil_div(nmax - off, NBT);
   std::vector<double*> W(count), W2(count);
   for (int g = 0; g < count; ++g) {
     W[g] = ctx.arena.alloc_n<double>((size_t)NBT * jobs[g].kk);
@@ -1079,6 +1089,12 @@ void back_transform(Ctx& ctx, const std::vector<EigJob>& jobs, const std::vector
     gemm_grouped(ctx, DType::F64, DType::F64, false, false, false, d2);
     gemm_grouped(ctx, DType::F64, DType::F64, false, false, false, d3);
   }
+}
+
+void back_transform(Ctx& ctx, const std::vector<EigJob>& jobs, const std::vector<EigDev>& dev,
+                    const EigDev* dd, int nmax, int off) {
+  back_prepare(ctx, dev, dd, nmax, off);
+  back_apply(ctx, jobs, dev, nmax, off);
 }
 
 // The job array is read by every launch of the solver, so it lives in arena

@@ -1331,6 +1331,17 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
     for (int g = 0; g < count; ++g)
       HSVD_CUDA(cudaMemcpyAsync(dev[g].band0, dev[g].band, (size_t)LDBB * dev[g].n * sizeof(double),
                                 cudaMemcpyDeviceToDevice, ctx.stream));
+  // The chase, the tridiagonal eigensolver and the cluster Gram-Schmidt are
+  // latency-bound and leave SMs idle (one CTA per matrix: 256 CTAs on 148 SMs
+  // at config 5, 128 at configs 2-4), so the work that depends only on the
+  // reflectors runs beside them on the side stream: the stage-1 WY factors
+  // of the back-transform now, the chase's WY blocks once the chase is done.
+  const bool side = !(std::getenv("HSVD_NO_SIDE") && std::atoi(std::getenv("HSVD_NO_SIDE")) != 0);
+  if (side) {
+    SideScope ss(ctx);
+    SubPhase spb(ctx, "back");
+    back_prepare(ctx, dev, dd, nmax, B2);
+  }
   // stage 2: band -> tridiagonal (values), eigenvalues by bisection
   SubPhase sp2(ctx, "tri");
   ctx.launch_begin();
@@ -1362,17 +1373,25 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
     HSVD_CUDA(cudaLaunchKernelEx(&cfg, k_chase<true>, dd, ccs));
   }
   ctx.check_launch("k_chase");
+  auto tbuild = [&] {
+    ctx.launch_begin();
+    const long long tmax = tblk_off(nmax, chase_steps(nmax));
+    const int tbx = std::max(1, std::min(ceil_div(tmax, TB_WARPS), ceil_div(8 * ctx.num_sms, count)));
+    k_q2_tbuild<<<dim3(tbx, count), TB_WARPS * 32, 0, ctx.stream>>>(dd);
+    ctx.check_launch("k_q2_tbuild");
+  };
+  if (side && !band_invit) {  // after the chase, beside k_steig / k_band_mgs
+    SideScope ss(ctx);
+    tbuild();
+  }
   launch_steig(ctx, dd, count, nmax, kkmax);
   // eigenvectors of the band matrix
   if (!band_invit) {
     launch_band_mgs(ctx, dd, dev);  // clusters of the tridiagonal's vectors
-    ctx.launch_begin();
-    {
-      const long long tmax = tblk_off(nmax, chase_steps(nmax));
-      const int tbx = std::max(1, std::min(ceil_div(tmax, TB_WARPS), ceil_div(8 * ctx.num_sms, count)));
-      k_q2_tbuild<<<dim3(tbx, count), TB_WARPS * 32, 0, ctx.stream>>>(dd);
-      ctx.check_launch("k_q2_tbuild");
-    }
+    if (side)
+      ctx.side_join();
+    else
+      tbuild();
     ctx.launch_begin();
     {  // algorithmic flops: 4 * 32 * kk per stored reflector
       double fl = 0.0;
@@ -1390,10 +1409,12 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
     k_band_invit<<<dim3(cpm, count), INV_WARPS * 32, smem, ctx.stream>>>(dd);
     ctx.check_launch("k_band_invit");
     launch_band_mgs(ctx, dd, dev);
+    if (side) ctx.side_join();
   }
   // back through the stage-1 reflectors
   SubPhase sp3(ctx, "back");
-  back_transform(ctx, jobs, dev, dd, nmax, B2);
+  if (!side) back_prepare(ctx, dev, dd, nmax, B2);
+  back_apply(ctx, jobs, dev, nmax, B2);
 }
 
 }  // namespace syev_impl

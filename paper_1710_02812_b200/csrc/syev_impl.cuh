@@ -115,6 +115,9 @@ void launch_steig(Ctx& ctx, const EigDev* dd, int count, int nmax, int kkmax);
 // k_band_mgs: orthonormalise the vectors of every eigenvalue cluster in Z
 void launch_band_mgs(Ctx& ctx, const EigDev* dd, const std::vector<EigDev>& dev);
 // Z <- Q Z through the reflectors stored in A (unit at row j + off)
+void back_prepare(Ctx& ctx, const std::vector<EigDev>& dev, const EigDev* dd, int nmax, int off);
+void back_apply(Ctx& ctx, const std::vector<EigJob>& jobs, const std::vector<EigDev>& dev, int nmax,
+                int off);
 void back_transform(Ctx& ctx, const std::vector<EigJob>& jobs, const std::vector<EigDev>& dev,
                     const EigDev* dd, int nmax, int off);
 // two-stage path of eig_topk (syev_band.cu)

@@ -382,16 +382,21 @@ class Context:
 
     def profile_report(self) -> dict:
         """{'phase[/sub]:kernel': (launches, total_ms, algorithmic_flops)} since
-        the last report (flops counted for the GEMM launches, else 0)."""
+        the last report (flops counted for the GEMM launches, else 0).  The
+        algorithmic HBM bytes the library counts for the factor-streaming
+        kernels (norms, scale/gather, digit-plane splits) are kept in
+        `self.profile_bytes` under the same keys."""
         need = self.lib.hsvd_cu_profile_report(self.handle, None, 0)
         if need < 0:
             _raise(ECUDA)
         buf = C.create_string_buffer(int(need) + 16)
         self.lib.hsvd_cu_profile_report(self.handle, buf, len(buf))
         out = {}
+        self.profile_bytes = {}
         for line in buf.value.decode().splitlines():
-            name, cnt, ms, fl = line.split("\t")
+            name, cnt, ms, fl, by = line.split("\t")
             out[name] = (int(cnt), float(ms), float(fl))
+            self.profile_bytes[name] = float(by)
         return out
 
 
