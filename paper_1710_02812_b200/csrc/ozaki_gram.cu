@@ -112,6 +112,47 @@ struct OzTile {
 // slicing
 // ---------------------------------------------------------------------------
 
+// Digit extraction without the conversion unit: rintf / (int) go through
+// FRND / F2I (16 lanes per clock per SM), which bound the split kernels at
+// ~0.47 of the HBM peak (14 conversions per element).  Adding 1.5 * 2^23
+// rounds v to the nearest-even integer in the mantissa's low bits (|v| < 2^22):
+// d = t - M is rintf(v) exactly, and the low byte of t's bit pattern is d as
+// an int8 -- full-rate FADD + one PRMT per digit, bit-identical digits.
+template <int U>
+__device__ __forceinline__ uint32_t put_byte(uint32_t packed, uint32_t src) {
+  constexpr uint32_t sel = U == 0 ? 0x3214u : U == 1 ? 0x3240u : U == 2 ? 0x3410u : 0x4210u;
+  return __byte_perm(packed, src, sel);
+}
+template <int U>
+__device__ __forceinline__ void oz_digits(float v, uint32_t (&packed)[kS]) {
+  const float M = 12582912.0f;  // 1.5 * 2^23
+#pragma unroll
+  for (int a = 0; a < kS; ++a) {
+    const float t = v + M;
+    const float d = t - M;
+    v = (v - d) * 128.0f;
+    packed[a] = put_byte<U>(packed[a], __float_as_uint(t));
+  }
+}
+template <int U>
+__device__ __forceinline__ void oz_digits(double v, uint32_t (&packed)[kS]) {
+  const double M = 6755399441055744.0;  // 1.5 * 2^52
+#pragma unroll
+  for (int a = 0; a < kS; ++a) {
+    const double t = v + M;
+    const double d = t - M;
+    v = (v - d) * 128.0;
+    packed[a] = put_byte<U>(packed[a], (uint32_t)__double2loint(t));
+  }
+}
+template <typename T>
+__device__ __forceinline__ void oz_digits4(const T (&v)[4], uint32_t (&packed)[kS]) {
+  oz_digits<0>(v[0], packed);
+  oz_digits<1>(v[1], packed);
+  oz_digits<2>(v[2], packed);
+  oz_digits<3>(v[3], packed);
+}
+
 __global__ void k_oz_colmax(const OzLeaf* __restrict__ leaves, int rows_per_block) {
   const OzLeaf L = leaves[blockIdx.z];
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -127,12 +168,23 @@ __global__ void k_oz_colmax(const OzLeaf* __restrict__ leaves, int rows_per_bloc
 
 // One CTA: 128 rows (K) x 32 columns of one leaf -> S planes of 32 rows x 128
 // bytes (K-major).  Thread (tx, ty): column tx, rows 4*ty + 32*rep + 0..3.
+// blockIdx.x walks super-tiles of 8 column tiles x 32 K chunks (column tile
+// fastest): CTAs resident together read 1 KB runs of the same rows and write
+// 4 KB runs of the same plane rows (DRAM page locality on both sides).
 __global__ void __launch_bounds__(256) k_oz_split(const OzLeaf* __restrict__ leaves,
                                                   signed char* __restrict__ planes,
-                                                  long long kpad, long long plane_rows) {
+                                                  long long kpad, long long plane_rows, int ntj) {
   __shared__ uint32_t sw[kS][32][33];
   const OzLeaf L = leaves[blockIdx.z];
-  const int j0 = blockIdx.y * 32, i0 = blockIdx.x * 128;
+  int j0, i0;
+  {
+    const unsigned per_super = 32u * (unsigned)ntj;  // CTAs per band of 32 K chunks
+    const unsigned sup = blockIdx.x / per_super, r = blockIdx.x % per_super;
+    const unsigned cs = r / 256u, r2 = r % 256u;     // 8 x 32 tiles per super-tile
+    j0 = (int)(cs * 8u + (r2 & 7u)) * 32;
+    i0 = (int)(sup * 32u + (r2 >> 3)) * 128;
+    if (i0 >= kpad) return;
+  }
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int q_pad = (L.q + kBN - 1) / kBN * kBN;
   if (j0 >= q_pad) return;
@@ -145,29 +197,28 @@ __global__ void __launch_bounds__(256) k_oz_split(const OzLeaf* __restrict__ lea
       frexpf(m, &e);  // m = f 2^e, f in [0.5, 1): m < 2^e
       inv = ldexpf(1.0f, -e);
     }
-    if (blockIdx.x == 0 && ty == 0) L.scale[j] = m > 0.0f ? ldexp(1.0, e) : 1.0;
-  } else if (blockIdx.x == 0 && ty == 0 && j < q_pad) {
+    if (i0 == 0 && ty == 0) L.scale[j] = m > 0.0f ? ldexp(1.0, e) : 1.0;
+  } else if (i0 == 0 && ty == 0 && j < q_pad) {
     L.scale[j] = 1.0;
   }
+  // all 16 loads of the thread first, then the digit arithmetic
+  float x[4][4];
+#pragma unroll
+  for (int rep = 0; rep < 4; ++rep)
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + ty * 4 + rep * 32 + u;
+      x[rep][u] = (j < L.q && i < L.K) ? __ldg(L.x + (long long)i * L.ld + j) : 0.0f;
+    }
 #pragma unroll
   for (int rep = 0; rep < 4; ++rep) {
     const int r4 = ty * 4 + rep * 32;
     uint32_t packed[kS];
 #pragma unroll
     for (int a = 0; a < kS; ++a) packed[a] = 0u;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int i = i0 + r4 + u;
-      float r = 0.0f;
-      if (j < L.q && i < L.K) r = __ldg(L.x + (long long)i * L.ld + j) * inv;
-      float v = r * 64.0f;
-#pragma unroll
-      for (int a = 0; a < kS; ++a) {
-        const float d = rintf(v);
-        v = (v - d) * 128.0f;
-        packed[a] |= (uint32_t)(uint8_t)(signed char)(int)d << (8 * u);
-      }
-    }
+    const float v[4] = {x[rep][0] * inv * 64.0f, x[rep][1] * inv * 64.0f, x[rep][2] * inv * 64.0f,
+                        x[rep][3] * inv * 64.0f};
+    oz_digits4(v, packed);
 #pragma unroll
     for (int a = 0; a < kS; ++a) sw[a][tx][r4 >> 2] = packed[a];
   }
@@ -186,25 +237,82 @@ __global__ void __launch_bounds__(256) k_oz_split(const OzLeaf* __restrict__ lea
   }
 }
 
-// per-row scale of a row-scaled source: one warp per row, max |x| over K
-__global__ void k_oz_rowmax(const OzRows* __restrict__ srcs) {
+// per-row scale of a row-scaled source: max |x| over K.  One CTA per 8 rows,
+// the whole CTA walking along one row at a time (4 KB per load instruction):
+// with a warp per row, ~9000 rows were streamed at once across the GPU, each
+// from its own DRAM page (0.55 of the HBM peak).
+__global__ void __launch_bounds__(256) k_oz_rowmax(const OzRows* __restrict__ srcs) {
   const OzRows S = srcs[blockIdx.y];
-  const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (row >= S.rows) return;
-  double m = 0.0;
+  const int row0 = blockIdx.x * 8, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (row0 >= S.rows) return;
+  __shared__ double red[8][8];
+  double m[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) m[r] = 0.0;
   if (S.f64) {
-    const double* p = static_cast<const double*>(S.x) + (long long)row * S.ld;
-    for (int k = lane; k < S.K; k += 32) m = fmax(m, fabs(p[k]));
+    // fp64 factors are short (kk rows): a warp per row, four loads in flight
+    if (row0 + warp < S.rows) {
+      const double* p = static_cast<const double*>(S.x) + (long long)(row0 + warp) * S.ld;
+      double a = 0.0, b = 0.0, c = 0.0, d = 0.0;
+      int k = lane;
+      for (; k + 96 < S.K; k += 128) {
+        a = fmax(a, fabs(p[k]));
+        b = fmax(b, fabs(p[k + 32]));
+        c = fmax(c, fabs(p[k + 64]));
+        d = fmax(d, fabs(p[k + 96]));
+      }
+      for (; k < S.K; k += 32) a = fmax(a, fabs(p[k]));
+      double v = fmax(fmax(a, b), fmax(c, d));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+      if (lane == 0) {
+        int e = 0;
+        if (v > 0.0) frexp(v, &e);  // v < 2^e
+        S.scale[row0 + warp] = v > 0.0 ? ldexp(1.0, e) : 1.0;
+      }
+    }
+    return;  // uniform per CTA
   } else {
-    const float* p = static_cast<const float*>(S.x) + (long long)row * S.ld;
-    for (int k = lane; k < S.K; k += 32) m = fmax(m, (double)fabsf(__ldg(p + k)));
+    for (int r = 0; r < 8 && row0 + r < S.rows; ++r) {
+      const float* p = static_cast<const float*>(S.x) + (long long)(row0 + r) * S.ld;
+      float f0 = 0.0f, f1 = 0.0f;
+      int k = tid;
+      if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) {  // 16-byte loads, four in flight
+        const float4* p4 = reinterpret_cast<const float4*>(p);
+        const int K4 = S.K >> 2;
+        int q = tid;
+        for (; q + 768 < K4; q += 1024) {
+          const float4 a = __ldg(p4 + q), b = __ldg(p4 + q + 256), c = __ldg(p4 + q + 512),
+                       d = __ldg(p4 + q + 768);
+          f0 = fmaxf(f0, fmaxf(fmaxf(fabsf(a.x), fabsf(a.y)), fmaxf(fabsf(a.z), fabsf(a.w))));
+          f1 = fmaxf(f1, fmaxf(fmaxf(fabsf(b.x), fabsf(b.y)), fmaxf(fabsf(b.z), fabsf(b.w))));
+          f0 = fmaxf(f0, fmaxf(fmaxf(fabsf(c.x), fabsf(c.y)), fmaxf(fabsf(c.z), fabsf(c.w))));
+          f1 = fmaxf(f1, fmaxf(fmaxf(fabsf(d.x), fabsf(d.y)), fmaxf(fabsf(d.z), fabsf(d.w))));
+        }
+        for (; q < K4; q += 256) {
+          const float4 a = __ldg(p4 + q);
+          f0 = fmaxf(f0, fmaxf(fmaxf(fabsf(a.x), fabsf(a.y)), fmaxf(fabsf(a.z), fabsf(a.w))));
+        }
+        k = (K4 << 2) + tid;  // tail elements
+      }
+      for (; k < S.K; k += 256) f0 = fmaxf(f0, fabsf(__ldg(p + k)));
+      m[r] = (double)fmaxf(f0, f1);
+    }
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if (lane == 0) {
+  for (int r = 0; r < 8; ++r) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m[r] = fmax(m[r], __shfl_xor_sync(0xffffffffu, m[r], o));
+    if (lane == 0) red[warp][r] = m[r];
+  }
+  __syncthreads();
+  if (tid < 8 && row0 + tid < S.rows) {
+    double v = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) v = fmax(v, red[w][tid]);
     int e = 0;
-    if (m > 0.0) frexp(m, &e);  // m < 2^e
-    S.scale[row] = m > 0.0 ? ldexp(1.0, e) : 1.0;
+    if (v > 0.0) frexp(v, &e);  // v < 2^e
+    S.scale[row0 + tid] = v > 0.0 ? ldexp(1.0, e) : 1.0;
   }
 }
 
@@ -221,29 +329,34 @@ __global__ void __launch_bounds__(256) k_oz_split_rows(const OzRows* __restrict_
   uint32_t packed[kS];
 #pragma unroll
   for (int a = 0; a < kS; ++a) packed[a] = 0u;
+  if (S.f64) {
+    const double* p = static_cast<const double*>(S.x) + (long long)row * S.ld + k4;
+    double v[4];
+    if (k4 + 3 < S.K && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+      const double2 a = *reinterpret_cast<const double2*>(p);
+      const double2 b = *reinterpret_cast<const double2*>(p + 2);
+      v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+    } else {
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const int k = k4 + u;
-    if (k < S.K) {
-      if (S.f64) {
-        double v = static_cast<const double*>(S.x)[(long long)row * S.ld + k] * inv * 64.0;
-#pragma unroll
-        for (int a = 0; a < kS; ++a) {
-          const double d = rint(v);
-          v = (v - d) * 128.0;
-          packed[a] |= (uint32_t)(uint8_t)(signed char)(int)d << (8 * u);
-        }
-      } else {
-        float v = __ldg(static_cast<const float*>(S.x) + (long long)row * S.ld + k) *
-                  (float)inv * 64.0f;
-#pragma unroll
-        for (int a = 0; a < kS; ++a) {
-          const float d = rintf(v);
-          v = (v - d) * 128.0f;
-          packed[a] |= (uint32_t)(uint8_t)(signed char)(int)d << (8 * u);
-        }
-      }
+      for (int u = 0; u < 4; ++u) v[u] = k4 + u < S.K ? p[u] : 0.0;
     }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = v[u] * inv * 64.0;
+    oz_digits4(v, packed);
+  } else {
+    const float* p = static_cast<const float*>(S.x) + (long long)row * S.ld + k4;
+    float v[4];
+    if (k4 + 3 < S.K && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+      const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = k4 + u < S.K ? __ldg(p + u) : 0.0f;
+    }
+    const float finv = (float)inv;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = v[u] * finv * 64.0f;
+    oz_digits4(v, packed);
   }
 #pragma unroll
   for (int a = 0; a < kS; ++a)
@@ -555,8 +668,9 @@ PlaneSet slice_cols(Ctx& ctx, std::vector<OzLeaf>& src, long long kpad) {
   ctx.check_launch("k_oz_colmax");
   ctx.launch_begin();
   ctx.pending_bytes = (4.0 + kS) * elems;
-  k_oz_split<<<dim3((unsigned)(kpad / 128), max_qp / 32, nl), 256, 0, ctx.stream>>>(
-      dl, ps.planes, kpad, ps.plane_rows);
+  k_oz_split<<<dim3((unsigned)(ceil_div((int)(kpad / 128), 32) * 32 * (max_qp / 32)), 1, nl), 256, 0,
+               ctx.stream>>>(
+      dl, ps.planes, kpad, ps.plane_rows, max_qp / 32);
   ctx.check_launch("k_oz_split");
   ps.map = make_map(ps.planes, kpad, kS * ps.plane_rows);
   return ps;

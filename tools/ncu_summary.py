@@ -28,28 +28,50 @@ def short(name):
     return (m.group(1) + (m.group(2) or "")) if m else name[:60]
 
 
+UNIT = {"ns": 1.0, "us": 1e3, "ms": 1e6, "s": 1e9, "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6,
+        "Gbyte": 1e9, "Tbyte": 1e12}
+
+
 def launches(path):
+    """Launch list of one command: per kernel the launches, the summed
+    gpu__time_duration and, when the pass also collected them, the summed
+    dram__bytes_read/write (-> average DRAM bytes per launch)."""
     rows = [r for r in csv.reader(l for l in open(path) if l.startswith('"'))]
     h = rows[0]
-    iname, ival = h.index("Kernel Name"), h.index("Metric Value")
+    iname, ival, imet, iunit, iid = (h.index("Kernel Name"), h.index("Metric Value"),
+                                     h.index("Metric Name"), h.index("Metric Unit"), h.index("ID"))
     agg = collections.OrderedDict()
     other = 0.0
+    seen = set()
     for r in rows[1:]:
-        ns = float(r[ival].replace(",", ""))
-        if "hsvdcu" not in r[iname] and "unnamed>::k_" not in r[iname]:
-            other += ns
-            continue
-        k = short(r[iname])
-        c, t = agg.get(k, (0, 0.0))
-        agg[k] = (c + 1, t + ns)
-    tot = sum(t for _, t in agg.values())
-    print("| kernel | launches | total ms | share of library time |")
-    print("|---|---|---|---|")
-    for k, (c, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
-        print(f"| `{k}` | {c} | {t / 1e6:.3f} | {100 * t / tot:.1f}% |")
-    print(f"\nlibrary kernels total {tot / 1e6:.1f} ms; non-library (torch input generation) "
-          f"{other / 1e6:.1f} ms.  ncu per-launch times are serialised and cold-cache: compare "
-          f"shares, not absolutes.")
+        v = float(r[ival].replace(",", "")) * UNIT.get(r[iunit], 1.0)
+        lib = "hsvdcu" in r[iname] or "unnamed>::k_" in r[iname]
+        if r[imet].startswith("gpu__time_duration"):
+            if not lib:
+                other += v
+                continue
+            k = short(r[iname])
+            a = agg.setdefault(k, [0, 0.0, 0.0, 0.0])
+            a[1] += v
+            if r[iid] not in seen:
+                seen.add(r[iid])
+                a[0] += 1
+        elif lib and r[imet].startswith("dram__bytes"):
+            a = agg.setdefault(short(r[iname]), [0, 0.0, 0.0, 0.0])
+            a[2 if "read" in r[imet] else 3] += v
+    tot = sum(a[1] for a in agg.values())
+    traffic = any(a[2] + a[3] > 0 for a in agg.values())
+    print("| kernel | launches | total ms | share of library time |"
+          + (" DRAM read GB | DRAM written GB | DRAM GB/s |" if traffic else ""))
+    print("|---|---|---|---|" + ("---|---|---|" if traffic else ""))
+    for k, a in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+        line = f"| `{k}` | {a[0]} | {a[1] / 1e6:.3f} | {100 * a[1] / tot:.1f}% |"
+        if traffic:
+            line += f" {a[2] / 1e9:.2f} | {a[3] / 1e9:.2f} | {(a[2] + a[3]) / max(a[1], 1.0):.0f} |"
+        print(line)
+    print(f"\nlibrary kernels total {tot / 1e6:.1f} ms; non-library (torch input generation, "
+          f"peak probes) {other / 1e6:.1f} ms.  ncu per-launch times are serialised and "
+          f"cold-cache: compare shares, not absolutes.")
 
 
 def full(paths):
