@@ -4,6 +4,9 @@
 // inverse iteration on the tridiagonal pushed through the chase reflectors
 // (k_q2_tbuild + k_q2_wy, blocked on DMMA) or, when forced, by inverse iteration on the band itself;
 // then back through the stage-1 reflectors (syev.cu back_transform).
+#include <map>
+#include <mutex>
+
 #include "syev_impl.cuh"
 #include "ozaki.h"
 
@@ -1346,13 +1349,45 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
   SubPhase sp2(ctx, "tri");
   ctx.launch_begin();
   // spread each matrix's sweeps over a cluster while SMs would idle
+  // (profiles/r02_chase_cs.json: 2 CTAs per matrix while every cluster is
+  // resident at once, 4 for the small batches of a multi-GPU rank -- 32
+  // Grams of order 4096: 140 / 91 / 58 ms with 1 / 2 / 4 -- as long as the
+  // device can hold all 4-CTA clusters together (37 matrices: 39 -> 61 ms
+  // when it cannot); 8 gains nothing over 4.  Same bits for every size.)
+  const size_t chase_smem = (size_t)CHASE_WARPS * B2 * LDBB * sizeof(double);
   int ccs = 1;
-  while (ccs < 2 && count * ccs * 2 <= ctx.num_sms) ccs *= 2;  // 4 measured slower
+  if (count * 2 * 2 <= ctx.num_sms) ccs = 2;
+  if (count * 4 <= ctx.num_sms) {
+    static std::mutex mu;
+    static std::map<int, int> cache;  // device -> co-resident 4-CTA clusters
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(ctx.device);
+    if (it == cache.end()) {
+      smem_optin(k_chase<true>, chase_smem);
+      cudaLaunchConfig_t qc = {};
+      qc.gridDim = dim3(4 * ctx.num_sms);
+      qc.blockDim = dim3(CHASE_WARPS * 32);
+      qc.dynamicSmemBytes = chase_smem;
+      cudaLaunchAttribute qa[1];
+      qa[0].id = cudaLaunchAttributeClusterDimension;
+      qa[0].val.clusterDim.x = 4;
+      qa[0].val.clusterDim.y = 1;
+      qa[0].val.clusterDim.z = 1;
+      qc.attrs = qa;
+      qc.numAttrs = 1;
+      int nc = 0;
+      if (cudaOccupancyMaxActiveClusters(&nc, k_chase<true>, &qc) != cudaSuccess) {
+        (void)cudaGetLastError();
+        nc = 0;
+      }
+      it = cache.emplace(ctx.device, nc).first;
+    }
+    if (count <= it->second) ccs = 4;
+  }
   if (const char* env = std::getenv("HSVD_CHASE_CS")) ccs = std::max(1, std::atoi(env));
   // (An L2 persisting access-policy window over the contiguous bands was
   // measured in round 2: no change at config 2, 388 -> 675 ms at config 5,
   // where the 545 MB of bands exceed the persisting carve-out; not used.)
-  const size_t chase_smem = (size_t)CHASE_WARPS * B2 * LDBB * sizeof(double);
   if (ccs == 1) {
     smem_optin(k_chase<false>, chase_smem);
     k_chase<false><<<count, CHASE_WARPS * 32, chase_smem, ctx.stream>>>(dd, 1);

@@ -100,9 +100,9 @@ def test_n4096_q2_wy():
     _check_batch(a, lam, z, kk, tol_lam=1e-11, tol_res=1e-10)
 
 
-@pytest.mark.parametrize("cs", ["1", "2", "4"])
+@pytest.mark.parametrize("cs", ["1", "2", "4", "8"])
 def test_chase_cluster_sizes_repeat(cs, monkeypatch):
-    """The bulge chase with its sweeps on 1, 2 or 4 CTAs (2 and 4: the
+    """The bulge chase with its sweeps on 1, 2, 4 or 8 CTAs (2 and 4: the
     sweeps run closest together, so a dependency the step-ahead band copy
     missed shows up there first); three runs, each against LAPACK."""
     import paper_1710_02812_b200 as H
