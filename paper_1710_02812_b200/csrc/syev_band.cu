@@ -1356,7 +1356,7 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
   // when it cannot); 8 gains nothing over 4.  Same bits for every size.)
   const size_t chase_smem = (size_t)CHASE_WARPS * B2 * LDBB * sizeof(double);
   int ccs = 1;
-  if (count * 2 * 2 <= ctx.num_sms) ccs = 2;
+  if (count * 2 <= ctx.num_sms) ccs = 2;
   if (count * 4 <= ctx.num_sms) {
     static std::mutex mu;
     static std::map<int, int> cache;  // device -> co-resident 4-CTA clusters
