@@ -1140,7 +1140,7 @@ void launch_steig(Ctx& ctx, const EigDev* dd, int count, int nmax, int kkmax) {
 // panel's own vectors by k_gs_panel.  The cluster starts are read back to
 // plan that (one small device->host copy, only when kk >= kBigCluster); big
 // clusters are then marked as singletons for k_band_mgs.
-constexpr int kBigCluster = 192;
+constexpr int kBigClusterDefault = 96;  // measured: config 5 k_band_mgs 24.1 -> 11.0 + GEMMs (64 leaves) with 96..128 against 192
 constexpr int GS_PW = 64;
 
 void launch_band_mgs(Ctx& ctx, const EigDev* dd, const std::vector<EigDev>& dev) {
@@ -1152,6 +1152,8 @@ void launch_band_mgs(Ctx& ctx, const EigDev* dd, const std::vector<EigDev>& dev)
   std::vector<Big> big;
   int kkmax = 0;
   for (const EigDev& e : dev) kkmax = std::max(kkmax, e.kk);
+  int kBigCluster = kBigClusterDefault;
+  if (const char* env = std::getenv("HSVD_BIG_CLUSTER")) kBigCluster = std::max(GS_PW, std::atoi(env));
   if (kkmax >= kBigCluster) {
     std::vector<size_t> off(count + 1, 0);
     for (int g = 0; g < count; ++g) off[g + 1] = off[g] + dev[g].kk;
