@@ -82,6 +82,10 @@ void begin(hsvd_cu_ctx* ctx) {
   HSVD_CUDA(cudaSetDevice(ctx->c.device));
   ctx->c.nvtx_close();
   ctx->c.arena.reset();
+  // a call that failed between a side-stream fork and its join may have left
+  // side work queued: the new call's stream waits for it before reusing memory
+  ctx->c.side_join();
+  ctx->c.side_arena.reset();
   ++ctx->generation;
 }
 
@@ -530,7 +534,7 @@ int hsvd_cu_ctx_stream(hsvd_cu_ctx* ctx, void** stream) {
 
 int64_t hsvd_cu_launch_count(const hsvd_cu_ctx* ctx) { return ctx ? ctx->c.launches : 0; }
 int64_t hsvd_cu_arena_bytes(const hsvd_cu_ctx* ctx) {
-  return ctx ? (int64_t)ctx->c.arena.capacity() : 0;
+  return ctx ? (int64_t)(ctx->c.arena.capacity() + ctx->c.side_arena.capacity()) : 0;
 }
 
 int hsvd_cu_profile(hsvd_cu_ctx* ctx, int enable) {

@@ -6,6 +6,7 @@
 // then back through the stage-1 reflectors (syev.cu back_transform).
 #include <map>
 #include <mutex>
+#include <string>
 
 #include "syev_impl.cuh"
 #include "ozaki.h"
@@ -251,6 +252,94 @@ __device__ __forceinline__ unsigned long long prog_encode(int s, unsigned steps)
   return ((unsigned long long)(unsigned)(s + 1) << 32) | steps;
 }
 constexpr unsigned kSweepDone = 0x7fffffffu;
+
+// Fused W of a panel (round 2; replaces X = Y T, P1 = V^T X, M = T^T P1,
+// W = X - V M / 2 and the copy into WV: five launches and nine passes over
+// m x 32 arrays).  With Q = V^T Y (one grouped GEMM):
+//   W = Y T - 1/2 V (T^T Q T) = [Y | V] [T ; Mb],  Mb = -1/2 T^T (Q T).
+// k_wcoef forms Mb (one CTA per matrix), k_wapply streams Y and V once and
+// writes W into both pending-pair panels (VW's W slot and WV's).
+__global__ void __launch_bounds__(B2 * B2) k_wcoef(const EigDev* __restrict__ jobs, int p, int j0) {
+  const EigDev J = jobs[blockIdx.x];
+  if (j0 + B2 > J.n - 2) return;
+  __shared__ double Ts[B2][B2 + 1], Qs[B2][B2 + 1], Rs[B2][B2 + 1];
+  const int i = threadIdx.x % B2, j = threadIdx.x / B2;
+  const double* T = J.Tp + (long long)p * B2 * B2;
+  Ts[i][j] = T[i + j * B2];
+  Qs[i][j] = J.P1[i + j * B2];
+  __syncthreads();
+  double r = 0.0;
+#pragma unroll
+  for (int l = 0; l < B2; ++l) r += Qs[i][l] * Ts[l][j];  // (Q T)[i][j]
+  Rs[i][j] = r;
+  __syncthreads();
+  double mm = 0.0;
+#pragma unroll
+  for (int l = 0; l < B2; ++l) mm += Ts[l][i] * Rs[l][j];  // (T^T Q T)[i][j]
+  J.Mb[i + j * B2] = -0.5 * mm;
+}
+
+constexpr int WA_THREADS = 128;
+__global__ void __launch_bounds__(WA_THREADS) k_wapply(const EigDev* __restrict__ jobs, int p, int j0,
+                                                       int vcol) {
+  const EigDev J = jobs[blockIdx.y];
+  const int n = J.n, r0 = j0 + B2, tid = threadIdx.x;
+  if (r0 > n - 2) {  // no trailing matrix: W := 0 on the rows r0..n-1 (as k_copy_w)
+    if (blockIdx.x == 0)
+      for (int e = tid; e < max(0, n - r0) * B2; e += WA_THREADS) {
+        const int i = r0 + e % max(1, n - r0), t = e / max(1, n - r0);
+        J.WV[i + (long long)(vcol + t) * n] = 0.0;
+        J.VW[i + (long long)(vcol + B2 + t) * n] = 0.0;
+      }
+    return;
+  }
+  const int m = n - r0;
+  if (blockIdx.x * WA_THREADS >= m) return;
+  __shared__ __align__(16) double Cs[2 * B2][B2];  // rows c < 32: T[c][:]; c >= 32: Mb[c - 32][:]
+  const double* T = J.Tp + (long long)p * B2 * B2;
+  for (int e = tid; e < 2 * B2 * B2; e += WA_THREADS) {
+    const int c = e / B2, t = e % B2;
+    Cs[c][t] = c < B2 ? T[c + t * B2] : J.Mb[(c - B2) + t * B2];
+  }
+  __syncthreads();
+  const long long lda = J.lda;
+  for (int i = blockIdx.x * WA_THREADS + tid; i < m; i += gridDim.x * WA_THREADS) {
+    double acc[B2];
+#pragma unroll
+    for (int t = 0; t < B2; ++t) acc[t] = 0.0;
+    const double* y = J.Y + r0 + i;
+    const double* v = J.A + r0 + i + (long long)j0 * lda;
+#pragma unroll 4
+    for (int c = 0; c < B2; ++c) {
+      const double yc = y[(long long)c * n];
+      const double2* row = reinterpret_cast<const double2*>(Cs[c]);
+#pragma unroll
+      for (int t = 0; t < B2 / 2; ++t) {
+        const double2 w = row[t];
+        acc[2 * t] += yc * w.x;
+        acc[2 * t + 1] += yc * w.y;
+      }
+    }
+#pragma unroll 4
+    for (int c = 0; c < B2; ++c) {
+      const double vc = v[(long long)c * lda];
+      const double2* row = reinterpret_cast<const double2*>(Cs[B2 + c]);
+#pragma unroll
+      for (int t = 0; t < B2 / 2; ++t) {
+        const double2 w = row[t];
+        acc[2 * t] += vc * w.x;
+        acc[2 * t + 1] += vc * w.y;
+      }
+    }
+    double* w1 = J.VW + (r0 + i) + (long long)(vcol + B2) * n;
+    double* w2 = J.WV + (r0 + i) + (long long)vcol * n;
+#pragma unroll
+    for (int t = 0; t < B2; ++t) {
+      w1[(long long)t * n] = acc[t];
+      w2[(long long)t * n] = acc[t];
+    }
+  }
+}
 
 constexpr int CHASE_WARPS = 8;
 static_assert(B2 == 32, "k_chase maps one band row per lane");
@@ -1257,7 +1346,9 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
   // and one SYR2K with K = 64 * kBandGroup updates the trailing matrix at the
   // end of the group (a quarter of the passes over A22).
   SubPhase sp1(ctx, "band");
-  std::vector<GemmDesc> gc, g1, gz, gy, g2, g3, g4, g5, g6;
+  std::vector<GemmDesc> gc, g1, gz, gy, g2, g3, g4, g5, g6, gq;
+  // HSVD_BAND_W=gemm: the five-launch W (kept for A/B runs)
+  const bool fused_w = !(std::getenv("HSVD_BAND_W") && std::string(std::getenv("HSVD_BAND_W")) == "gemm");
   for (int p = 0; p < npan; ++p) {
     const int j0 = p * B2, r0 = j0 + B2;
     const int gi = p % kBandGroup;        // panel index inside its group
@@ -1277,6 +1368,7 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
     }
     launch_panel_qr(ctx, count, std::max(0, nmax - r0), dd, j0, vcol);
     g1.clear(); gz.clear(); gy.clear(); g2.clear(); g3.clear(); g4.clear(); g5.clear(); g6.clear();
+    gq.clear();
     for (int g = 0; g < count; ++g) {
       const EigDev& e = dev[g];
       const int n = e.n;
@@ -1293,6 +1385,7 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
       }
       g2.push_back({e.Y + r0, Tp, X, n, B2, n, m, B2, B2, 1.0, 0.0});               // X = Y T
       g3.push_back({V, X, e.P1, e.lda, n, B2, B2, B2, m, 1.0, 0.0});                // P1 = V^T X
+      gq.push_back({V, e.Y + r0, e.P1, e.lda, n, B2, B2, B2, m, 1.0, 0.0});         // Q = V^T Y (fused W)
       g4.push_back({Tp, e.P1, e.Mb, B2, B2, B2, B2, B2, B2, 1.0, 0.0});             // M = T^T P1
       g5.push_back({V, e.Mb, X, e.lda, B2, n, m, B2, B2, -0.5, 1.0});               // W = X - V M/2
       if (last_in_group)                                                             // syr2k
@@ -1314,13 +1407,30 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
     }
     {
       SubPhase sw(ctx, "band.w");
-      gemm_grouped(ctx, DType::F64, DType::F64, false, false, false, g2);
-      gemm_grouped(ctx, DType::F64, DType::F64, true, false, false, g3);
-      gemm_grouped(ctx, DType::F64, DType::F64, true, false, false, g4);
-      gemm_grouped(ctx, DType::F64, DType::F64, false, false, false, g5);
-      ctx.launch_begin();
-      k_copy_w<<<dim3(256, count), 256, 0, ctx.stream>>>(dd, j0, vcol);
-      ctx.check_launch("k_copy_w");
+      if (fused_w) {
+        // Q = V^T Y, Mb = -1/2 T^T Q T, W = Y T + V Mb into VW and WV
+        gemm_grouped(ctx, DType::F64, DType::F64, true, false, false, gq);
+        ctx.launch_begin();
+        k_wcoef<<<count, B2 * B2, 0, ctx.stream>>>(dd, p, j0);
+        ctx.check_launch("k_wcoef");
+        ctx.launch_begin();
+        {
+          double by = 0.0;  // Y and V read, W written twice
+          for (const GemmDesc& g : g1) by += 4.0 * 8.0 * g.M * B2;
+          ctx.pending_bytes = by;
+        }
+        k_wapply<<<dim3(std::max(1, std::min(ceil_div(std::max(0, nmax - r0), WA_THREADS), 64)), count),
+                   WA_THREADS, 0, ctx.stream>>>(dd, p, j0, vcol);
+        ctx.check_launch("k_wapply");
+      } else {
+        gemm_grouped(ctx, DType::F64, DType::F64, false, false, false, g2);
+        gemm_grouped(ctx, DType::F64, DType::F64, true, false, false, g3);
+        gemm_grouped(ctx, DType::F64, DType::F64, true, false, false, g4);
+        gemm_grouped(ctx, DType::F64, DType::F64, false, false, false, g5);
+        ctx.launch_begin();
+        k_copy_w<<<dim3(256, count), 256, 0, ctx.stream>>>(dd, j0, vcol);
+        ctx.check_launch("k_copy_w");
+      }
     }
     if (!g6.empty()) {
       SubPhase s2k(ctx, "band.syr2k");
