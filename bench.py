@@ -381,7 +381,7 @@ def load_traffic(workload):
         return {}
 
 
-def roofline(prof, steps, w, hbm_peak, fp64_peak):
+def roofline(prof, steps, w, hbm_peak, fp64_peak, prof_bytes=None):
     """Roofline of the kernel family with the largest share of the step.
     k_gemm (the grouped DMMA GEMM: Grams, projections, the two-stage band
     reduction and both back-transforms) is tensor-bound: achieved = its
@@ -403,6 +403,11 @@ def roofline(prof, steps, w, hbm_peak, fp64_peak):
                 "traffic": traffic, "traffic_unit": "bytes per launch",
                 "peak_source": "fp64 cuBLAS DGEMM 8192^3 measured in this run",
                 "algorithmic_flops_per_launch": fl / cnt, "avg_launch_ms": ms / cnt,
+                # operands read once + C written (read too when accumulated): what
+                # `traffic` (ncu DRAM bytes per launch) is to be compared with
+                "algorithmic_bytes_per_launch": (sum(
+                    b for k, b in (prof_bytes or {}).items()
+                    if k.rsplit(":", 1)[-1] in ("k_gemm", "k_gemm_sk")) / cnt) or None,
                 "launches_per_step": cnt / steps, "share": ms / sum(v[1] for v in fam.values())}
     if name == "k_latrd":
         nleaves, q = w.P * w.Q, min(w.c, w.d)
@@ -547,7 +552,7 @@ def run_ours(args, w):
     except Exception:
         pass
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    roof = roofline(prof, args.steps, w, hbm_peak, lambda: fp64_peak_tflops(torch, dev))
+    roof = roofline(prof, args.steps, w, hbm_peak, lambda: fp64_peak_tflops(torch, dev), prof_bytes)
     roof["measured"] = ("per-launch CUDA events over a second timed pass of the same K steps "
                         "(the headline pass runs without them)")
     roof["profiled_pass_ms_per_step"] = ms_prof

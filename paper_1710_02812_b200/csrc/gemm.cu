@@ -394,11 +394,17 @@ void gemm_grouped(Ctx& ctx, DType ta, DType tb, bool trans_a, bool trans_b, bool
   const int BMt = skinny ? 128 : 64, BNt = skinny ? 32 : 64;
   long long tiles = 0;
   double flops = 0.0;  // algorithmic (SYRK: the lower triangle)
+  double bytes = 0.0;
   for (const auto& d : live) {
     long long t = (long long)ceil_div(d.M, BMt) * ceil_div(d.N, BNt);
     if (syrk) t = (t + ceil_div(d.M, BMt)) / 2;
     tiles += t;
     flops += syrk ? (double)d.M * (d.M + 1) * d.K : 2.0 * d.M * d.N * d.K;
+    // algorithmic HBM bytes: each operand once (SYRK: op(A) only), C written
+    // (and read when beta != 0)
+    const double sa = ta == DType::F64 ? 8.0 : 4.0, sb = tb == DType::F64 ? 8.0 : 4.0;
+    bytes += sa * d.M * d.K + (syrk ? 0.0 : sb * d.K * d.N) +
+             8.0 * d.M * d.N * (d.beta != 0.0 ? 2.0 : 1.0);
   }
 
   const long long slots = (long long)ctx.num_sms * occupancy(ta, tb, trans_a, trans_b, skinny);
@@ -420,6 +426,7 @@ void gemm_grouped(Ctx& ctx, DType ta, DType tb, bool trans_a, bool trans_b, bool
   }
   const int mode = (syrk ? kModeSyrk : 0) | ((flags & kGemmLowerOnly) ? kModeLower : 0);
   ctx.pending_flops = flops;
+  ctx.pending_bytes = bytes;
   if (ta == DType::F64 && tb == DType::F64)
     launch_typed<double, double>(ctx, trans_a, trans_b, skinny, maxM, maxN, count, dd, mode,
                                  splits, ws, slot, pack);

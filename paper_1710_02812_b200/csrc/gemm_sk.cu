@@ -163,15 +163,17 @@ bool gemm_sk_applicable(const std::vector<GemmDesc>& descs, int num_sms) {
 
 void gemm_sk(Ctx& ctx, const std::vector<GemmDesc>& descs) {
   int maxM = 0;
-  double flops = 0.0;
+  double flops = 0.0, bytes = 0.0;  // algorithmic flops and HBM bytes (profile)
   for (const GemmDesc& d : descs) {
     maxM = std::max(maxM, d.M);
     flops += 2.0 * d.M * d.N * d.K;
+    bytes += 8.0 * ((double)d.M * d.K + (double)d.K * d.N + (double)d.M * d.N * (d.beta != 0.0 ? 2.0 : 1.0));
   }
   const GemmDesc* dd = static_cast<const GemmDesc*>(
       ctx.staging.put(descs.data(), descs.size() * sizeof(GemmDesc), ctx.stream));
   smem_optin(k_gemm_sk, SK_SMEM);
   ctx.pending_flops = flops;
+  ctx.pending_bytes = bytes;
   ctx.launch_begin();
   k_gemm_sk<<<dim3(ceil_div(maxM, SK_BM), (unsigned)descs.size()), SK_THREADS, SK_SMEM, ctx.stream>>>(dd);
   ctx.check_launch("k_gemm_sk");

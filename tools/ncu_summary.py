@@ -2,6 +2,10 @@
 metrics of the top kernels).  Usage:
   python tools/ncu_summary.py launches <launches.csv> > profiles/..._launches.md
   python tools/ncu_summary.py full <report.ncu-rep> [...] > profiles/..._full.md
+  python tools/ncu_summary.py traffic <launches.csv> <workload> <passes> [profiles/traffic.json]
+    (DRAM bytes per launch of the DMMA GEMM family from a launch list that
+    also collected dram__bytes_read/write.sum; `passes` = rank-k HSVD steps in
+    the profiled command; what bench.py's roofline.traffic reads)
 """
 import collections
 import csv
@@ -91,8 +95,41 @@ def full(paths):
             print()
 
 
+def traffic(path, workload, passes, out):
+    import json
+    rows = [r for r in csv.reader(l for l in open(path) if l.startswith('"'))]
+    h = rows[0]
+    iname, ival, imet, iunit, iid = (h.index("Kernel Name"), h.index("Metric Value"),
+                                     h.index("Metric Name"), h.index("Metric Unit"), h.index("ID"))
+    ids, byts = set(), 0.0
+    for r in rows[1:]:
+        k = short(r[iname])
+        if not (k.startswith("k_gemm<") or k == "k_gemm" or k == "k_gemm_sk"):
+            continue
+        ids.add(r[iid])
+        if r[imet].startswith("dram__bytes"):
+            byts += float(r[ival].replace(",", "")) * UNIT.get(r[iunit], 1.0)
+    try:
+        data = json.load(open(out))
+    except Exception:
+        data = {}
+    data[workload] = {
+        "k_gemm": byts / max(1, len(ids)),
+        "_source": f"ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum over {passes} rank-k "
+                   f"HSVD steps of bench.py ({len(ids)} launches of k_gemm + k_gemm_sk, "
+                   f"{byts / 1e9:.1f} GB read + written); {path.split('/')[-1]}",
+        "launches_per_step": len(ids) / passes,
+    }
+    with open(out, "w") as f:
+        json.dump(data, f, indent=1)
+    print(json.dumps(data[workload]))
+
+
 if __name__ == "__main__":
-    if sys.argv[1] == "launches":
+    if sys.argv[1] == "traffic":
+        traffic(sys.argv[2], sys.argv[3], int(sys.argv[4]),
+                sys.argv[5] if len(sys.argv) > 5 else "profiles/traffic.json")
+    elif sys.argv[1] == "launches":
         launches(sys.argv[2])
     else:
         full(sys.argv[2:])
