@@ -280,6 +280,18 @@ __global__ void __launch_bounds__(B2 * B2) k_wcoef(const EigDev* __restrict__ jo
 }
 
 constexpr int WA_THREADS = 128;
+__device__ __forceinline__ void dmma_w(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+// W = [Y | V] [T ; Mb] on DMMA: a warp owns 32 rows x 32 columns (K = 64);
+// the 64 x 32 coefficient matrix stays in registers as B fragments for the
+// whole kernel (64 doubles per lane), the A fragments come straight from
+// global memory (8 rows x 4 columns per load: whole 32-byte sectors), so the
+// kernel streams Y and V once and writes W twice with no shared-memory
+// traffic.  (A CUDA-core version with the coefficients broadcast from shared
+// memory was bound by the LDS return path: 30 ms at config 5.)
 __global__ void __launch_bounds__(WA_THREADS) k_wapply(const EigDev* __restrict__ jobs, int p, int j0,
                                                        int vcol) {
   const EigDev J = jobs[blockIdx.y];
@@ -294,49 +306,59 @@ __global__ void __launch_bounds__(WA_THREADS) k_wapply(const EigDev* __restrict_
     return;
   }
   const int m = n - r0;
-  if (blockIdx.x * WA_THREADS >= m) return;
-  __shared__ __align__(16) double Cs[2 * B2][B2];  // rows c < 32: T[c][:]; c >= 32: Mb[c - 32][:]
+  const int lane = tid & 31, warp = tid >> 5, grp = lane >> 2, tig = lane & 3;
+  constexpr int NW = WA_THREADS / 32;
+  if ((blockIdx.x * NW + warp) * 32 >= m) return;
+  // B fragments: b[ks][j] = C[4 ks + tig][8 j + grp], C = [T ; Mb] (column-major 32 x 32 each)
   const double* T = J.Tp + (long long)p * B2 * B2;
-  for (int e = tid; e < 2 * B2 * B2; e += WA_THREADS) {
-    const int c = e / B2, t = e % B2;
-    Cs[c][t] = c < B2 ? T[c + t * B2] : J.Mb[(c - B2) + t * B2];
-  }
-  __syncthreads();
+  double bf[16][4];
+#pragma unroll
+  for (int ks = 0; ks < 16; ++ks)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = 4 * ks + tig, t = 8 * j + grp;
+      bf[ks][j] = c < B2 ? T[c + t * B2] : J.Mb[(c - B2) + t * B2];
+    }
   const long long lda = J.lda;
-  for (int i = blockIdx.x * WA_THREADS + tid; i < m; i += gridDim.x * WA_THREADS) {
-    double acc[B2];
+  // 16 rows per pass (two passes per 32-row block: the B fragments take 128
+  // registers, so the accumulators stay at 16 doubles)
+  for (int i0 = (blockIdx.x * NW + warp) * 32; i0 < m; i0 += gridDim.x * NW * 32) {
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+      const int ib = i0 + 16 * h;
+      if (ib >= m) break;
+      double acc[2][4][2];
 #pragma unroll
-    for (int t = 0; t < B2; ++t) acc[t] = 0.0;
-    const double* y = J.Y + r0 + i;
-    const double* v = J.A + r0 + i + (long long)j0 * lda;
-#pragma unroll 4
-    for (int c = 0; c < B2; ++c) {
-      const double yc = y[(long long)c * n];
-      const double2* row = reinterpret_cast<const double2*>(Cs[c]);
+      for (int i = 0; i < 2; ++i)
 #pragma unroll
-      for (int t = 0; t < B2 / 2; ++t) {
-        const double2 w = row[t];
-        acc[2 * t] += yc * w.x;
-        acc[2 * t + 1] += yc * w.y;
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      const double* y = J.Y + r0 + ib + grp;
+      const double* v = J.A + r0 + ib + grp + (long long)j0 * lda;
+      const bool ok0 = ib + grp < m, ok1 = ib + 8 + grp < m;
+#pragma unroll
+      for (int ks = 0; ks < 16; ++ks) {
+        const int c = (4 * ks + tig) & (B2 - 1);
+        const double* src = ks < 8 ? y + (long long)c * n : v + (long long)c * lda;
+        const double a0 = ok0 ? src[0] : 0.0, a1 = ok1 ? src[8] : 0.0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          dmma_w(acc[0][j], a0, bf[ks][j]);
+          dmma_w(acc[1][j], a1, bf[ks][j]);
+        }
       }
-    }
-#pragma unroll 4
-    for (int c = 0; c < B2; ++c) {
-      const double vc = v[(long long)c * lda];
-      const double2* row = reinterpret_cast<const double2*>(Cs[B2 + c]);
 #pragma unroll
-      for (int t = 0; t < B2 / 2; ++t) {
-        const double2 w = row[t];
-        acc[2 * t] += vc * w.x;
-        acc[2 * t + 1] += vc * w.y;
+      for (int i = 0; i < 2; ++i) {
+        const int row = ib + 8 * i + grp;
+        if (row >= m) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            const int t = 8 * j + 2 * tig + r;
+            J.VW[(r0 + row) + (long long)(vcol + B2 + t) * n] = acc[i][j][r];
+            J.WV[(r0 + row) + (long long)(vcol + t) * n] = acc[i][j][r];
+          }
       }
-    }
-    double* w1 = J.VW + (r0 + i) + (long long)(vcol + B2) * n;
-    double* w2 = J.WV + (r0 + i) + (long long)vcol * n;
-#pragma unroll
-    for (int t = 0; t < B2; ++t) {
-      w1[(long long)t * n] = acc[t];
-      w2[(long long)t * n] = acc[t];
     }
   }
 }
