@@ -358,11 +358,15 @@ def streaming_roofline(prof, prof_bytes, hbm_peak):
                         for k, (c, m, b) in sorted(per.items(), key=lambda t: -t[1][1])}}
 
 
-def kernel_families(prof):
+def kernel_families(prof, with_overlapped=False):
     """{kernel name: (launches, ms, flops)} summed over phases (the grouped
     DMMA GEMM and its bulk-copy-fed skinny variant form one family)."""
     fam = {}
     for key, (cnt, ms, fl) in prof.items():
+        if "/back.prep:" in key and not with_overlapped:
+            # launched on the side stream under the bulge chase: their event
+            # times include sharing the GPU, so they stay out of the rooflines
+            continue
         k = key.rsplit(":", 1)[-1]
         if k == "k_gemm_sk":
             k = "k_gemm"
@@ -393,7 +397,9 @@ def roofline(prof, steps, w, hbm_peak, fp64_peak, prof_bytes=None):
     cnt, ms, fl = fam[name]
     meas = load_traffic(w.name)
     # a committed measurement applies only to the same launch mix
-    traffic = meas.get(name) if meas.get("launches_per_step") == cnt / steps else None
+    # (the ncu launch list counts every launch of the family, overlapped ones too)
+    cnt_all = kernel_families(prof, True)[name][0]
+    traffic = meas.get(name) if meas.get("launches_per_step") == cnt_all / steps else None
     if name == "k_gemm" and fl > 0:
         peak = fp64_peak()
         achieved = fl / (ms / 1000.0) / 1e12
@@ -407,7 +413,10 @@ def roofline(prof, steps, w, hbm_peak, fp64_peak, prof_bytes=None):
                 # `traffic` (ncu DRAM bytes per launch) is to be compared with
                 "algorithmic_bytes_per_launch": (sum(
                     b for k, b in (prof_bytes or {}).items()
-                    if k.rsplit(":", 1)[-1] in ("k_gemm", "k_gemm_sk")) / cnt) or None,
+                    if k.rsplit(":", 1)[-1] in ("k_gemm", "k_gemm_sk")
+                    and "/back.prep:" not in k) / cnt) or None,
+                "excluded": "the reflector-only GEMMs overlapped with the bulge chase on the "
+                            "side stream (profile keys */back.prep:*)",
                 "launches_per_step": cnt / steps, "share": ms / sum(v[1] for v in fam.values())}
     if name == "k_latrd":
         nleaves, q = w.P * w.Q, min(w.c, w.d)

@@ -1474,7 +1474,7 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
   const bool side = !(std::getenv("HSVD_NO_SIDE") && std::atoi(std::getenv("HSVD_NO_SIDE")) != 0);
   if (side) {
     SideScope ss(ctx);
-    SubPhase spb(ctx, "back");
+    SubPhase spb(ctx, "back.prep");  // profile key of the overlapped launches
     back_prepare(ctx, dev, dd, nmax, B2);
   }
   // stage 2: band -> tridiagonal (values), eigenvalues by bisection
