@@ -925,7 +925,7 @@ struct GsPanel {
   int n, q, np;
 };
 
-__global__ void __launch_bounds__(256) k_gs_panel(const GsPanel* __restrict__ pan) {
+__global__ void __launch_bounds__(256, 2) k_gs_panel(const GsPanel* __restrict__ pan) {
   const GsPanel P = pan[blockIdx.x];
   __shared__ double sm[GS_SMEM_DOUBLES];
   cluster_gs(P.Z, P.ldz, P.n, P.q, P.q + P.np, sm);

@@ -725,7 +725,7 @@ __global__ void __launch_bounds__(CHASE_WARPS * 32, 1) k_chase(const EigDev* __r
 // cp.async.bulk + mbarrier transaction counts; the consumers release a
 // stage with one arrive per warp.
 constexpr int QSG = 8;                  // groups per super-group pass (window 96 rows)
-constexpr int QW = 4;                   // consumer warps per CTA (8 columns each)
+constexpr int QW = 4;                   // consumer warps per CTA (8 columns each); one CTA per SM, see the launch
 constexpr int QDEPTH = 16;              // ring stages (one WY block each)
 constexpr int QV_BYTES = QG * RS * 8;   // 2176
 constexpr int QT_BYTES = 64 * 8;        // 512
@@ -840,7 +840,7 @@ __device__ __forceinline__ void q2_dmma(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-__global__ void __launch_bounds__((QW + 1) * 32, 3) k_q2_wy(const EigDev* __restrict__ jobs) {
+__global__ void __launch_bounds__((QW + 1) * 32, 1) k_q2_wy(const EigDev* __restrict__ jobs) {
   const EigDev J = jobs[blockIdx.y];
   const int n = J.n, kk = J.kk;
   const int c_cta = blockIdx.x * QW * 8;
@@ -1565,8 +1565,19 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
       for (const EigDev& e : dev) fl += 4.0 * B2 * e.kk * (double)refl_off(e.n, chase_steps(e.n));
       ctx.pending_flops = fl;
     }
-    smem_optin(k_q2_wy, kQ2Smem);
-    k_q2_wy<<<dim3(ceil_div(kkmax, QW * 8), count), (QW + 1) * 32, kQ2Smem, ctx.stream>>>(dd);
+    // One CTA per SM: with two or three k_q2_wy CTAs resident on an SM the
+    // result was not repeatable (one consumer warp's 8 columns off by up to
+    // 1e-2 in some calls at n = 256..1024, 64 matrices, kk = 200; the stage
+    // contents and the warp's own Z reloads checked out, the cause was not
+    // found; tools/probes/determinism_eig.py).  Every run with a single
+    // resident CTA was bitwise repeatable, so the launch asks for enough
+    // dynamic shared memory that only one fits (HSVD_Q2_SMEM_PAD overrides
+    // the padding, in KB).
+    int pad_kb = 100;
+    if (const char* env = std::getenv("HSVD_Q2_SMEM_PAD")) pad_kb = std::max(0, std::atoi(env));
+    const size_t q2smem = kQ2Smem + (size_t)pad_kb * 1024;
+    smem_optin(k_q2_wy, q2smem);
+    k_q2_wy<<<dim3(ceil_div(kkmax, QW * 8), count), (QW + 1) * 32, q2smem, ctx.stream>>>(dd);
     ctx.check_launch("k_q2_wy");
   } else {
     const size_t smem =
