@@ -725,7 +725,8 @@ __global__ void __launch_bounds__(CHASE_WARPS * 32, 1) k_chase(const EigDev* __r
 // cp.async.bulk + mbarrier transaction counts; the consumers release a
 // stage with one arrive per warp.
 constexpr int QSG = 8;                  // groups per super-group pass (window 96 rows)
-constexpr int QW = 4;                   // consumer warps per CTA (8 columns each); one CTA per SM, see the launch
+constexpr int QW = 4;                   // consumer warps per CTA (8 columns each), small batches
+constexpr int QWMAX = 13;               // ... large batches (one CTA per SM; 104 columns per CTA)
 constexpr int QDEPTH = 16;              // ring stages (one WY block each)
 constexpr int QV_BYTES = QG * RS * 8;   // 2176
 constexpr int QT_BYTES = 64 * 8;        // 512
@@ -840,12 +841,12 @@ __device__ __forceinline__ void q2_dmma(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-__global__ void __launch_bounds__((QW + 1) * 32, 1) k_q2_wy(const EigDev* __restrict__ jobs) {
+__global__ void __launch_bounds__((QWMAX + 1) * 32, 1) k_q2_wy(const EigDev* __restrict__ jobs, int qw) {
   const EigDev J = jobs[blockIdx.y];
   const int n = J.n, kk = J.kk;
-  const int c_cta = blockIdx.x * QW * 8;
+  const int c_cta = blockIdx.x * qw * 8;
   if (n < 3 || c_cta >= kk) return;
-  const int nwork = min(QW, (kk - c_cta + 7) / 8);  // consumer warps with columns
+  const int nwork = min(qw, (kk - c_cta + 7) / 8);  // consumer warps with columns
   extern __shared__ __align__(128) unsigned char q2s[];
   uint64_t* full = reinterpret_cast<uint64_t*>(q2s);
   uint64_t* empty = full + QDEPTH;
@@ -944,14 +945,22 @@ __global__ void __launch_bounds__((QW + 1) * 32, 1) k_q2_wy(const EigDev* __rest
         if (b * QSG + g >= Ak) continue;
         const int slot = it % QDEPTH;
         q2_mbar_wait(full + slot, (it / QDEPTH) & 1);
-        const double* sv = reinterpret_cast<const double*>(stages + (size_t)slot * QSTAGE);
-        const double2 tf = reinterpret_cast<const double2*>(sv + QV_BYTES / 8)[lane];
+        // Operands from global memory (L2: the producer's bulk copy of this
+        // block into the ring has just completed); the shared-memory copy is
+        // not read -- see the note at the launch.
+        const int a_ = b * QSG + g;
+        const int jmin_ = a_ == 0 ? 1 : 0;
+        const int sfirst_ = QG * a_ - 1 + jmin_;
+        const int jmax_ = min(QG * a_ + QG - 2, n - 3 - B2 * k) - sfirst_ + jmin_;
+        const double* sv = J.refl + (refl_off(n, k) + sfirst_ - jmin_) * RS;  // row j <-> sweep sfirst_ - jmin_ + j
+        const double2 tf = reinterpret_cast<const double2*>(J.q2T + (tblk_off(n, k) + a_) * 64)[lane];
+#define SVROW(j, e) (((j) >= jmin_ && (j) <= jmax_) ? __ldg(sv + (j) * RS + (e)) : 0.0)
         // W^T = Z_w^T V: k-step kt covers window rows 8(kt/2) + 2q + (kt&1)
         double w0[2] = {0.0, 0.0}, w1[2] = {0.0, 0.0};
 #pragma unroll
         for (int kt = 0; kt < 10; ++kt) {
           const int e = 8 * (kt >> 1) + 2 * q + (kt & 1) - j1;
-          const double bv = (e >= 0 && e < B2) ? sv[j1 * RS + e] : 0.0;
+          const double bv = (e >= 0 && e < B2) ? SVROW(j1, e) : 0.0;
           if (kt & 1) q2_dmma(w1, z[g + (kt >> 1)][1], bv);
           else q2_dmma(w0, z[g + (kt >> 1)][0], bv);
         }
@@ -962,7 +971,7 @@ __global__ void __launch_bounds__((QW + 1) * 32, 1) k_q2_wy(const EigDev* __rest
 #pragma unroll
           for (int kt = 0; kt < 2; ++kt) {
             const int j3 = 2 * q + kt, e = 8 * nt + j1 - j3;
-            vb[nt][kt] = (e >= 0 && e < B2) ? sv[j3 * RS + e] : 0.0;
+            vb[nt][kt] = (e >= 0 && e < B2) ? SVROW(j3, e) : 0.0;
           }
         __syncwarp();
         if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(empty + slot)) : "memory");
@@ -1565,19 +1574,27 @@ void two_stage(Ctx& ctx, const std::vector<EigJob>& jobs, std::vector<EigDev>& d
       for (const EigDev& e : dev) fl += 4.0 * B2 * e.kk * (double)refl_off(e.n, chase_steps(e.n));
       ctx.pending_flops = fl;
     }
-    // One CTA per SM: with two or three k_q2_wy CTAs resident on an SM the
-    // result was not repeatable (one consumer warp's 8 columns off by up to
-    // 1e-2 in some calls at n = 256..1024, 64 matrices, kk = 200; the stage
-    // contents and the warp's own Z reloads checked out, the cause was not
-    // found; tools/probes/determinism_eig.py).  Every run with a single
-    // resident CTA was bitwise repeatable, so the launch asks for enough
-    // dynamic shared memory that only one fits (HSVD_Q2_SMEM_PAD overrides
-    // the padding, in KB).
-    int pad_kb = 100;
-    if (const char* env = std::getenv("HSVD_Q2_SMEM_PAD")) pad_kb = std::max(0, std::atoi(env));
-    const size_t q2smem = kQ2Smem + (size_t)pad_kb * 1024;
-    smem_optin(k_q2_wy, q2smem);
-    k_q2_wy<<<dim3(ceil_div(kkmax, QW * 8), count), (QW + 1) * 32, q2smem, ctx.stream>>>(dd);
+    // The consumers take the V and T operands of a block from GLOBAL memory
+    // (L2, right after the producer's bulk copy of that block into the ring
+    // completed: the ring now only paces the consumers and warms L2).  Read
+    // from the shared-memory ring, the result was not repeatable once more
+    // than four consumer warps shared an SM (three 4-warp CTAs, or one
+    // 13-warp CTA): in some calls one warp's 8 columns came out off by up to
+    // 1e-2 at n = 256..1024 with 64 matrices and kk = 200, although the
+    // stage contents checked equal to their global source right after the
+    // mbarrier wait and the ring protocol allows no early overwrite; masking
+    // the never-written rows of partial blocks reduced but did not remove it;
+    // the cause was not found (tools/probes/determinism_eig.py, DESIGN 8).
+    // With the operands read from global memory the consumers do not depend
+    // on shared-memory contents at all, so the result is repeatable by
+    // construction; tests/test_gpu_eig.py::test_two_stage_band_back_transform_repeatable.
+    // Large batches use 13 consumer warps per CTA (one CTA per SM), small
+    // ones 4 (three CTAs per SM) to spread a matrix over more SMs.
+    const int kk8 = ceil_div(kkmax, 8);
+    int qw = (long long)count * ceil_div(kk8, QWMAX) >= ctx.num_sms ? QWMAX : QW;
+    if (const char* env = std::getenv("HSVD_Q2_QW")) qw = std::max(1, std::min(QWMAX, std::atoi(env)));
+    smem_optin(k_q2_wy, kQ2Smem);
+    k_q2_wy<<<dim3(ceil_div(kkmax, qw * 8), count), (qw + 1) * 32, kQ2Smem, ctx.stream>>>(dd, qw);
     ctx.check_launch("k_q2_wy");
   } else {
     const size_t smem =
