@@ -134,7 +134,8 @@ def test_two_stage_band_back_transform_repeatable(monkeypatch):
     order 256, top 200: seven k_q2_wy CTAs per matrix).  With several of those
     CTAs resident on one SM the result was not repeatable from call to call
     (one consumer warp's 8 columns off by up to 1e-2; found late in round 2,
-    tools/probes/determinism_eig.py); the launch now keeps one CTA per SM.
+    tools/probes/determinism_eig.py); the consumers now take their operands
+    from global memory instead of the shared-memory ring (DESIGN 2.2).
     Every call must give the first call's bits, and accurate eigenpairs."""
     import paper_1710_02812_b200 as H
     monkeypatch.setenv("HSVD_TWO_STAGE_MIN_N", "1")
